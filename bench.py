@@ -1,0 +1,387 @@
+"""RSOC graph-coloring benchmark on B200 (driver contract: one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config tri]
+    python bench.py --impl reference ...   # the reference's own CPU RSOC
+
+A step = one full RSOC coloring (initial tentative pass + fused
+detect-and-recolor rounds until no conflict) of the configuration's graph.
+`value` = directed adjacency entries m / mean device coloring time, in
+GE/s, with the CSR already resident in HBM; `e2e` = the same metric through
+the public C ABI with host buffers (CSR upload + colours download inside the
+timed region).  Default workload: BASELINE.json configs[1] (2000x2000
+triangular mesh); --config er|tri|stencil|rmat24 selects the others.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIG_WORKLOAD = {
+    "er": "BASELINE configs[0]: Erdos-Renyi n=1,000,000 avg degree 16, ids random",
+    "tri": "BASELINE configs[1]: 2D triangular mesh 2000x2000, ids permuted",
+    "stencil": "BASELINE configs[2]: 3D 27-point stencil 200^3, ids permuted",
+    "rmat24": "BASELINE configs[3]: R-MAT scale 24 ef 16 (.57,.19,.19,.05), ids permuted",
+    "rmat27": "BASELINE configs[4]: R-MAT scale 27 ef 16 (.57,.19,.19,.05), ids permuted",
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="tri", choices=sorted(CONFIG_WORKLOAD))
+    p.add_argument("--priority", default="id_low", choices=["id_low", "id_high", "degree_id"])
+    p.add_argument("--k1-blocks-per-sm", type=int, default=0)
+    p.add_argument("--k1-read-all", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0,
+                   help="budget of the bounded CPU-baseline sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--report", default="", help="also write the JSON line to this path")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- helpers
+def measured_peak():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profile_traffic(config: str):
+    """dram read+write bytes per K1 launch from the committed ncu capture."""
+    path = os.path.join(REPO, "profiles", f"k1_traffic_{config}.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+def make_graph(config: str, device: str):
+    from paper_1505_04086_b200 import graphs
+    return graphs.make_config(config, device)
+
+
+def cpu_reference_runs(off_np, cols_np, seconds: float, max_runs: int, threads: int):
+    """The reference's own color_rsoc (oracle/_ref, compiled from
+    /root/reference) on the host cores; falls back to our C port of it
+    (oracle/gcol_oracle.c) when the reference library is absent."""
+    from oracle import oracle
+    oracle.build()
+    results = []
+    if oracle.ref_available():
+        kind = "reference"
+        R = oracle.RefGraph.from_csr(off_np, cols_np)
+        ff = R.first_fit_sequential()
+        runner = lambda: R.color("rsoc", threads)  # noqa: E731
+    else:
+        kind = "port"
+        g = oracle.CSR(off_np, cols_np)
+        ff = oracle.first_fit_sequential(g)
+        runner = lambda: oracle.color_parallel(g, threads, "rsoc")  # noqa: E731
+    serial_ff = int(len(set(ff.tolist()))) if ff.size else 0
+    t0 = time.time()
+    while len(results) < max_runs and (time.time() - t0 < seconds or len(results) < 1):
+        _, st = runner()
+        results.append(st)
+    return kind, results, serial_ff
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import torch
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    off, cols = make_graph(args.config, dev)
+    off_np, cols_np = off.cpu().numpy(), cols.cpu().numpy()
+    del off, cols
+    n, m = off_np.size - 1, int(off_np[-1])
+    threads = os.cpu_count() or 1
+    from oracle import oracle
+    oracle.build()
+    if oracle.ref_available():
+        kind = "reference"
+        R = oracle.RefGraph.from_csr(off_np, cols_np)
+        runner = lambda: R.color("rsoc", threads)  # noqa: E731
+    else:
+        kind = "port"
+        g = oracle.CSR(off_np, cols_np)
+        runner = lambda: oracle.color_parallel(g, threads, "rsoc")  # noqa: E731
+    for _ in range(args.warmup):
+        runner()
+    t0 = time.perf_counter()
+    times, colors = [], []
+    for _ in range(args.steps):
+        _, st = runner()
+        times.append(st["wall_time_ns"] * 1e-9)
+        colors.append(st["num_colors"])
+    wall = time.perf_counter() - t0
+    mean_t = sum(times) / len(times)
+    value = m / mean_t / 1e9
+    line = {
+        "impl": "reference", "metric": "edges colored/sec (directed adjacency entries)",
+        "value": value, "unit": "GE/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": mean_t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": CONFIG_WORKLOAD[args.config], "config": args.config,
+                   "n": n, "m_directed": m, "algorithm": "rsoc", "threads": threads},
+        "colors": {"median": sorted(colors)[(len(colors) - 1) // 2], "all": colors},
+        "cpu_baseline": {"value": value, "unit": "GE/s", "cores": threads, "kind": kind,
+                         "sample": f"{args.steps} full color_rsoc runs of the {args.config} "
+                                   f"graph (wall_time_ns, verification excluded)"},
+        "e2e": {"value": value, "unit": "GE/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        dist = None
+    torch.cuda.set_device(local)
+    from paper_1505_04086_b200 import _lib, gcol
+
+    off, cols = make_graph(args.config, "cuda")
+    n, m = off.numel() - 1, int(cols.numel())
+    g = gcol.Graph.from_device(off, cols)
+    maxdeg = g.max_degree()
+    prio = gcol.Priority[args.priority]
+    opt = gcol.ParallelOptions(priority=prio, k1_blocks_per_sm=args.k1_blocks_per_sm,
+                               k1_read_all=args.k1_read_all)
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def step():
+        flush.fill_(1)  # L2 flush between timed iterations (outside the timed events)
+        return gcol.color_rsoc(g, 1, opt, colors_out=out)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    runs = [step() for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    region_s = time.perf_counter() - t0
+    clocks = sampler.stop()
+
+    walls = [r.stats.wall_time_ns * 1e-9 for r in runs]
+    k1s = [r.stats.initial_pass_ns * 1e-9 for r in runs]
+    tot = sum(walls)
+    if dist:
+        t = torch.tensor([tot], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot = float(t.item())
+    ms_per_step = tot / args.steps * 1e3
+    value = world * m / (tot / args.steps) / 1e9
+    launches = sum(2 + 3 * r.stats.rounds for r in runs)
+    colors = [r.stats.num_colors for r in runs]
+    rounds = [r.stats.rounds for r in runs]
+    last = runs[-1].stats
+
+    # roofline of the dominant kernel (K1, the tentative-colour pass)
+    k1_mean = sum(k1s) / len(k1s)
+    gathers = last.k1_gathers
+    k1_bytes = 8 * (n + 1) + 4 * m + 4 * gathers + 4 * n
+    achieved = k1_bytes / k1_mean / 1e9
+    peak, peak_src = measured_peak()
+    traffic = profile_traffic(args.config)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": "k1_tentative",
+                "algorithmic_bytes_per_launch": k1_bytes,
+                "bytes_formula": "8(n+1) offsets + 4m cols + 4*gathers (lower-id neighbour "
+                                 "colours) + 4n colour stores",
+                "k1_ms": k1_mean * 1e3, "k1_share_of_step": k1_mean / (tot / args.steps),
+                "peak_source": peak_src}
+
+    line = {
+        "metric": "edges colored/sec (directed adjacency entries m / device coloring time)",
+        "value": value, "unit": "GE/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": CONFIG_WORKLOAD[args.config], "config": args.config, "n": n,
+                   "m_directed": m, "max_degree": maxdeg, "priority": args.priority,
+                   "parallelism": "replicas" if world > 1 else "single-gpu",
+                   "l2": "flushed between timed iterations (512 MB write, untimed)"},
+        "colors": {"gpu": colors[-1], "gpu_all": sorted(set(colors)), "rounds": rounds[-1],
+                   "conflicts_total": last.conflicts_total,
+                   "conflicts_per_round": last.conflicts_per_round,
+                   "pairs_logged": last.pairs_logged,
+                   "round1_candidates": last.round1_candidates},
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "clocks": clocks,
+        "timed_region_wall_s": region_s,
+    }
+
+    if rank == 0 and not args.no_e2e:
+        line["e2e"] = e2e_measure(args, off, cols, n, m, opt, _lib, gcol)
+    if rank == 0 and not args.no_cpu_baseline:
+        off_np, cols_np = off.cpu().numpy(), cols.cpu().numpy()
+        threads = os.cpu_count() or 1
+        kind, res, serial_ff = cpu_reference_runs(off_np, cols_np, args.cpu_seconds, 50, threads)
+        tmean = sum(r["wall_time_ns"] for r in res) / len(res) * 1e-9
+        ref_colors = sorted(r["num_colors"] for r in res)
+        med = ref_colors[(len(ref_colors) - 1) // 2]
+        line["cpu_baseline"] = {
+            "value": m / tmean / 1e9, "unit": "GE/s", "cores": threads, "kind": kind,
+            "sample": f"{len(res)} full color_rsoc runs of the {args.config} graph at "
+                      f"{threads} threads ({tmean * 1e3:.1f} ms each)"}
+        line["colors"].update({"ref_rsoc_median": med, "ref_rsoc_all": ref_colors,
+                               "serial_ff": serial_ff, "gate_1p05": math.floor(1.05 * med),
+                               "within_gate": colors[-1] <= math.floor(1.05 * med)})
+    if rank == 0:
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.report:
+            with open(args.report, "w") as f:
+                f.write(s + "\n")
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_measure(args, off, cols, n, m, opt, _lib, gcol):
+    """Public C ABI with HOST buffers: create (H2D upload of the CSR from
+    pinned memory) + color_rsoc (colours D2H into pinned memory) + destroy,
+    all inside the timed region."""
+    import torch
+    h_off = off.cpu().pin_memory()
+    h_cols = cols.cpu().pin_memory()
+    h_out = torch.empty(n, dtype=torch.int32).pin_memory()
+    copt = opt.to_c(1)
+    st = _lib.Stats()
+
+    def once():
+        h = C.c_void_p()
+        rc = _lib.LIB.gcol_cuda_graph_create(C.c_void_p(h_off.data_ptr()),
+                                             C.c_void_p(h_cols.data_ptr()), n, m,
+                                             _lib.GCOL_MEM_HOST, -1, C.byref(h))
+        if rc:
+            raise RuntimeError(_lib.last_error())
+        rc = _lib.LIB.gcol_cuda_color_rsoc(h, C.byref(copt), C.c_void_p(h_out.data_ptr()),
+                                           _lib.GCOL_MEM_HOST, C.byref(st))
+        if rc:
+            raise RuntimeError(_lib.last_error())
+        _lib.LIB.gcol_cuda_graph_destroy(h)
+
+    once()
+    t = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        once()
+        t.append(time.perf_counter() - t0)
+    mean_t = sum(t) / len(t)
+    return {"value": m / mean_t / 1e9, "unit": "GE/s", "h2d_bytes_per_step": 8 * (n + 1) + 4 * m,
+            "d2h_bytes_per_step": 4 * n, "ms_per_step": mean_t * 1e3,
+            "path": "gcol_cuda_graph_create(host CSR) + gcol_cuda_color_rsoc(host colours) + "
+                    "gcol_cuda_graph_destroy"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,199 @@
+/*
+ * gcol_cuda.h -- C ABI of the B200 (sm_100a) RSOC graph-coloring library.
+ *
+ * Drop-in boundary for the reference's coloring entry points
+ * (/root/reference/proj/include/gcol/...):
+ *
+ *   reference                                  replaced by
+ *   ---------------------------------------    ---------------------------------
+ *   Graph / build_graph   graph.hpp:20-138     gcol_cuda_graph_create (uploads a
+ *                                              canonical CSR once; the graph is
+ *                                              immutable like gcol::Graph)
+ *   color_rsoc            parallel.hpp:253-319 gcol_cuda_color_rsoc
+ *   run_coloring          bench.hpp:35-60      gcol_cuda_run_coloring (seq | rsoc)
+ *   first_fit_sequential  coloring.hpp:110-116 gcol_cuda_first_fit_sequential
+ *   smallest_available_color coloring.hpp:95-106
+ *                                              gcol_cuda_tentative_snapshot
+ *   detect_conflicts      coloring.hpp:133-141 gcol_cuda_detect_conflicts
+ *   verify_coloring       coloring.hpp:159-177 gcol_cuda_verify_coloring
+ *   count_colors          coloring.hpp:181-196 gcol_cuda_count_colors
+ *   ColoringStats         parallel.hpp:47-57   gcol_cuda_stats
+ *   ParallelOptions       parallel.hpp:64-72   gcol_cuda_options
+ *   errors.hpp exception taxonomy              gcol_status codes (below)
+ *
+ * Plain C types only: int64 row offsets (n+1), int32 column ids (m), int32
+ * colors (-1 = uncolored).  Pointers may be host or device memory; the
+ * `memory` arguments say which.  Nothing here falls back to the CPU: with no
+ * usable CUDA device every call returns GCOL_ERR_NO_DEVICE.
+ * A graph handle is not thread-safe (one stream per handle); separate
+ * handles may be used concurrently.
+ */
+#ifndef GCOL_CUDA_H
+#define GCOL_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GCOL_CUDA_ABI_VERSION 1
+
+/* Status codes.  The C++ adapter (gcol_cuda.hpp) rethrows them as the
+ * reference's exceptions (errors.hpp:11-52). */
+typedef enum {
+  GCOL_OK = 0,
+  GCOL_ERR_INVALID_ARGUMENT = 1, /* gcol::input_error */
+  GCOL_ERR_CAPACITY = 2,         /* gcol::capacity_error */
+  GCOL_ERR_CUDA = 3,             /* CUDA runtime failure (message in last_error) */
+  GCOL_ERR_NCCL = 4,             /* collective failure (multi-GPU) */
+  GCOL_ERR_ROUND_CAP = 5,        /* round_cap reached; the reference would run its
+                                    sequential repair here -- we never fall back
+                                    to the CPU, so this is an error */
+  GCOL_ERR_VERIFY = 6,           /* improper result (gcol::verification_error /
+                                    the logic_error of parallel.hpp:174-175) */
+  GCOL_ERR_NO_DEVICE = 7         /* no CUDA device: there is no CPU fallback */
+} gcol_status;
+
+/* Where a pointer lives. */
+typedef enum { GCOL_MEM_HOST = 0, GCOL_MEM_DEVICE = 1 } gcol_memory;
+
+/* Which endpoint of a monochromatic edge recolors.  Any strict total order
+ * terminates; ID_LOW is the reference rule
+ * (coloring.hpp:118-120: "the lower-indexed endpoint is the one that
+ * recolors") and the default. */
+typedef enum {
+  GCOL_PRIORITY_ID_LOW = 0,    /* reference: lower id recolors */
+  GCOL_PRIORITY_ID_HIGH = 1,   /* mirror: higher id recolors */
+  GCOL_PRIORITY_DEGREE_ID = 2  /* lower (degree, id) recolors */
+} gcol_priority;
+
+/* Algorithm ids follow gcol::Algorithm (parallel.hpp:21). */
+typedef enum { GCOL_ALG_SEQ = 0, GCOL_ALG_CATALYUREK = 1, GCOL_ALG_RSOC = 2 } gcol_algorithm;
+
+/* ParallelOptions (parallel.hpp:64-72) plus device knobs.  Zero-initialise
+ * and set struct_size = sizeof(gcol_cuda_options); zero fields = defaults. */
+typedef struct {
+  uint32_t struct_size;
+  uint32_t thread_count;     /* recorded in stats only (the GPU has no threads knob) */
+  uint64_t chunk_size;       /* accepted for API parity; ignored on the GPU */
+  uint64_t min_chunk_size;   /* accepted for API parity; ignored on the GPU */
+  uint64_t round_cap;        /* 0 -> 1000 (parallel.hpp:71) */
+  int32_t priority;          /* gcol_priority, default ID_LOW */
+  int32_t k1_blocks_per_sm;  /* K1 residency (in-flight window) knob, 0 = auto */
+  int32_t k1_read_all;       /* 0 (default): the initial pass gathers only the
+                                lower-id neighbours' colours; 1: every neighbour,
+                                like smallest_available_color (coloring.hpp:95-106).
+                                Both are valid RSOC initial passes. */
+  int32_t reserved[5];
+} gcol_cuda_options;
+
+/* ColoringStats (parallel.hpp:47-57) + device-side instrumentation. */
+typedef struct {
+  int32_t algorithm;
+  uint32_t thread_count;
+  uint64_t rounds;
+  uint64_t conflicts_total;
+  uint64_t barrier_events;     /* rounds + 1 for rsoc (kernel boundaries) */
+  uint32_t num_colors;         /* distinct colors (count_colors semantics) */
+  uint32_t fallback_triggered; /* always 0: no CPU repair exists here */
+  uint64_t wall_time_ns;       /* device time of the coloring graph (CUDA events) */
+  uint64_t initial_pass_ns;    /* device time of the tentative-color kernel (K1) */
+  uint64_t cpr_len;            /* == rounds */
+  uint64_t* conflicts_per_round; /* caller buffer (may be NULL) */
+  uint64_t cpr_cap;            /* its capacity */
+  uint64_t pairs_logged;       /* K1 in-flight (u,v) observations */
+  uint64_t round1_candidates;  /* vertices re-checked in round 1 */
+  uint32_t pair_overflow;      /* 1 if round 1 had to scan all of V */
+  int32_t priority;
+  uint64_t k1_gathers;         /* neighbour-colour loads issued by K1 */
+} gcol_cuda_stats;
+
+/* verify_coloring (coloring.hpp:159-177) summary + color bound check. */
+typedef struct {
+  uint64_t violations;     /* == reference ConflictReport.violations.size() */
+  uint64_t uncolored;      /* vertices with color -1 */
+  uint64_t conflict_edges; /* monochromatic undirected edges */
+  uint64_t out_of_bound;   /* vertices with color < -1 or color > degree */
+  uint64_t negative;       /* vertices with color < -1 */
+  uint32_t num_colors;     /* distinct non-negative colors (count_colors) */
+  int32_t max_color;
+} gcol_cuda_verify_report;
+
+typedef struct gcol_cuda_graph gcol_cuda_graph;
+
+/* Library / device queries. */
+int gcol_cuda_abi_version(void);
+int gcol_cuda_device_count(int32_t* count);
+/* Thread-local message for the last failing call on this thread. */
+const char* gcol_cuda_last_error(void);
+
+/* Uploads (memory == HOST) or borrows (memory == DEVICE, caller keeps the
+ * buffers alive and unchanged) a canonical CSR: offsets[0] == 0,
+ * offsets[n] == m, rows sorted ascending, symmetric, no self loops
+ * (graph.hpp:15-19; not re-validated beyond cheap checks).  n < 2^31 and
+ * column ids < n.  m may exceed 2^31 (int64 offsets).  device < 0 selects
+ * the current device. */
+int gcol_cuda_graph_create(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t m,
+                           int32_t memory, int32_t device, gcol_cuda_graph** out);
+int gcol_cuda_graph_destroy(gcol_cuda_graph* g);
+int gcol_cuda_graph_info(const gcol_cuda_graph* g, int64_t* n, int64_t* m, int32_t* max_degree);
+
+/* color_rsoc (parallel.hpp:253-319).  colors_out (n entries, host or
+ * device per colors_memory) receives the final proper coloring; stats may be
+ * NULL.  The run is verified on the device after the timed region (like
+ * finalize_run, parallel.hpp:164-177); an improper result is
+ * GCOL_ERR_VERIFY. */
+int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt, int32_t* colors_out,
+                         int32_t colors_memory, gcol_cuda_stats* stats);
+
+/* run_coloring (bench.hpp:35-60) dispatch: GCOL_ALG_SEQ -> the exact
+ * sequential First-Fit on the device, GCOL_ALG_RSOC -> color_rsoc,
+ * GCOL_ALG_CATALYUREK -> color_catalyurek. */
+int gcol_cuda_run_coloring(gcol_cuda_graph* g, int32_t algorithm, const gcol_cuda_options* opt,
+                           int32_t* colors_out, int32_t colors_memory, gcol_cuda_stats* stats);
+
+/* first_fit_sequential (coloring.hpp:110-116), bit-identical output. */
+int gcol_cuda_first_fit_sequential(gcol_cuda_graph* g, int32_t* colors_out, int32_t colors_memory);
+
+/* Snapshot-mode tentative pass (the production K1 with its in-place reads
+ * redirected to a frozen snapshot): for every v in worklist (or all v when
+ * worklist == NULL), colors_out[v] = smallest_available_color(v) computed
+ * over colors_in (coloring.hpp:95-106).  lower_only != 0 restricts the
+ * neighbourhood to ids < v (the initial-pass variant).  Deterministic.
+ * All buffers in `memory`. */
+int gcol_cuda_tentative_snapshot(gcol_cuda_graph* g, const int32_t* colors_in,
+                                 const int32_t* worklist, int64_t nwl, int32_t lower_only,
+                                 int32_t* colors_out, int32_t memory);
+
+/* detect_conflicts (coloring.hpp:133-141) under a priority rule:
+ * flags_out[i] = 1 iff pending[i] is defective.  ID_LOW reproduces the
+ * reference predicate exactly.  pending == NULL means all vertices. */
+int gcol_cuda_detect_conflicts(gcol_cuda_graph* g, const int32_t* colors, const int32_t* pending,
+                               int64_t npending, int32_t priority, int32_t* flags_out,
+                               int32_t memory);
+
+/* One fused detect-and-recolor step (the K2 round body, parallel.hpp:297-313)
+ * over `pending`, in place on `colors`; recolored ids are returned in
+ * recolored_out (capacity npending), their number in *nrecolored.
+ * Deterministic when `pending` is an independent set. */
+int gcol_cuda_detect_and_recolor(gcol_cuda_graph* g, int32_t* colors, const int32_t* pending,
+                                 int64_t npending, int32_t priority, int32_t* recolored_out,
+                                 int64_t* nrecolored, int32_t memory);
+
+/* verify_coloring (coloring.hpp:159-177).  Up to cap violations are written
+ * (u, v, color) in the reference order; report may be NULL.  colors in
+ * `memory`; out_* are host arrays (may be NULL when cap == 0). */
+int gcol_cuda_verify_coloring(gcol_cuda_graph* g, const int32_t* colors, int64_t ncolors,
+                              int32_t memory, gcol_cuda_verify_report* report, uint32_t* out_u,
+                              uint32_t* out_v, int32_t* out_c, int64_t cap);
+
+/* count_colors (coloring.hpp:181-196): distinct colors.  Incomplete or
+ * negative colorings are GCOL_ERR_INVALID_ARGUMENT (input_error). */
+int gcol_cuda_count_colors(gcol_cuda_graph* g, const int32_t* colors, int64_t ncolors,
+                           int32_t memory, uint32_t* num_colors);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GCOL_CUDA_H */

@@ -1,0 +1,752 @@
+// gcol_cuda.cu -- host side of libgcol_cuda.so: the C ABI of include/gcol_cuda.h
+// over the sm_100a kernels, with the RSOC round loop captured once per
+// handle as a CUDA graph (K1 -> candidates -> WHILE{list, heavy, control}).
+//
+// No CPU fallback exists anywhere in this file: every algorithmic step runs
+// on the device, and a missing device is an error (GCOL_ERR_NO_DEVICE).
+#include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "gcol_cuda.h"
+#include "gcol_kernels.cuh"
+
+using namespace gcol::dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define GCOL_CK(expr)                                                                    \
+  do {                                                                                   \
+    cudaError_t e__ = (expr);                                                            \
+    if (e__ != cudaSuccess)                                                              \
+      return fail(GCOL_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+template <class T>
+struct Identity {
+  using type = T;
+};
+
+// Adds a kernel node; argument values are copied into the node at call time.
+template <class... A>
+cudaError_t add_kernel(cudaGraphNode_t* node, cudaGraph_t g, const cudaGraphNode_t* deps,
+                       size_t ndeps, void (*f)(A...), dim3 grid, dim3 block,
+                       typename Identity<A>::type... args) {
+  void* params[] = {static_cast<void*>(&args)...};
+  cudaKernelNodeParams p{};
+  p.func = reinterpret_cast<void*>(f);
+  p.gridDim = grid;
+  p.blockDim = block;
+  p.sharedMemBytes = 0;
+  p.kernelParams = params;
+  p.extra = nullptr;
+  return cudaGraphAddKernelNode(node, g, deps, ndeps, &p);
+}
+
+struct ExecKey {
+  int rule, lower, k1_blocks;
+  bool operator<(const ExecKey& o) const {
+    return std::tie(rule, lower, k1_blocks) < std::tie(o.rule, o.lower, o.k1_blocks);
+  }
+};
+
+}  // namespace
+
+struct gcol_cuda_graph {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n = 0, m = 0;
+  int max_degree = 0;
+  long long* d_off = nullptr;
+  int* d_cols = nullptr;
+  bool owns_csr = false;
+  // run buffers (allocated on first coloring)
+  int* d_colors = nullptr;
+  int* d_listA = nullptr;
+  int* d_listB = nullptr;
+  int* d_heavy = nullptr;
+  int* d_marks = nullptr;
+  int2* d_pairs = nullptr;
+  unsigned long long pair_cap = 0;
+  Ctrl* d_ctrl = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_k1 = nullptr, ev_end = nullptr;
+  std::map<ExecKey, std::pair<cudaGraph_t, cudaGraphExec_t>> execs;
+};
+
+namespace {
+
+int ensure_device(int device, int* chosen) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(GCOL_ERR_NO_DEVICE,
+                std::string("no CUDA device available (there is no CPU fallback): ") +
+                    (e != cudaSuccess ? cudaGetErrorString(e) : "device count 0"));
+  if (device < 0) GCOL_CK(cudaGetDevice(&device));
+  if (device >= count) return fail(GCOL_ERR_INVALID_ARGUMENT, "device index out of range");
+  GCOL_CK(cudaSetDevice(device));
+  *chosen = device;
+  return GCOL_OK;
+}
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count, cudaStream_t s) {
+  return cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T), s);
+}
+
+int ensure_run_buffers(gcol_cuda_graph* g) {
+  if (g->d_colors) return GCOL_OK;
+  const size_t n = static_cast<size_t>(g->n);
+  GCOL_CK(dalloc(&g->d_colors, n, g->stream));
+  GCOL_CK(dalloc(&g->d_listA, n, g->stream));
+  GCOL_CK(dalloc(&g->d_listB, n, g->stream));
+  GCOL_CK(dalloc(&g->d_heavy, n, g->stream));
+  GCOL_CK(dalloc(&g->d_marks, n, g->stream));
+  // Round-1 observation log: m/8 + 1M pairs (8 B each); an overflow is
+  // handled on the device by scanning all of V.
+  g->pair_cap = static_cast<unsigned long long>(g->m / 8 + (1 << 20));
+  GCOL_CK(dalloc(&g->d_pairs, g->pair_cap, g->stream));
+  GCOL_CK(dalloc(&g->d_ctrl, 1, g->stream));
+  GCOL_CK(cudaEventCreate(&g->ev_start));
+  GCOL_CK(cudaEventCreate(&g->ev_k1));
+  GCOL_CK(cudaEventCreate(&g->ev_end));
+  return GCOL_OK;
+}
+
+int k1_grid(const gcol_cuda_graph* g, int blocks_per_sm, const void* kernel) {
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kBlock, 0);
+  if (occ < 1) occ = 1;
+  const int bps = blocks_per_sm > 0 ? std::min(blocks_per_sm, occ) : occ;
+  return g->sms * bps;
+}
+
+template <int R, bool kLower>
+int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, cudaGraph_t* out_graph,
+                     cudaGraphExec_t* out_exec) {
+  cudaGraph_t graph;
+  GCOL_CK(cudaGraphCreate(&graph, 0));
+  const int n = static_cast<int>(g->n);
+  PairLog L{g->d_pairs, g->pair_cap, &g->d_ctrl->pair_len, &g->d_ctrl->pair_overflow};
+  cudaGraphNode_t n_ev0, n_k1, n_ev1, n_cand, n_while, n_ev2;
+  GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
+  auto k1 = k1_tentative<false, kLower, true>;
+  const int grid1 = k1_grid(g, k1_blocks, reinterpret_cast<const void*>(k1));
+  GCOL_CK(add_kernel(&n_k1, graph, &n_ev0, 1, k1, dim3(grid1), dim3(kBlock), g->d_off,
+                     g->d_cols, n, n, static_cast<const int*>(nullptr),
+                     static_cast<const int*>(g->d_colors), g->d_colors, g->d_ctrl, L));
+  GCOL_CK(cudaGraphAddEventRecordNode(&n_ev1, graph, &n_k1, 1, g->ev_k1));
+  GCOL_CK(add_kernel(&n_cand, graph, &n_ev1, 1, k_candidates<R>, dim3(g->sms * 4), dim3(kBlock),
+                     g->d_off, g->d_cols, n, static_cast<const int*>(g->d_colors), g->d_ctrl,
+                     static_cast<const int2*>(g->d_pairs), g->pair_cap, g->d_marks));
+
+  cudaGraphConditionalHandle handle;
+  GCOL_CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  GCOL_CK(cudaGraphAddNode(&n_while, graph, &n_cand, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaGraphNode_t b_list, b_heavy, b_ctl;
+  GCOL_CK(add_kernel(&b_list, body, nullptr, 0, k_list<R, false>, dim3(g->sms * 4), dim3(kBlock),
+                     g->d_off, g->d_cols, g->d_colors, g->d_ctrl, g->d_heavy));
+  GCOL_CK(add_kernel(&b_heavy, body, &b_list, 1, k_heavy<R, false>, dim3(g->sms * 2),
+                     dim3(kBlock), g->d_off, g->d_cols, g->d_colors, g->d_ctrl,
+                     static_cast<const int*>(g->d_heavy)));
+  GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle));
+  GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, graph, &n_while, 1, g->ev_end));
+  GCOL_CK(cudaGraphInstantiate(out_exec, graph, 0));
+  *out_graph = graph;
+  return GCOL_OK;
+}
+
+int get_exec(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, cudaGraphExec_t* exec) {
+  ExecKey key{rule, lower, k1_blocks};
+  auto it = g->execs.find(key);
+  if (it != g->execs.end()) {
+    *exec = it->second.second;
+    return GCOL_OK;
+  }
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  int rc;
+  if (rule == kIdLow)
+    rc = lower ? build_rsoc_graph<kIdLow, true>(g, k1_blocks, &graph, &ex)
+               : build_rsoc_graph<kIdLow, false>(g, k1_blocks, &graph, &ex);
+  else if (rule == kIdHigh)
+    rc = lower ? build_rsoc_graph<kIdHigh, true>(g, k1_blocks, &graph, &ex)
+               : build_rsoc_graph<kIdHigh, false>(g, k1_blocks, &graph, &ex);
+  else
+    rc = lower ? build_rsoc_graph<kDegId, true>(g, k1_blocks, &graph, &ex)
+               : build_rsoc_graph<kDegId, false>(g, k1_blocks, &graph, &ex);
+  if (rc != GCOL_OK) return rc;
+  g->execs[key] = {graph, ex};
+  *exec = ex;
+  return GCOL_OK;
+}
+
+// Resets the control block for a run (host-side struct, one H2D copy).
+int reset_ctrl(gcol_cuda_graph* g, int round_cap, int* in_list, int* out_list, int* flags,
+               int in_len) {
+  // only the header is reset; cpr[] entries are written before being read
+  const size_t hdr = offsetof(Ctrl, cpr);
+  static thread_local std::vector<char> buf;
+  buf.assign(hdr, 0);
+  Ctrl* c = reinterpret_cast<Ctrl*>(buf.data());
+  c->in_list = in_list;
+  c->out_list = out_list;
+  c->flags = flags;
+  c->in_len = in_len;
+  c->round_cap = round_cap;
+  GCOL_CK(cudaMemcpyAsync(g->d_ctrl, buf.data(), hdr, cudaMemcpyHostToDevice, g->stream));
+  return GCOL_OK;
+}
+
+int copy_in(gcol_cuda_graph* g, void* dst, const void* src, size_t bytes, int memory) {
+  if (bytes == 0) return GCOL_OK;
+  GCOL_CK(cudaMemcpyAsync(dst, src, bytes,
+                          memory == GCOL_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                    : cudaMemcpyHostToDevice,
+                          g->stream));
+  return GCOL_OK;
+}
+
+int copy_out(gcol_cuda_graph* g, void* dst, const void* src, size_t bytes, int memory) {
+  if (bytes == 0) return GCOL_OK;
+  GCOL_CK(cudaMemcpyAsync(dst, src, bytes,
+                          memory == GCOL_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                    : cudaMemcpyDeviceToHost,
+                          g->stream));
+  return GCOL_OK;
+}
+
+// Device verification + census of a device colour buffer.
+int verify_device(gcol_cuda_graph* g, const int* d_col, gcol_cuda_verify_report* rep,
+                  uint32_t* out_u, uint32_t* out_v, int32_t* out_c, int64_t cap) {
+  const int n = static_cast<int>(g->n);
+  VerifyAcc* d_acc = nullptr;
+  int* d_vcount = nullptr;
+  GCOL_CK(dalloc(&d_acc, 1, g->stream));
+  GCOL_CK(cudaMemsetAsync(d_acc, 0, sizeof(VerifyAcc), g->stream));
+  GCOL_CK(cudaMemsetAsync(&d_acc->max_color, 0xff, sizeof(int), g->stream));
+  if (cap > 0) GCOL_CK(dalloc(&d_vcount, static_cast<size_t>(n), g->stream));
+  const int grid = g->sms * 8;
+  if (n > 0)
+    k_verify_count<<<grid, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, d_col, d_acc, d_vcount);
+  GCOL_CK(cudaGetLastError());
+  VerifyAcc acc;
+  GCOL_CK(cudaMemcpyAsync(&acc, d_acc, sizeof acc, cudaMemcpyDeviceToHost, g->stream));
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  uint32_t distinct = 0;
+  if (acc.max_color >= 0) {
+    const int words = acc.max_color / 32 + 1;
+    unsigned* d_bitmap = nullptr;
+    GCOL_CK(dalloc(&d_bitmap, words, g->stream));
+    GCOL_CK(cudaMemsetAsync(d_bitmap, 0, sizeof(unsigned) * words, g->stream));
+    k_census<<<grid, kBlock, 0, g->stream>>>(d_col, n, d_bitmap, acc.max_color);
+    GCOL_CK(cudaGetLastError());
+    std::vector<unsigned> bitmap(words);
+    GCOL_CK(cudaMemcpyAsync(bitmap.data(), d_bitmap, sizeof(unsigned) * words,
+                            cudaMemcpyDeviceToHost, g->stream));
+    GCOL_CK(cudaStreamSynchronize(g->stream));
+    GCOL_CK(cudaFreeAsync(d_bitmap, g->stream));
+    for (unsigned w : bitmap) distinct += static_cast<uint32_t>(__builtin_popcount(w));
+  }
+  if (cap > 0 && n > 0) {
+    long long* d_pos = nullptr;
+    int3* d_out = nullptr;
+    void* d_tmp = nullptr;
+    size_t tmp_bytes = 0;
+    GCOL_CK(dalloc(&d_pos, static_cast<size_t>(n), g->stream));
+    GCOL_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_vcount, d_pos, n, g->stream));
+    GCOL_CK(cudaMallocAsync(&d_tmp, std::max<size_t>(tmp_bytes, 1), g->stream));
+    GCOL_CK(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_vcount, d_pos, n, g->stream));
+    const long long want = std::min<long long>(cap, static_cast<long long>(acc.violations));
+    if (want > 0) {
+      GCOL_CK(dalloc(&d_out, static_cast<size_t>(want), g->stream));
+      k_verify_write<<<grid, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, d_col, d_vcount,
+                                                     d_pos, d_out, want);
+      GCOL_CK(cudaGetLastError());
+      std::vector<int3> h(static_cast<size_t>(want));
+      GCOL_CK(cudaMemcpyAsync(h.data(), d_out, sizeof(int3) * want, cudaMemcpyDeviceToHost,
+                              g->stream));
+      GCOL_CK(cudaStreamSynchronize(g->stream));
+      for (long long i = 0; i < want; ++i) {
+        if (out_u) out_u[i] = static_cast<uint32_t>(h[i].x);
+        if (out_v) out_v[i] = static_cast<uint32_t>(h[i].y);
+        if (out_c) out_c[i] = h[i].z;
+      }
+      GCOL_CK(cudaFreeAsync(d_out, g->stream));
+    }
+    GCOL_CK(cudaFreeAsync(d_tmp, g->stream));
+    GCOL_CK(cudaFreeAsync(d_pos, g->stream));
+    GCOL_CK(cudaFreeAsync(d_vcount, g->stream));
+  }
+  GCOL_CK(cudaFreeAsync(d_acc, g->stream));
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  if (rep) {
+    rep->violations = acc.violations;
+    rep->uncolored = acc.uncolored;
+    rep->conflict_edges = acc.conflict_edges;
+    rep->out_of_bound = acc.out_of_bound;
+    rep->negative = acc.negative;
+    rep->num_colors = distinct;
+    rep->max_color = acc.max_color;
+  }
+  return GCOL_OK;
+}
+
+int check_graph(const gcol_cuda_graph* g) {
+  if (!g) return fail(GCOL_ERR_INVALID_ARGUMENT, "null graph handle");
+  return GCOL_OK;
+}
+
+void default_options(gcol_cuda_options* o) {
+  std::memset(o, 0, sizeof *o);
+  o->struct_size = sizeof *o;
+  o->thread_count = 1;
+  o->min_chunk_size = 64;
+  o->round_cap = 1000;
+}
+
+int read_options(const gcol_cuda_options* in, gcol_cuda_options* o) {
+  default_options(o);
+  if (in) {
+    if (in->struct_size != 0 && in->struct_size < sizeof(gcol_cuda_options))
+      return fail(GCOL_ERR_INVALID_ARGUMENT, "gcol_cuda_options.struct_size too small");
+    *o = *in;
+    if (o->round_cap == 0) o->round_cap = 1000;
+  }
+  if (o->thread_count < 1)
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "thread_count must be at least 1");  // parallel.hpp:255
+  if (o->priority < GCOL_PRIORITY_ID_LOW || o->priority > GCOL_PRIORITY_DEGREE_ID)
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "unknown priority rule");
+  if (o->round_cap > 0x7fffffffull) o->round_cap = 0x7fffffffull;
+  return GCOL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gcol_cuda_abi_version(void) { return GCOL_CUDA_ABI_VERSION; }
+
+const char* gcol_cuda_last_error(void) { return g_last_error.c_str(); }
+
+int gcol_cuda_device_count(int32_t* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) c = 0;
+  if (count) *count = c;
+  if (c == 0) return fail(GCOL_ERR_NO_DEVICE, "no CUDA device available");
+  return GCOL_OK;
+}
+
+int gcol_cuda_graph_create(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t m,
+                           int32_t memory, int32_t device, gcol_cuda_graph** out) {
+  if (!out) return fail(GCOL_ERR_INVALID_ARGUMENT, "out is null");
+  *out = nullptr;
+  if (n < 0 || m < 0) return fail(GCOL_ERR_INVALID_ARGUMENT, "negative size");
+  if (n >= 0x7fffffffLL)
+    return fail(GCOL_ERR_CAPACITY, "vertex count exceeds the 31-bit id space of int32 columns");
+  if (!offsets) return fail(GCOL_ERR_INVALID_ARGUMENT, "offsets is null");
+  if (m > 0 && !cols) return fail(GCOL_ERR_INVALID_ARGUMENT, "cols is null");
+  if (memory != GCOL_MEM_HOST && memory != GCOL_MEM_DEVICE)
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "bad memory kind");
+  if (memory == GCOL_MEM_HOST) {  // cheap structural checks (graph.hpp:50-56)
+    if (offsets[0] != 0 || offsets[n] != m)
+      return fail(GCOL_ERR_INVALID_ARGUMENT, "graph: offsets do not cover the adjacency array");
+    for (int64_t v = 0; v < n; ++v)
+      if (offsets[v] > offsets[v + 1])
+        return fail(GCOL_ERR_INVALID_ARGUMENT, "graph: offsets are not monotone");
+  }
+  int dev = 0;
+  int rc = ensure_device(device, &dev);
+  if (rc != GCOL_OK) return rc;
+  auto* g = new gcol_cuda_graph();
+  g->device = dev;
+  g->n = n;
+  g->m = m;
+  cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete g;
+    return fail(GCOL_ERR_CUDA, std::string("stream create: ") + cudaGetErrorString(e));
+  }
+  // Keep freed pool memory cached so repeated create/destroy stays cheap.
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  auto bail = [&](int code) {
+    gcol_cuda_graph_destroy(g);
+    return code;
+  };
+  if (memory == GCOL_MEM_DEVICE) {
+    g->d_off = const_cast<long long*>(reinterpret_cast<const long long*>(offsets));
+    g->d_cols = const_cast<int*>(cols);
+    g->owns_csr = false;
+  } else {
+    g->owns_csr = true;
+    if (dalloc(&g->d_off, static_cast<size_t>(n) + 1, g->stream) != cudaSuccess ||
+        dalloc(&g->d_cols, static_cast<size_t>(m), g->stream) != cudaSuccess)
+      return bail(fail(GCOL_ERR_CUDA, "device allocation of the CSR failed"));
+    if (copy_in(g, g->d_off, offsets, sizeof(long long) * (static_cast<size_t>(n) + 1), memory) ||
+        copy_in(g, g->d_cols, cols, sizeof(int) * static_cast<size_t>(m), memory))
+      return bail(GCOL_ERR_CUDA);
+  }
+  int* d_max = nullptr;
+  if (dalloc(&d_max, 1, g->stream) != cudaSuccess) return bail(fail(GCOL_ERR_CUDA, "alloc"));
+  cudaMemsetAsync(d_max, 0, sizeof(int), g->stream);
+  if (n > 0) k_max_degree<<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, static_cast<int>(n), d_max);
+  cudaMemcpyAsync(&g->max_degree, d_max, sizeof(int), cudaMemcpyDeviceToHost, g->stream);
+  cudaFreeAsync(d_max, g->stream);
+  e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess)
+    return bail(fail(GCOL_ERR_CUDA, std::string("graph upload: ") + cudaGetErrorString(e)));
+  *out = g;
+  return GCOL_OK;
+}
+
+int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
+  if (!g) return GCOL_OK;
+  cudaSetDevice(g->device);
+  for (auto& kv : g->execs) {
+    cudaGraphExecDestroy(kv.second.second);
+    cudaGraphDestroy(kv.second.first);
+  }
+  if (g->stream) {
+    if (g->owns_csr) {
+      cudaFreeAsync(g->d_off, g->stream);
+      cudaFreeAsync(g->d_cols, g->stream);
+    }
+    for (void* p : {static_cast<void*>(g->d_colors), static_cast<void*>(g->d_listA),
+                    static_cast<void*>(g->d_listB), static_cast<void*>(g->d_heavy),
+                    static_cast<void*>(g->d_marks), static_cast<void*>(g->d_pairs),
+                    static_cast<void*>(g->d_ctrl)})
+      if (p) cudaFreeAsync(p, g->stream);
+    cudaStreamSynchronize(g->stream);
+    cudaStreamDestroy(g->stream);
+  }
+  for (cudaEvent_t ev : {g->ev_start, g->ev_k1, g->ev_end})
+    if (ev) cudaEventDestroy(ev);
+  delete g;
+  return GCOL_OK;
+}
+
+int gcol_cuda_graph_info(const gcol_cuda_graph* g, int64_t* n, int64_t* m, int32_t* max_degree) {
+  if (int rc = check_graph(g)) return rc;
+  if (n) *n = g->n;
+  if (m) *m = g->m;
+  if (max_degree) *max_degree = g->max_degree;
+  return GCOL_OK;
+}
+
+int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, int32_t* colors_out,
+                         int32_t colors_memory, gcol_cuda_stats* stats) {
+  if (int rc = check_graph(g)) return rc;
+  gcol_cuda_options opt;
+  if (int rc = read_options(opt_in, &opt)) return rc;
+  if (g->n > 0 && !colors_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "colors_out is null");
+  GCOL_CK(cudaSetDevice(g->device));
+  if (int rc = ensure_run_buffers(g)) return rc;
+  cudaGraphExec_t exec;
+  const int lower = opt.k1_read_all ? 0 : 1;
+  if (int rc = get_exec(g, opt.priority, lower, opt.k1_blocks_per_sm, &exec)) return rc;
+  // Untimed prologue, like Coloring(n) before the reference's timer
+  // (parallel.hpp:258 vs :267): colours := -1, marks := 0, control reset.
+  const size_t n = static_cast<size_t>(g->n);
+  GCOL_CK(cudaMemsetAsync(g->d_colors, 0xff, sizeof(int) * n, g->stream));
+  GCOL_CK(cudaMemsetAsync(g->d_marks, 0, sizeof(int) * n, g->stream));
+  if (int rc = reset_ctrl(g, static_cast<int>(opt.round_cap), g->d_listA, g->d_listB, nullptr, 0))
+    return rc;
+  GCOL_CK(cudaGraphLaunch(exec, g->stream));
+  // Header + conflicts_per_round back in two copies.
+  Ctrl hdr;
+  GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  const int rounds = hdr.round;
+  std::vector<unsigned long long> cpr(std::min(rounds, kMaxRoundsRecorded));
+  if (!cpr.empty())
+    GCOL_CK(cudaMemcpyAsync(cpr.data(), g->d_ctrl->cpr, sizeof(unsigned long long) * cpr.size(),
+                            cudaMemcpyDeviceToHost, g->stream));
+  float ms_total = 0.f, ms_k1 = 0.f;
+  GCOL_CK(cudaEventElapsedTime(&ms_total, g->ev_start, g->ev_end));
+  GCOL_CK(cudaEventElapsedTime(&ms_k1, g->ev_start, g->ev_k1));
+  // finalize_run (parallel.hpp:164-177): verify after the timed region.
+  gcol_cuda_verify_report rep{};
+  if (int rc = verify_device(g, g->d_colors, &rep, nullptr, nullptr, nullptr, 0)) return rc;
+  if (int rc = copy_out(g, colors_out, g->d_colors, sizeof(int) * n, colors_memory)) return rc;
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  if (stats) {
+    stats->algorithm = GCOL_ALG_RSOC;
+    stats->thread_count = opt.thread_count;
+    stats->rounds = static_cast<uint64_t>(rounds);
+    uint64_t total = 0;
+    for (auto c : cpr) total += c;
+    stats->conflicts_total = total;
+    stats->barrier_events = static_cast<uint64_t>(rounds) + 1;
+    stats->num_colors = rep.num_colors;
+    stats->fallback_triggered = 0;
+    stats->wall_time_ns = static_cast<uint64_t>(static_cast<double>(ms_total) * 1e6);
+    stats->initial_pass_ns = static_cast<uint64_t>(static_cast<double>(ms_k1) * 1e6);
+    stats->cpr_len = static_cast<uint64_t>(rounds);
+    if (stats->conflicts_per_round)
+      for (uint64_t i = 0; i < cpr.size() && i < stats->cpr_cap; ++i)
+        stats->conflicts_per_round[i] = cpr[i];
+    stats->pairs_logged = hdr.pair_len;
+    stats->round1_candidates = static_cast<uint64_t>(hdr.cand_total);
+    stats->pair_overflow = static_cast<uint32_t>(hdr.pair_overflow);
+    stats->priority = opt.priority;
+    stats->k1_gathers = hdr.k1_gathers;
+  }
+  if (hdr.capped)
+    return fail(GCOL_ERR_ROUND_CAP,
+                "round_cap reached before convergence (no CPU repair fallback exists)");
+  if (rep.violations != 0 || rep.out_of_bound != 0)
+    return fail(GCOL_ERR_VERIFY, "parallel coloring finished improper");
+  return GCOL_OK;
+}
+
+int gcol_cuda_first_fit_sequential(gcol_cuda_graph* g, int32_t* colors_out, int32_t colors_memory) {
+  if (int rc = check_graph(g)) return rc;
+  GCOL_CK(cudaSetDevice(g->device));
+  if (int rc = ensure_run_buffers(g)) return rc;
+  const size_t n = static_cast<size_t>(g->n);
+  GCOL_CK(cudaMemsetAsync(g->d_colors, 0xff, sizeof(int) * n, g->stream));
+  if (n > 0)
+    k_first_fit_seq<<<1, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, static_cast<int>(n),
+                                                 g->d_colors);
+  GCOL_CK(cudaGetLastError());
+  if (int rc = copy_out(g, colors_out, g->d_colors, sizeof(int) * n, colors_memory)) return rc;
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  return GCOL_OK;
+}
+
+int gcol_cuda_run_coloring(gcol_cuda_graph* g, int32_t algorithm, const gcol_cuda_options* opt_in,
+                           int32_t* colors_out, int32_t colors_memory, gcol_cuda_stats* stats) {
+  if (int rc = check_graph(g)) return rc;
+  if (algorithm == GCOL_ALG_RSOC)
+    return gcol_cuda_color_rsoc(g, opt_in, colors_out, colors_memory, stats);
+  if (algorithm != GCOL_ALG_SEQ)
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "algorithm not available on the device yet");
+  gcol_cuda_options opt;
+  if (int rc = read_options(opt_in, &opt)) return rc;
+  cudaEvent_t a, b;
+  GCOL_CK(cudaSetDevice(g->device));
+  GCOL_CK(cudaEventCreate(&a));
+  GCOL_CK(cudaEventCreate(&b));
+  GCOL_CK(cudaEventRecord(a, g->stream));
+  int rc = gcol_cuda_first_fit_sequential(g, colors_out, colors_memory);
+  if (rc) return rc;
+  GCOL_CK(cudaEventRecord(b, g->stream));
+  GCOL_CK(cudaEventSynchronize(b));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (stats) {  // run_coloring's seq stats (bench.hpp:52-58)
+    gcol_cuda_verify_report rep{};
+    if (int r2 = verify_device(g, g->d_colors, &rep, nullptr, nullptr, nullptr, 0)) return r2;
+    stats->algorithm = GCOL_ALG_SEQ;
+    stats->thread_count = opt.thread_count;
+    stats->rounds = 1;
+    stats->conflicts_total = 0;
+    stats->barrier_events = 0;
+    stats->num_colors = rep.num_colors;
+    stats->fallback_triggered = 0;
+    stats->wall_time_ns = static_cast<uint64_t>(static_cast<double>(ms) * 1e6);
+    stats->initial_pass_ns = stats->wall_time_ns;
+    stats->cpr_len = 1;
+    if (stats->conflicts_per_round && stats->cpr_cap > 0) stats->conflicts_per_round[0] = 0;
+    stats->pairs_logged = 0;
+    stats->round1_candidates = 0;
+    stats->pair_overflow = 0;
+    stats->priority = opt.priority;
+    stats->k1_gathers = 0;
+  }
+  return GCOL_OK;
+}
+
+int gcol_cuda_tentative_snapshot(gcol_cuda_graph* g, const int32_t* colors_in,
+                                 const int32_t* worklist, int64_t nwl, int32_t lower_only,
+                                 int32_t* colors_out, int32_t memory) {
+  if (int rc = check_graph(g)) return rc;
+  if (!colors_in || !colors_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "null colour buffer");
+  GCOL_CK(cudaSetDevice(g->device));
+  if (int rc = ensure_run_buffers(g)) return rc;
+  const size_t n = static_cast<size_t>(g->n);
+  const int nitems = worklist ? static_cast<int>(nwl) : static_cast<int>(n);
+  int *d_in = nullptr, *d_out = g->d_colors, *d_wl = nullptr;
+  GCOL_CK(dalloc(&d_in, n, g->stream));
+  if (int rc = copy_in(g, d_in, colors_in, sizeof(int) * n, memory)) return rc;
+  GCOL_CK(cudaMemcpyAsync(d_out, d_in, sizeof(int) * n, cudaMemcpyDeviceToDevice, g->stream));
+  if (worklist) {
+    GCOL_CK(dalloc(&d_wl, static_cast<size_t>(nitems), g->stream));
+    if (int rc = copy_in(g, d_wl, worklist, sizeof(int) * nitems, memory)) return rc;
+  }
+  if (int rc = reset_ctrl(g, 1, nullptr, nullptr, nullptr, 0)) return rc;
+  PairLog L{};
+  if (nitems > 0) {
+    if (lower_only) {
+      auto k = k1_tentative<true, true, false>;
+      k<<<k1_grid(g, 0, reinterpret_cast<const void*>(k)), kBlock, 0, g->stream>>>(
+          g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, L);
+    } else {
+      auto k = k1_tentative<true, false, false>;
+      k<<<k1_grid(g, 0, reinterpret_cast<const void*>(k)), kBlock, 0, g->stream>>>(
+          g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, L);
+    }
+  }
+  GCOL_CK(cudaGetLastError());
+  if (int rc = copy_out(g, colors_out, d_out, sizeof(int) * n, memory)) return rc;
+  GCOL_CK(cudaFreeAsync(d_in, g->stream));
+  if (d_wl) GCOL_CK(cudaFreeAsync(d_wl, g->stream));
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  return GCOL_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+template <int R, bool kDetect>
+void launch_round(gcol_cuda_graph* g) {
+  k_list<R, kDetect><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
+                                                            g->d_ctrl, g->d_heavy);
+  k_heavy<R, kDetect><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
+                                                             g->d_ctrl, g->d_heavy);
+}
+
+template <bool kDetect>
+void launch_round_rule(gcol_cuda_graph* g, int rule) {
+  if (rule == kIdLow) launch_round<kIdLow, kDetect>(g);
+  else if (rule == kIdHigh) launch_round<kIdHigh, kDetect>(g);
+  else launch_round<kDegId, kDetect>(g);
+}
+
+// Shared driver of the detect-only and detect-and-recolour API entries.
+int run_list_api(gcol_cuda_graph* g, const int32_t* colors, const int32_t* pending,
+                 int64_t npending, int32_t priority, bool detect_only, int32_t* out,
+                 int64_t* nout, int32_t memory, int32_t* colors_back) {
+  if (int rc = check_graph(g)) return rc;
+  if (priority < GCOL_PRIORITY_ID_LOW || priority > GCOL_PRIORITY_DEGREE_ID)
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "unknown priority rule");
+  if (!colors) return fail(GCOL_ERR_INVALID_ARGUMENT, "null colours");
+  GCOL_CK(cudaSetDevice(g->device));
+  if (int rc = ensure_run_buffers(g)) return rc;
+  const size_t n = static_cast<size_t>(g->n);
+  const int np = pending ? static_cast<int>(npending) : static_cast<int>(n);
+  if (int rc = copy_in(g, g->d_colors, colors, sizeof(int) * n, memory)) return rc;
+  if (pending) {
+    if (int rc = copy_in(g, g->d_listA, pending, sizeof(int) * np, memory)) return rc;
+  } else if (np > 0) {
+    std::vector<int> iota(np);
+    for (int i = 0; i < np; ++i) iota[i] = i;
+    GCOL_CK(cudaMemcpyAsync(g->d_listA, iota.data(), sizeof(int) * np, cudaMemcpyHostToDevice,
+                            g->stream));
+    GCOL_CK(cudaStreamSynchronize(g->stream));
+  }
+  int* d_flags = nullptr;
+  if (detect_only) GCOL_CK(dalloc(&d_flags, static_cast<size_t>(np), g->stream));
+  if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, d_flags, np)) return rc;
+  if (np > 0) {
+    if (detect_only) launch_round_rule<true>(g, priority);
+    else launch_round_rule<false>(g, priority);
+  }
+  GCOL_CK(cudaGetLastError());
+  if (detect_only) {
+    if (int rc = copy_out(g, out, d_flags, sizeof(int) * np, memory)) return rc;
+    GCOL_CK(cudaFreeAsync(d_flags, g->stream));
+    if (nout) *nout = np;
+  } else {
+    Ctrl hdr;
+    GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost,
+                            g->stream));
+    GCOL_CK(cudaStreamSynchronize(g->stream));
+    if (int rc = copy_out(g, out, g->d_listB, sizeof(int) * hdr.out_len, memory)) return rc;
+    if (colors_back)
+      if (int rc = copy_out(g, colors_back, g->d_colors, sizeof(int) * n, memory)) return rc;
+    if (nout) *nout = hdr.out_len;
+  }
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  return GCOL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gcol_cuda_detect_conflicts(gcol_cuda_graph* g, const int32_t* colors, const int32_t* pending,
+                               int64_t npending, int32_t priority, int32_t* flags_out,
+                               int32_t memory) {
+  if (!flags_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "flags_out is null");
+  return run_list_api(g, colors, pending, npending, priority, true, flags_out, nullptr, memory,
+                      nullptr);
+}
+
+int gcol_cuda_detect_and_recolor(gcol_cuda_graph* g, int32_t* colors, const int32_t* pending,
+                                 int64_t npending, int32_t priority, int32_t* recolored_out,
+                                 int64_t* nrecolored, int32_t memory) {
+  if (!recolored_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "recolored_out is null");
+  return run_list_api(g, colors, pending, npending, priority, false, recolored_out, nrecolored,
+                      memory, colors);
+}
+
+int gcol_cuda_verify_coloring(gcol_cuda_graph* g, const int32_t* colors, int64_t ncolors,
+                              int32_t memory, gcol_cuda_verify_report* report, uint32_t* out_u,
+                              uint32_t* out_v, int32_t* out_c, int64_t cap) {
+  if (int rc = check_graph(g)) return rc;
+  if (ncolors != g->n)  // coloring.hpp:161-164 input_error
+    return fail(GCOL_ERR_INVALID_ARGUMENT,
+                "verify_coloring: coloring has " + std::to_string(ncolors) + " entries, graph has " +
+                    std::to_string(g->n) + " vertices");
+  if (g->n > 0 && !colors) return fail(GCOL_ERR_INVALID_ARGUMENT, "null colours");
+  GCOL_CK(cudaSetDevice(g->device));
+  const size_t n = static_cast<size_t>(g->n);
+  const int* d = colors;
+  int* tmp = nullptr;
+  if (memory == GCOL_MEM_HOST) {
+    GCOL_CK(dalloc(&tmp, n, g->stream));
+    if (int rc = copy_in(g, tmp, colors, sizeof(int) * n, memory)) return rc;
+    d = tmp;
+  }
+  int rc = verify_device(g, d, report, out_u, out_v, out_c, cap);
+  if (tmp) cudaFreeAsync(tmp, g->stream);
+  cudaStreamSynchronize(g->stream);
+  return rc;
+}
+
+int gcol_cuda_count_colors(gcol_cuda_graph* g, const int32_t* colors, int64_t ncolors,
+                           int32_t memory, uint32_t* num_colors) {
+  gcol_cuda_verify_report rep{};
+  if (int rc = gcol_cuda_verify_coloring(g, colors, ncolors, memory, &rep, nullptr, nullptr,
+                                         nullptr, 0))
+    return rc;
+  if (rep.uncolored)
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "count_colors: coloring is incomplete");
+  if (rep.negative)  // coloring.hpp:186-188
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "count_colors: negative color value");
+  if (num_colors) *num_colors = rep.num_colors;
+  return GCOL_OK;
+}
+
+}  // extern "C"

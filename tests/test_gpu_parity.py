@@ -1,0 +1,272 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden fixtures.  Integer work, so every comparison is bit-exact
+except colour COUNTS of concurrent runs, which follow the reference's own
+band rules (test_parallel.cpp, acceptance.cpp:165-190).
+"""
+import numpy as np
+import pytest
+
+from tests.golden_util import coloring_fixtures
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # collected on CPU runs, skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1505_04086_b200 import gcol, graphs  # noqa: E402
+
+
+def dev_graph(case):
+    return gcol.Graph(case["off"], case["cols"])
+
+
+def oracle_csr(oracle_mod, g):
+    return oracle_mod.CSR(g.offsets(), g.adjacency(), g.max_degree())
+
+
+def check_run(g, run, threads, algorithm="rsoc"):
+    """test_parallel.cpp:18-36 invariants + north_star bit-exact gates."""
+    c = run.coloring
+    st = run.stats
+    assert (c >= 0).all(), "every vertex coloured"
+    assert gcol.verify_coloring(g, c).ok(), "no monochromatic edge"
+    deg = np.diff(g.offsets())
+    assert (c <= deg).all(), "colour <= degree (0-based; <= degree+1 in 1-based terms)"
+    assert st.num_colors == gcol.count_colors(c)
+    assert st.num_colors <= g.max_degree() + 1
+    assert st.thread_count == threads
+    assert st.rounds >= 1
+    assert len(st.conflicts_per_round) == st.rounds
+    assert st.conflicts_total == sum(st.conflicts_per_round)
+    assert st.conflicts_per_round[-1] == 0
+    assert not st.fallback_triggered
+    if algorithm == "rsoc":
+        assert st.barrier_events == st.rounds + 1
+
+
+NAMES = list(coloring_fixtures().keys())
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_golden_first_fit_and_snapshot(name):
+    """first_fit_sequential and snapshot-mode K1 are bit-identical to the
+    reference (coloring.hpp:95-116)."""
+    case = coloring_fixtures()[name]
+    g = dev_graph(case)
+    assert np.array_equal(gcol.first_fit_sequential(g), case["ff"])
+    assert np.array_equal(gcol.tentative_snapshot(g, case["snap"]), case["snap_sac"])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_golden_detect_verify_count(name):
+    case = coloring_fixtures()[name]
+    g = dev_graph(case)
+    n = g.num_vertices()
+    allv = list(range(n))
+    assert gcol.detect_conflicts(g, case["pal"], allv) == list(case["detect_all"])
+    assert gcol.detect_conflicts(g, case["pal"], allv[::2]) == list(case["detect_even"])
+    rep = gcol.verify_coloring(g, case["pal"])
+    want = [tuple(int(x) for x in r) for r in case["verify"]]
+    assert [(v.u, v.v, v.color) for v in rep.violations] == want
+    assert gcol.count_colors(case["ff"], g) == int(case["count_ff"][0])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_golden_rsoc_valid(name):
+    case = coloring_fixtures()[name]
+    g = dev_graph(case)
+    for threads in (1, 8):
+        run = gcol.color_rsoc(g, threads)
+        check_run(g, run, threads)
+
+
+def test_kats_shapes():
+    """test_parallel.cpp:63-116: K12 -> 12, star, lone vertex, empty graph."""
+    k12 = gcol.build_graph([(u, v) for u in range(12) for v in range(u + 1, 12)], 12)
+    star = gcol.build_graph([(0, v) for v in range(1, 200)], 200)
+    lone = gcol.build_graph([], 1)
+    for g in (k12, star, lone):
+        check_run(g, gcol.color_rsoc(g, 4), 4)
+    assert gcol.color_rsoc(k12, 4).stats.num_colors == 12
+    assert gcol.color_rsoc(star, 4).stats.num_colors == 2
+    assert list(gcol.color_rsoc(lone, 1).coloring) == [0]
+    empty = gcol.build_graph([], 0)
+    run = gcol.color_rsoc(empty, 2)
+    assert run.coloring.size == 0
+    assert run.stats.rounds == 1 and run.stats.conflicts_per_round == [0]
+    assert run.stats.barrier_events == 2
+    with pytest.raises(gcol.input_error):
+        gcol.color_rsoc(k12, 0)
+
+
+def test_lockstep_pair_converges():
+    """The SIMT livelock of PAPER.md §5 (lockstep.hpp) cannot happen with a
+    tie-break: the 2-vertex graph converges in <= 2 rounds."""
+    pair = gcol.build_graph([(0, 1)], 2)
+    for prio in gcol.Priority:
+        for _ in range(20):
+            run = gcol.color_rsoc(pair, 1, gcol.ParallelOptions(priority=prio))
+            assert sorted(run.coloring) == [0, 1]
+            assert run.stats.rounds <= 2
+
+
+def random_graph(rng, n, avg):
+    m = int(n * avg / 2)
+    e = rng.integers(0, max(n, 1), size=(m, 2)) if n > 1 else np.zeros((0, 2), np.int64)
+    return gcol.build_graph(e, n)
+
+
+def test_snapshot_k1_random_and_lower(oracle_mod):
+    """K1 snapshot mode (full and lower-only neighbourhoods, whole graph and
+    worklists) bit-exact vs the oracle, with uncoloured entries and colours
+    above the degree bound in the snapshot."""
+    rng = np.random.default_rng(11)
+    for it in range(12):
+        n = int(rng.integers(2, 5000))
+        g = random_graph(rng, n, float(rng.uniform(1, 90)))
+        o = oracle_csr(oracle_mod, g)
+        deg = np.diff(g.offsets())
+        snap = np.where(rng.random(n) < 0.3, -1, rng.integers(0, deg + 3)).astype(np.int32)
+        for lower in (False, True):
+            got = gcol.tentative_snapshot(g, snap, lower_only=lower)
+            want = oracle_mod.tentative_snapshot(o, snap, lower_only=lower)
+            assert np.array_equal(got, want), (it, lower)
+            wl = rng.choice(n, size=max(1, n // 3), replace=False)
+            got = gcol.tentative_snapshot(g, snap, wl, lower_only=lower)
+            want = oracle_mod.tentative_snapshot(o, snap, wl, lower_only=lower)
+            assert np.array_equal(got, want), (it, lower, "worklist")
+
+
+def test_snapshot_window_boundaries(oracle_mod):
+    """Answers at 63/64 (thread->warp), 1023/1024 (warp->CTA) and past the
+    16384-colour CTA window."""
+    for d, fill in ((63, 63), (64, 64), (200, 64), (1023, 1023), (1024, 1024), (1500, 1024),
+                    (20000, 17000)):
+        n = d + 1
+        e = [(0, v) for v in range(1, n)]
+        g = gcol.build_graph(e, n)
+        snap = np.full(n, -1, np.int32)
+        snap[1:fill + 1] = np.arange(fill, dtype=np.int32)  # neighbours take 0..fill-1
+        got = gcol.tentative_snapshot(g, snap, [0])
+        want = oracle_mod.tentative_snapshot(oracle_csr(oracle_mod, g), snap, [0])
+        assert got[0] == want[0] == fill, (d, fill, got[0])
+
+
+def rule_detect(g, colors, pending, prio):
+    """Python restatement of the three priority rules (reference rule id_low =
+    has_conflicting_higher_neighbor, coloring.hpp:121-129)."""
+    off, adj = g.offsets(), g.adjacency()
+    deg = np.diff(off)
+    out = []
+    for v in pending:
+        cv = colors[v]
+        if cv == -1:
+            continue
+        hit = False
+        for w in adj[off[v]:off[v + 1]]:
+            if colors[w] != cv:
+                continue
+            if prio == gcol.Priority.id_low and w > v:
+                hit = True
+            elif prio == gcol.Priority.id_high and w < v:
+                hit = True
+            elif prio == gcol.Priority.degree_id and (deg[v], v) < (deg[w], w):
+                hit = True
+        if hit:
+            out.append(int(v))
+    return out
+
+
+def test_detect_all_rules_and_recolor_independent_sets(oracle_mod):
+    rng = np.random.default_rng(303)
+    for it in range(10):
+        n = int(rng.integers(2, 3000))
+        g = random_graph(rng, n, float(rng.uniform(2, 60)))
+        pal = rng.integers(-1, 3, size=n).astype(np.int32)
+        allv = list(range(n))
+        for prio in gcol.Priority:
+            assert gcol.detect_conflicts(g, pal, allv, prio) == rule_detect(g, pal, allv, prio)
+        # fused detect+recolour on an independent set is deterministic:
+        # defective members get smallest_available_color over the rest
+        o = oracle_csr(oracle_mod, g)
+        col = np.abs(pal).astype(np.int32)
+        indep, taken = [], np.zeros(n, bool)
+        for v in rng.permutation(n):
+            if not taken[v]:
+                indep.append(int(v))
+                taken[v] = True
+                taken[g.neighbors(v)] = True
+        new, rec = gcol.detect_and_recolor(g, col, indep)
+        exp = col.copy()
+        defective = oracle_mod.detect_conflicts(o, col, indep)
+        for v in defective:
+            exp[v] = oracle_mod.smallest_available_color(o, col, v)
+        assert rec == sorted(defective)
+        assert np.array_equal(new, exp)
+
+
+def test_verify_count_random(oracle_mod):
+    rng = np.random.default_rng(99)
+    for it in range(8):
+        n = int(rng.integers(1, 4000))
+        g = random_graph(rng, n, float(rng.uniform(1, 50)))
+        pal = rng.integers(-1, 4, size=n).astype(np.int32)
+        want = oracle_mod.verify_coloring(oracle_csr(oracle_mod, g), pal)
+        got = gcol.verify_coloring(g, pal)
+        assert [(v.u, v.v, v.color) for v in got.violations] == want
+        good = gcol.first_fit_sequential(g)
+        assert gcol.count_colors(good, g) == oracle_mod.count_colors(good)
+    with pytest.raises(gcol.input_error):
+        gcol.count_colors([0, -1])
+    with pytest.raises(gcol.input_error):
+        gcol.count_colors([-5])
+    assert gcol.count_colors([0, 5]) == 2
+    with pytest.raises(gcol.input_error):
+        gcol.verify_coloring(gcol.build_graph([(0, 1)], 2), [0])
+
+
+def test_rsoc_stress_random_and_rules():
+    """acceptance.cpp:82-135 analogue: properness + bounds over many shapes."""
+    rng = np.random.default_rng(97001)
+    for it in range(40):
+        n = int(10 ** rng.uniform(0.31, 5.0))
+        g = random_graph(rng, n, 2.0 + (rng.integers(0, 70) / 10.0))
+        for prio in gcol.Priority:
+            run = gcol.color_rsoc(g, 16, gcol.ParallelOptions(priority=prio))
+            check_run(g, run, 16)
+            assert run.stats.priority == prio
+
+
+@pytest.mark.parametrize("name", ["er", "tri", "stencil", "rmat24"])
+def test_rsoc_configs_scaled(oracle_mod, name):
+    """The BASELINE configs at reduced size: valid, and colour count in the
+    band of the oracle's multi-threaded RSOC on the same graph."""
+    off, cols = graphs.make_config(name, "cuda", scale_down=2 if name != "rmat24" else 6)
+    g = gcol.Graph.from_device(off, cols)
+    run = gcol.color_rsoc(g, 1)
+    hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
+    check_run(hg, run, 1)
+    o = oracle_mod.CSR(hg.offsets(), hg.adjacency())
+    counts = sorted(oracle_mod.color_parallel(o, 8, "rsoc")[1]["num_colors"] for _ in range(3))
+    ref = counts[1]
+    assert run.stats.num_colors <= int(1.05 * ref) + 2, (run.stats.num_colors, ref)
+
+
+def test_k1_read_all_variant_and_residency_knob():
+    rng = np.random.default_rng(5)
+    g = random_graph(rng, 20000, 16)
+    for opt in (gcol.ParallelOptions(k1_read_all=True), gcol.ParallelOptions(k1_blocks_per_sm=1),
+                gcol.ParallelOptions(k1_blocks_per_sm=2, priority=gcol.Priority.degree_id)):
+        check_run(g, gcol.color_rsoc(g, 1, opt), 1)
+
+
+def test_device_resident_graph_and_output():
+    off, cols = graphs.erdos_renyi(50000, 16, 3, "cuda")
+    g = gcol.Graph.from_device(off, cols)
+    out = torch.empty(50000, dtype=torch.int32, device="cuda")
+    run = gcol.color_rsoc(g, 1, colors_out=out)
+    host = out.cpu().numpy()
+    hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
+    assert gcol.verify_coloring(hg, host).ok()
+    assert run.stats.num_colors == gcol.count_colors(host)

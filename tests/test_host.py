@@ -1,0 +1,127 @@
+"""CPU: the C-ABI library, the host-side mirror of the reference interface,
+and the synthetic generators.  No compute calls are made without a GPU."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+from tests.golden_util import coloring_fixtures
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(REPO, "include", "gcol_cuda.h")).read()
+    return sorted(set(re.findall(r"^\w[\w\s\*]*?\b(gcol_cuda_\w+)\(", src, re.M)))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    from paper_1505_04086_b200 import _lib
+    syms = header_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(_lib.LIB, s), f"{s} declared in include/gcol_cuda.h but not exported"
+        assert s in _lib.SIGNATURES, f"{s} has no ctypes signature"
+    assert _lib.LIB.gcol_cuda_abi_version() == 1
+
+
+def test_struct_layouts_match_header():
+    """Field count / order of the ctypes mirrors against the C header."""
+    from paper_1505_04086_b200 import _lib
+    src = open(os.path.join(REPO, "include", "gcol_cuda.h")).read()
+
+    def fields(struct_name):
+        body = re.search(r"typedef struct \{((?:(?!typedef struct).)*?)\} " + struct_name + ";", src,
+                         re.S).group(1)
+        body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+        return re.findall(r"\b(\w+)(?:\[\d+\])?;", body)
+
+    assert fields("gcol_cuda_options") == [f for f, _ in _lib.Options._fields_]
+    assert fields("gcol_cuda_stats") == [f for f, _ in _lib.Stats._fields_]
+    assert fields("gcol_cuda_verify_report") == [f for f, _ in _lib.VerifyReport._fields_]
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device behaviour")
+def test_no_device_fails_loudly():
+    from paper_1505_04086_b200 import gcol
+    g = gcol.build_graph([(0, 1)], 2)
+    with pytest.raises(gcol.NoDeviceError):
+        gcol.color_rsoc(g, 1)
+    assert gcol.device_count() == 0
+
+
+@pytest.mark.parametrize("name", [k for k, v in coloring_fixtures().items() if "edges" in v])
+def test_build_graph_matches_reference(name):
+    """gcol.build_graph (host numpy) == the reference's build_graph CSR."""
+    from paper_1505_04086_b200 import gcol
+    case = coloring_fixtures()[name]
+    g = gcol.build_graph(case["edges"], int(case["n"][0]))
+    assert np.array_equal(g.offsets(), case["off"])
+    assert np.array_equal(g.adjacency(), case["cols"])
+    g.validate()
+    assert g.max_degree() == (int(np.diff(case["off"]).max()) if case["off"].size > 1 else 0)
+
+
+def test_build_graph_examples_and_errors():  # SPEC.md graph-core examples, graph.hpp:100-104
+    from paper_1505_04086_b200 import gcol
+    g = gcol.build_graph([], 0)
+    assert g.num_vertices() == 0 and g.max_degree() == 0
+    g = gcol.build_graph([(0, 1), (1, 0), (1, 1)], 2)
+    assert g.num_edges() == 1 and g.max_degree() == 1
+    g = gcol.build_graph([(0, 1), (1, 2), (2, 0)], 3)
+    assert all(g.degree(v) == 2 for v in range(3))
+    assert g.degree(0) == 2 and list(g.neighbors(1)) == [0, 2]
+    with pytest.raises(gcol.input_error):
+        gcol.build_graph([(0, 5)], 3)
+    with pytest.raises(gcol.input_error):
+        g.degree(3)
+
+
+def test_graph_validate_detects_corruption():  # graph.hpp:50-77
+    from paper_1505_04086_b200 import gcol
+    bad = [
+        (np.array([0, 1, 1]), np.array([1])),            # one direction only
+        (np.array([0, 1, 2]), np.array([0, 0])),         # self loop
+        (np.array([0, 2, 3, 4]), np.array([2, 1, 0, 0])),  # unsorted row
+        (np.array([0, 1, 2]), np.array([1, 5])),         # out of range
+    ]
+    for off, cols in bad:
+        with pytest.raises(gcol.input_error):
+            gcol.Graph(off, cols).validate()
+
+
+def test_generators_valid_and_deterministic():
+    from paper_1505_04086_b200 import gcol, graphs
+    for f in (lambda: graphs.erdos_renyi(3000, 16, 5), lambda: graphs.tri_mesh(30, 20, 5),
+              lambda: graphs.stencil27(9, 8, 7, 5), lambda: graphs.rmat(11, 16, .57, .19, .19, 5)):
+        o1, c1 = f()
+        o2, c2 = f()
+        assert torch.equal(o1, o2) and torch.equal(c1, c2)
+        g = gcol.Graph(o1.numpy(), c1.numpy())
+        g.validate()
+    off, cols = graphs.tri_mesh(40, 40, 1)
+    assert cols.numel() == 2 * (39 * 40 * 2 + 39 * 39) and int(torch.diff(off).max()) == 6
+    off, cols = graphs.stencil27(10, 10, 10, 1)
+    assert int(torch.diff(off).max()) == 26
+    # 13 forward directions on a 10^3 grid: 2*(3*9*100 + 6*9*9*10 + 4*9*9*9)
+    assert cols.numel() == 2 * (3 * 900 + 6 * 810 + 4 * 729)
+
+
+def test_generators_reference_build_parity(oracle_mod):
+    """Our torch CSR construction == the reference's build_graph on the same pairs."""
+    from paper_1505_04086_b200 import graphs
+    if not oracle_mod.ref_available():
+        pytest.skip("oracle/_ref not built")
+    off, cols = graphs.rmat(10, 8, .57, .19, .19, 3)
+    n = off.numel() - 1
+    # feed the upper triangle to the reference build_graph
+    rows = torch.repeat_interleave(torch.arange(n), torch.diff(off))
+    up = cols.to(torch.int64) > rows
+    e = torch.stack([rows[up], cols.to(torch.int64)[up]], 1).numpy()
+    R = oracle_mod.RefGraph.from_edges(e, n)
+    csr = R.csr()
+    assert np.array_equal(csr.off.astype(np.int64), off.numpy())
+    assert np.array_equal(csr.cols.astype(np.int32), cols.numpy())
