@@ -45,8 +45,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="tri", choices=sorted(CONFIG_WORKLOAD))
-    p.add_argument("--priority", default="id_low", choices=["id_low", "id_high", "degree_id"])
-    p.add_argument("--k1-blocks-per-sm", type=int, default=0)
+    p.add_argument("--priority", default="degree_id", choices=["id_low", "id_high", "degree_id", "ordered"])
+    p.add_argument("--k1-blocks-per-sm", type=int, default=2)
     p.add_argument("--k1-read-all", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="budget of the bounded CPU-baseline sample")

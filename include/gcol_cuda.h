@@ -63,9 +63,13 @@ typedef enum { GCOL_MEM_HOST = 0, GCOL_MEM_DEVICE = 1 } gcol_memory;
  * (coloring.hpp:118-120: "the lower-indexed endpoint is the one that
  * recolors") and the default. */
 typedef enum {
-  GCOL_PRIORITY_ID_LOW = 0,    /* reference: lower id recolors */
-  GCOL_PRIORITY_ID_HIGH = 1,   /* mirror: higher id recolors */
-  GCOL_PRIORITY_DEGREE_ID = 2  /* lower (degree, id) recolors */
+  GCOL_PRIORITY_ID_LOW = 0,    /* reference: lower id recolors (full neighbourhood) */
+  GCOL_PRIORITY_ID_HIGH = 1,   /* mirror: higher id recolors (full neighbourhood) */
+  GCOL_PRIORITY_DEGREE_ID = 2, /* lower (degree, id) recolors (full neighbourhood) */
+  GCOL_PRIORITY_ORDERED = 3    /* higher id recolors -- "only if it loses a tie to a
+                                  lower-id neighbour" -- with First-Fit over its lower
+                                  neighbours, pushing higher neighbours it now collides
+                                  with; converges towards sequential First-Fit quality */
 } gcol_priority;
 
 /* Algorithm ids follow gcol::Algorithm (parallel.hpp:21). */

@@ -27,6 +27,7 @@ GCOL_MEM_DEVICE = 1
 PRIORITY_ID_LOW = 0
 PRIORITY_ID_HIGH = 1
 PRIORITY_DEGREE_ID = 2
+PRIORITY_ORDERED = 3
 
 ALG_SEQ = 0
 ALG_CATALYUREK = 1

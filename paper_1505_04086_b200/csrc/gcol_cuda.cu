@@ -166,10 +166,10 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, cudaGraph_t* out_graph,
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   cudaGraphNode_t b_list, b_heavy, b_ctl;
   GCOL_CK(add_kernel(&b_list, body, nullptr, 0, k_list<R, false>, dim3(g->sms * 4), dim3(kBlock),
-                     g->d_off, g->d_cols, g->d_colors, g->d_ctrl, g->d_heavy));
+                     g->d_off, g->d_cols, g->d_colors, g->d_ctrl, g->d_heavy, g->d_marks));
   GCOL_CK(add_kernel(&b_heavy, body, &b_list, 1, k_heavy<R, false>, dim3(g->sms * 2),
                      dim3(kBlock), g->d_off, g->d_cols, g->d_colors, g->d_ctrl,
-                     static_cast<const int*>(g->d_heavy)));
+                     static_cast<const int*>(g->d_heavy), g->d_marks));
   GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle));
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, graph, &n_while, 1, g->ev_end));
   GCOL_CK(cudaGraphInstantiate(out_exec, graph, 0));
@@ -193,9 +193,12 @@ int get_exec(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, cudaGraphEx
   else if (rule == kIdHigh)
     rc = lower ? build_rsoc_graph<kIdHigh, true>(g, k1_blocks, &graph, &ex)
                : build_rsoc_graph<kIdHigh, false>(g, k1_blocks, &graph, &ex);
-  else
+  else if (rule == kDegId)
     rc = lower ? build_rsoc_graph<kDegId, true>(g, k1_blocks, &graph, &ex)
                : build_rsoc_graph<kDegId, false>(g, k1_blocks, &graph, &ex);
+  else
+    rc = lower ? build_rsoc_graph<kOrdered, true>(g, k1_blocks, &graph, &ex)
+               : build_rsoc_graph<kOrdered, false>(g, k1_blocks, &graph, &ex);
   if (rc != GCOL_OK) return rc;
   g->execs[key] = {graph, ex};
   *exec = ex;
@@ -336,7 +339,7 @@ int read_options(const gcol_cuda_options* in, gcol_cuda_options* o) {
   }
   if (o->thread_count < 1)
     return fail(GCOL_ERR_INVALID_ARGUMENT, "thread_count must be at least 1");  // parallel.hpp:255
-  if (o->priority < GCOL_PRIORITY_ID_LOW || o->priority > GCOL_PRIORITY_DEGREE_ID)
+  if (o->priority < GCOL_PRIORITY_ID_LOW || o->priority > GCOL_PRIORITY_ORDERED)
     return fail(GCOL_ERR_INVALID_ARGUMENT, "unknown priority rule");
   if (o->round_cap > 0x7fffffffull) o->round_cap = 0x7fffffffull;
   return GCOL_OK;
@@ -631,16 +634,17 @@ namespace {
 template <int R, bool kDetect>
 void launch_round(gcol_cuda_graph* g) {
   k_list<R, kDetect><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
-                                                            g->d_ctrl, g->d_heavy);
+                                                            g->d_ctrl, g->d_heavy, g->d_marks);
   k_heavy<R, kDetect><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
-                                                             g->d_ctrl, g->d_heavy);
+                                                             g->d_ctrl, g->d_heavy, g->d_marks);
 }
 
 template <bool kDetect>
 void launch_round_rule(gcol_cuda_graph* g, int rule) {
   if (rule == kIdLow) launch_round<kIdLow, kDetect>(g);
   else if (rule == kIdHigh) launch_round<kIdHigh, kDetect>(g);
-  else launch_round<kDegId, kDetect>(g);
+  else if (rule == kDegId) launch_round<kDegId, kDetect>(g);
+  else launch_round<kOrdered, kDetect>(g);
 }
 
 // Shared driver of the detect-only and detect-and-recolour API entries.
@@ -648,7 +652,7 @@ int run_list_api(gcol_cuda_graph* g, const int32_t* colors, const int32_t* pendi
                  int64_t npending, int32_t priority, bool detect_only, int32_t* out,
                  int64_t* nout, int32_t memory, int32_t* colors_back) {
   if (int rc = check_graph(g)) return rc;
-  if (priority < GCOL_PRIORITY_ID_LOW || priority > GCOL_PRIORITY_DEGREE_ID)
+  if (priority < GCOL_PRIORITY_ID_LOW || priority > GCOL_PRIORITY_ORDERED)
     return fail(GCOL_ERR_INVALID_ARGUMENT, "unknown priority rule");
   if (!colors) return fail(GCOL_ERR_INVALID_ARGUMENT, "null colours");
   GCOL_CK(cudaSetDevice(g->device));
@@ -667,6 +671,7 @@ int run_list_api(gcol_cuda_graph* g, const int32_t* colors, const int32_t* pendi
   }
   int* d_flags = nullptr;
   if (detect_only) GCOL_CK(dalloc(&d_flags, static_cast<size_t>(np), g->stream));
+  GCOL_CK(cudaMemsetAsync(g->d_marks, 0, sizeof(int) * n, g->stream));
   if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, d_flags, np)) return rc;
   if (np > 0) {
     if (detect_only) launch_round_rule<true>(g, priority);

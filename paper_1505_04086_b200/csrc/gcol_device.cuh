@@ -25,7 +25,18 @@ constexpr int kBWinWords = 512;         // block window: 16384 colours (2 KB)
 constexpr int kMaxRoundsRecorded = 1 << 16;
 constexpr unsigned kFull = 0xffffffffu;
 
-enum Rule : int { kIdLow = 0, kIdHigh = 1, kDegId = 2 };
+// Who recolours on a monochromatic edge, and with which neighbourhood:
+//   kIdLow   lower id recolours, full neighbourhood (reference/paper rule,
+//            coloring.hpp:118-120, Alg. 3)
+//   kIdHigh  higher id recolours, full neighbourhood (mirror)
+//   kDegId   lower (degree, id) recolours, full neighbourhood
+//   kOrdered higher id recolours ("a vertex recolours only if it loses a tie
+//            to a lower-id neighbour", BASELINE north_star) with First-Fit over
+//            its LOWER neighbours only, and pushes any higher neighbour its new
+//            colour collides with.  Converges towards sequential First-Fit;
+//            terminates because the minimum id recoloured strictly increases
+//            round over round.
+enum Rule : int { kIdLow = 0, kIdHigh = 1, kDegId = 2, kOrdered = 3 };
 
 // Device control block: round state of the on-device round loop (the GPU
 // RoundState of parallel.hpp:115-138).
@@ -39,6 +50,7 @@ struct Ctrl {
   int in_len;
   int out_len;
   int heavy_len;
+  int recolored;                    // vertices recoloured in the current round
   int round;                        // completed detect-and-recolor rounds
   int round_cap;
   int pair_overflow;
@@ -127,8 +139,16 @@ __device__ __forceinline__ void append_warp(int* list, int* len, bool pred, int 
 template <int R>
 __device__ __forceinline__ bool yields_to(int v, int dv, int w, int dw) {
   if (R == kIdLow) return v < w;             // coloring.hpp:118-120
-  if (R == kIdHigh) return v > w;
+  if (R == kIdHigh || R == kOrdered) return v > w;
   return dv < dw || (dv == dw && v < w);      // lower (degree, id) yields
+}
+
+// Neighbours w a defect test of v has to look at under rule R.
+template <int R>
+__device__ __forceinline__ bool considers(int v, int w) {
+  if (R == kIdLow) return w > v;
+  if (R == kIdHigh || R == kOrdered) return w < v;
+  return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -278,7 +298,7 @@ __device__ bool warp_defective(const long long* __restrict__ off, const int* __r
       const int i = base + u * 32 + lane;
       const bool in = i < deg;
       w[u] = in ? ld_col(cols + b + i, pol) : 0;
-      cons[u] = in && (R == kIdLow ? w[u] > v : (R == kIdHigh ? w[u] < v : true));
+      cons[u] = in && considers<R>(v, w[u]);
     }
     bool hit = false;
 #pragma unroll
@@ -311,7 +331,7 @@ __device__ bool block_defective(const long long* __restrict__ off, const int* __
       const int i = base + u * kBlock + tid;
       if (i < deg) {
         const int w = ld_col(cols + b + i, pol);
-        const bool cons = R == kIdLow ? w > v : (R == kIdHigh ? w < v : true);
+        const bool cons = considers<R>(v, w);
         if (cons && ld_color(colors + w) == cv) {
           if (R == kDegId) {
             const int dw = (int)(ld_off(off + w + 1, pol) - ld_off(off + w, pol));
@@ -337,7 +357,7 @@ __device__ bool thread_defective(const long long* __restrict__ off, const int* _
   const int dv = (int)(e - b);
   for (long long i = b; i < e; ++i) {
     const int w = ld_col(cols + i, pol);
-    const bool cons = R == kIdLow ? w > v : (R == kIdHigh ? w < v : true);
+    const bool cons = considers<R>(v, w);
     if (cons && ld_color(colors + w) == cv) {
       if (R != kDegId) return true;
       const int dw = (int)(ld_off(off + w + 1, pol) - ld_off(off + w, pol));
@@ -345,6 +365,47 @@ __device__ bool thread_defective(const long long* __restrict__ off, const int* _
     }
   }
   return false;
+}
+
+// ---------------------------------------------------------------------------
+// kOrdered push step: after v took colour c (First-Fit over its lower
+// neighbours), every higher neighbour now carrying c is appended to the next
+// worklist (once per round: marks[w] holds the round stamp of its last
+// insertion).  Warp- and CTA-cooperative versions.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool claim_slot(int* marks, int w, int stamp) {
+  return atomicMax(marks + w, stamp) < stamp;
+}
+
+__device__ void warp_push_higher(const int* __restrict__ cols, const int* colors, int v,
+                                 long long b, int deg, int c, int* marks, int stamp, int* out,
+                                 int* out_len, uint64_t pol) {
+  const int lane = lane_id();
+  for (int base = 0; base < deg; base += 32) {
+    const int i = base + lane;
+    bool pred = false;
+    int w = 0;
+    if (i < deg) {
+      w = ld_col(cols + b + i, pol);
+      if (w > v && ld_color(colors + w) == c) pred = claim_slot(marks, w, stamp);
+    }
+    append_warp(out, out_len, pred, w);
+  }
+}
+
+__device__ void block_push_higher(const int* __restrict__ cols, const int* colors, int v,
+                                  long long b, int deg, int c, int* marks, int stamp, int* out,
+                                  int* out_len, uint64_t pol) {
+  for (int base = 0; base < deg; base += kBlock) {
+    const int i = base + threadIdx.x;
+    bool pred = false;
+    int w = 0;
+    if (i < deg) {
+      w = ld_col(cols + b + i, pol);
+      if (w > v && ld_color(colors + w) == c) pred = claim_slot(marks, w, stamp);
+    }
+    append_warp(out, out_len, pred, w);
+  }
 }
 
 }  // namespace dev

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kBlock) k_candidates(const long long* __restri
         if (ld_color(colors + u) == ld_color(colors + v)) {
           if (R == kIdLow) {
             loser = u;
-          } else if (R == kIdHigh) {
+          } else if (R == kIdHigh || R == kOrdered) {
             loser = v;
           } else {
             const int du = (int)(ld_off(off + u + 1, pol) - ld_off(off + u, pol));
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(kBlock) k_candidates(const long long* __restri
 template <int R, bool kDetectOnly>
 __global__ void __launch_bounds__(kBlock) k_list(const long long* __restrict__ off,
                                                  const int* __restrict__ cols, int* colors,
-                                                 Ctrl* ctrl, int* heavy) {
+                                                 Ctrl* ctrl, int* heavy, int* marks) {
   __shared__ unsigned s_win[kWarps][32];
   const uint64_t pol = policy_evict_first();
   const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -266,11 +266,25 @@ __global__ void __launch_bounds__(kBlock) k_list(const long long* __restrict__ o
       continue;
     }
     if (d) {
-      const int c = warp_first_fit<false, false, false>(cols, colors, v, b, deg, s_win[warp], pol,
-                                                        L, dummy);
-      if (lane == 0) {
-        st_color(colors + v, c);
-        out[atomicAdd(&ctrl->out_len, 1)] = v;
+      if (R == kOrdered) {
+        const int stamp = ctrl->round + 2;  // insertion into W_{r+1}
+        const int c = warp_first_fit<false, true, false>(cols, colors, v, b, deg, s_win[warp],
+                                                         pol, L, dummy);
+        if (lane == 0) {
+          st_color(colors + v, c);
+          atomicAdd(&ctrl->recolored, 1);
+          if (claim_slot(marks, v, stamp)) out[atomicAdd(&ctrl->out_len, 1)] = v;
+        }
+        __syncwarp();
+        warp_push_higher(cols, colors, v, b, deg, c, marks, stamp, out, &ctrl->out_len, pol);
+      } else {
+        const int c = warp_first_fit<false, false, false>(cols, colors, v, b, deg, s_win[warp],
+                                                          pol, L, dummy);
+        if (lane == 0) {
+          st_color(colors + v, c);
+          atomicAdd(&ctrl->recolored, 1);
+          out[atomicAdd(&ctrl->out_len, 1)] = v;
+        }
       }
     }
   }
@@ -279,7 +293,7 @@ __global__ void __launch_bounds__(kBlock) k_list(const long long* __restrict__ o
 template <int R, bool kDetectOnly>
 __global__ void __launch_bounds__(kBlock) k_heavy(const long long* __restrict__ off,
                                                   const int* __restrict__ cols, int* colors,
-                                                  Ctrl* ctrl, const int* heavy) {
+                                                  Ctrl* ctrl, const int* heavy, int* marks) {
   __shared__ unsigned s_bwin[kBWinWords];
   __shared__ int s_red;
   const uint64_t pol = policy_evict_first();
@@ -298,11 +312,26 @@ __global__ void __launch_bounds__(kBlock) k_heavy(const long long* __restrict__ 
       continue;
     }
     if (d) {
-      const int c = block_first_fit<false, false, false>(cols, colors, v, b, deg, s_bwin, &s_red,
-                                                         pol, L, dummy);
-      if (threadIdx.x == 0) {
-        st_color(colors + v, c);
-        ctrl->out_list[atomicAdd(&ctrl->out_len, 1)] = v;
+      if (R == kOrdered) {
+        const int stamp = ctrl->round + 2;
+        const int c = block_first_fit<false, true, false>(cols, colors, v, b, deg, s_bwin, &s_red,
+                                                          pol, L, dummy);
+        if (threadIdx.x == 0) {
+          st_color(colors + v, c);
+          atomicAdd(&ctrl->recolored, 1);
+          if (claim_slot(marks, v, stamp)) ctrl->out_list[atomicAdd(&ctrl->out_len, 1)] = v;
+        }
+        __syncthreads();
+        block_push_higher(cols, colors, v, b, deg, c, marks, stamp, ctrl->out_list,
+                          &ctrl->out_len, pol);
+      } else {
+        const int c = block_first_fit<false, false, false>(cols, colors, v, b, deg, s_bwin,
+                                                           &s_red, pol, L, dummy);
+        if (threadIdx.x == 0) {
+          st_color(colors + v, c);
+          atomicAdd(&ctrl->recolored, 1);
+          ctrl->out_list[atomicAdd(&ctrl->out_len, 1)] = v;
+        }
       }
     }
   }
@@ -313,9 +342,10 @@ __global__ void __launch_bounds__(kBlock) k_heavy(const long long* __restrict__ 
 __global__ void k_control(Ctrl* ctrl, cudaGraphConditionalHandle handle) {
   const int r = ctrl->round + 1;
   ctrl->round = r;
-  const int found = ctrl->out_len;
+  const int found = ctrl->out_len;  // next worklist (recoloured + pushed)
   if (r == 1) ctrl->cand_total = ctrl->in_len;
-  if (r - 1 < kMaxRoundsRecorded) ctrl->cpr[r - 1] = (unsigned long long)found;
+  if (r - 1 < kMaxRoundsRecorded) ctrl->cpr[r - 1] = (unsigned long long)ctrl->recolored;
+  ctrl->recolored = 0;
   int* t = ctrl->in_list;
   ctrl->in_list = ctrl->out_list;
   ctrl->out_list = t;

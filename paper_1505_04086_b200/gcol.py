@@ -98,6 +98,7 @@ class Priority(enum.IntEnum):
     id_low = _lib.PRIORITY_ID_LOW        # reference rule, coloring.hpp:118-120
     id_high = _lib.PRIORITY_ID_HIGH
     degree_id = _lib.PRIORITY_DEGREE_ID
+    ordered = _lib.PRIORITY_ORDERED      # north_star rule; converges towards serial FF
 
 
 @dataclass

@@ -169,7 +169,7 @@ def rule_detect(g, colors, pending, prio):
                 continue
             if prio == gcol.Priority.id_low and w > v:
                 hit = True
-            elif prio == gcol.Priority.id_high and w < v:
+            elif prio in (gcol.Priority.id_high, gcol.Priority.ordered) and w < v:
                 hit = True
             elif prio == gcol.Priority.degree_id and (deg[v], v) < (deg[w], w):
                 hit = True
