@@ -63,10 +63,13 @@ typedef enum { GCOL_MEM_HOST = 0, GCOL_MEM_DEVICE = 1 } gcol_memory;
  * (coloring.hpp:118-120: "the lower-indexed endpoint is the one that
  * recolors") and the default. */
 typedef enum {
-  GCOL_PRIORITY_ID_LOW = 0,    /* reference: lower id recolors (full neighbourhood) */
-  GCOL_PRIORITY_ID_HIGH = 1,   /* mirror: higher id recolors (full neighbourhood) */
-  GCOL_PRIORITY_DEGREE_ID = 2, /* lower (degree, id) recolors (full neighbourhood) */
-  GCOL_PRIORITY_ORDERED = 3    /* higher id recolors -- "only if it loses a tie to a
+  GCOL_PRIORITY_DEFAULT = 0,   /* library default: DEGREE_ID (the rule that keeps the
+                                  colour count inside the reference's band at GPU
+                                  concurrency) */
+  GCOL_PRIORITY_ID_LOW = 1,    /* reference: lower id recolors (full neighbourhood) */
+  GCOL_PRIORITY_ID_HIGH = 2,   /* mirror: higher id recolors (full neighbourhood) */
+  GCOL_PRIORITY_DEGREE_ID = 3, /* lower (degree, id) recolors (full neighbourhood) */
+  GCOL_PRIORITY_ORDERED = 4    /* higher id recolors -- "only if it loses a tie to a
                                   lower-id neighbour" -- with First-Fit over its lower
                                   neighbours, pushing higher neighbours it now collides
                                   with; converges towards sequential First-Fit quality */
@@ -83,7 +86,7 @@ typedef struct {
   uint64_t chunk_size;       /* accepted for API parity; ignored on the GPU */
   uint64_t min_chunk_size;   /* accepted for API parity; ignored on the GPU */
   uint64_t round_cap;        /* 0 -> 1000 (parallel.hpp:71) */
-  int32_t priority;          /* gcol_priority, default ID_LOW */
+  int32_t priority;          /* gcol_priority; 0 = library default */
   int32_t k1_blocks_per_sm;  /* K1 residency (in-flight window) knob, 0 = auto */
   int32_t k1_read_all;       /* 0 (default): the initial pass gathers only the
                                 lower-id neighbours' colours; 1: every neighbour,

@@ -24,10 +24,11 @@ GCOL_ERR_NO_DEVICE = 7
 GCOL_MEM_HOST = 0
 GCOL_MEM_DEVICE = 1
 
-PRIORITY_ID_LOW = 0
-PRIORITY_ID_HIGH = 1
-PRIORITY_DEGREE_ID = 2
-PRIORITY_ORDERED = 3
+PRIORITY_DEFAULT = 0
+PRIORITY_ID_LOW = 1
+PRIORITY_ID_HIGH = 2
+PRIORITY_DEGREE_ID = 3
+PRIORITY_ORDERED = 4
 
 ALG_SEQ = 0
 ALG_CATALYUREK = 1

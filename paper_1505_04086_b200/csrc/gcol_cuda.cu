@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -170,11 +171,51 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, cudaGraph_t* out_graph,
   GCOL_CK(add_kernel(&b_heavy, body, &b_list, 1, k_heavy<R, false>, dim3(g->sms * 2),
                      dim3(kBlock), g->d_off, g->d_cols, g->d_colors, g->d_ctrl,
                      static_cast<const int*>(g->d_heavy), g->d_marks));
-  GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle));
+  GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle, 1));
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, graph, &n_while, 1, g->ev_end));
   GCOL_CK(cudaGraphInstantiate(out_exec, graph, 0));
   *out_graph = graph;
   return GCOL_OK;
+}
+
+// Eager (graph-less) execution of the same kernel sequence, with the round
+// loop driven from the host.  Only for profilers that cannot see into
+// conditional graph nodes (GCOL_EAGER=1); the product path is the graph.
+template <int R, bool kLower>
+int run_eager(gcol_cuda_graph* g, int k1_blocks) {
+  const int n = static_cast<int>(g->n);
+  PairLog L{g->d_pairs, g->pair_cap, &g->d_ctrl->pair_len, &g->d_ctrl->pair_overflow};
+  auto k1 = k1_tentative<false, kLower, true>;
+  const int grid1 = k1_grid(g, k1_blocks, reinterpret_cast<const void*>(k1));
+  GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
+  k1<<<grid1, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, n, nullptr, g->d_colors, g->d_colors,
+                                      g->d_ctrl, L);
+  GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
+  k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors,
+                                                         g->d_ctrl, g->d_pairs, g->pair_cap,
+                                                         g->d_marks);
+  for (;;) {
+    k_list<R, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
+                                                            g->d_ctrl, g->d_heavy, g->d_marks);
+    k_heavy<R, false><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
+                                                             g->d_ctrl, g->d_heavy, g->d_marks);
+    k_control<<<1, 1, 0, g->stream>>>(g->d_ctrl, cudaGraphConditionalHandle{}, 0);
+    GCOL_CK(cudaGetLastError());
+    int done = 0;
+    GCOL_CK(cudaMemcpyAsync(&done, &g->d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost,
+                            g->stream));
+    GCOL_CK(cudaStreamSynchronize(g->stream));
+    if (done) break;
+  }
+  GCOL_CK(cudaEventRecord(g->ev_end, g->stream));
+  return GCOL_OK;
+}
+
+int launch_eager(gcol_cuda_graph* g, int rule, int lower, int k1_blocks) {
+  if (rule == kIdLow) return lower ? run_eager<kIdLow, true>(g, k1_blocks) : run_eager<kIdLow, false>(g, k1_blocks);
+  if (rule == kIdHigh) return lower ? run_eager<kIdHigh, true>(g, k1_blocks) : run_eager<kIdHigh, false>(g, k1_blocks);
+  if (rule == kDegId) return lower ? run_eager<kDegId, true>(g, k1_blocks) : run_eager<kDegId, false>(g, k1_blocks);
+  return lower ? run_eager<kOrdered, true>(g, k1_blocks) : run_eager<kOrdered, false>(g, k1_blocks);
 }
 
 int get_exec(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, cudaGraphExec_t* exec) {
@@ -316,6 +357,9 @@ int verify_device(gcol_cuda_graph* g, const int* d_col, gcol_cuda_verify_report*
   return GCOL_OK;
 }
 
+// gcol_priority (1..4) -> device Rule (0..3)
+int rule_of(int priority) { return priority - GCOL_PRIORITY_ID_LOW; }
+
 int check_graph(const gcol_cuda_graph* g) {
   if (!g) return fail(GCOL_ERR_INVALID_ARGUMENT, "null graph handle");
   return GCOL_OK;
@@ -339,6 +383,7 @@ int read_options(const gcol_cuda_options* in, gcol_cuda_options* o) {
   }
   if (o->thread_count < 1)
     return fail(GCOL_ERR_INVALID_ARGUMENT, "thread_count must be at least 1");  // parallel.hpp:255
+  if (o->priority == GCOL_PRIORITY_DEFAULT) o->priority = GCOL_PRIORITY_DEGREE_ID;
   if (o->priority < GCOL_PRIORITY_ID_LOW || o->priority > GCOL_PRIORITY_ORDERED)
     return fail(GCOL_ERR_INVALID_ARGUMENT, "unknown priority rule");
   if (o->round_cap > 0x7fffffffull) o->round_cap = 0x7fffffffull;
@@ -471,9 +516,12 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   if (g->n > 0 && !colors_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "colors_out is null");
   GCOL_CK(cudaSetDevice(g->device));
   if (int rc = ensure_run_buffers(g)) return rc;
-  cudaGraphExec_t exec;
+  cudaGraphExec_t exec = nullptr;
   const int lower = opt.k1_read_all ? 0 : 1;
-  if (int rc = get_exec(g, opt.priority, lower, opt.k1_blocks_per_sm, &exec)) return rc;
+  const char* eager_env = std::getenv("GCOL_EAGER");
+  const bool eager = eager_env && eager_env[0] == '1';
+  if (!eager)
+    if (int rc = get_exec(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, &exec)) return rc;
   // Untimed prologue, like Coloring(n) before the reference's timer
   // (parallel.hpp:258 vs :267): colours := -1, marks := 0, control reset.
   const size_t n = static_cast<size_t>(g->n);
@@ -481,7 +529,11 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   GCOL_CK(cudaMemsetAsync(g->d_marks, 0, sizeof(int) * n, g->stream));
   if (int rc = reset_ctrl(g, static_cast<int>(opt.round_cap), g->d_listA, g->d_listB, nullptr, 0))
     return rc;
-  GCOL_CK(cudaGraphLaunch(exec, g->stream));
+  if (eager) {
+    if (int rc = launch_eager(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm)) return rc;
+  } else {
+    GCOL_CK(cudaGraphLaunch(exec, g->stream));
+  }
   // Header + conflicts_per_round back in two copies.
   Ctrl hdr;
   GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
@@ -652,6 +704,7 @@ int run_list_api(gcol_cuda_graph* g, const int32_t* colors, const int32_t* pendi
                  int64_t npending, int32_t priority, bool detect_only, int32_t* out,
                  int64_t* nout, int32_t memory, int32_t* colors_back) {
   if (int rc = check_graph(g)) return rc;
+  if (priority == GCOL_PRIORITY_DEFAULT) priority = GCOL_PRIORITY_DEGREE_ID;
   if (priority < GCOL_PRIORITY_ID_LOW || priority > GCOL_PRIORITY_ORDERED)
     return fail(GCOL_ERR_INVALID_ARGUMENT, "unknown priority rule");
   if (!colors) return fail(GCOL_ERR_INVALID_ARGUMENT, "null colours");
@@ -674,8 +727,8 @@ int run_list_api(gcol_cuda_graph* g, const int32_t* colors, const int32_t* pendi
   GCOL_CK(cudaMemsetAsync(g->d_marks, 0, sizeof(int) * n, g->stream));
   if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, d_flags, np)) return rc;
   if (np > 0) {
-    if (detect_only) launch_round_rule<true>(g, priority);
-    else launch_round_rule<false>(g, priority);
+    if (detect_only) launch_round_rule<true>(g, rule_of(priority));
+    else launch_round_rule<false>(g, rule_of(priority));
   }
   GCOL_CK(cudaGetLastError());
   if (detect_only) {

@@ -56,6 +56,7 @@ struct Ctrl {
   int pair_overflow;
   int capped;
   int cand_total;                   // round-1 candidates
+  int done;                         // loop exit flag (eager mode reads it)
   unsigned long long cpr[kMaxRoundsRecorded];  // conflicts_per_round
 };
 

@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kBlock) k_heavy(const long long* __restrict__ 
 
 // K3: one thread closes the round (finish_round, parallel.hpp:140-154) and
 // drives the graph's WHILE node.
-__global__ void k_control(Ctrl* ctrl, cudaGraphConditionalHandle handle) {
+__global__ void k_control(Ctrl* ctrl, cudaGraphConditionalHandle handle, int in_graph) {
   const int r = ctrl->round + 1;
   ctrl->round = r;
   const int found = ctrl->out_len;  // next worklist (recoloured + pushed)
@@ -357,7 +357,8 @@ __global__ void k_control(Ctrl* ctrl, cudaGraphConditionalHandle handle) {
     if (r >= ctrl->round_cap) ctrl->capped = 1;
     else cont = 1;
   }
-  cudaGraphSetConditional(handle, cont);
+  ctrl->done = cont ? 0 : 1;
+  if (in_graph) cudaGraphSetConditional(handle, cont);
 }
 
 // ---------------------------------------------------------------------------

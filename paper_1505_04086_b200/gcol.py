@@ -107,7 +107,7 @@ class ParallelOptions:
     chunk_size: int = 0
     min_chunk_size: int = 64
     round_cap: int = 1000
-    priority: Priority = Priority.id_low
+    priority: Priority = Priority.degree_id  # library default
     k1_blocks_per_sm: int = 0
     k1_read_all: bool = False
 
@@ -140,7 +140,7 @@ class ColoringStats:
     pairs_logged: int = 0
     round1_candidates: int = 0
     pair_overflow: bool = False
-    priority: Priority = Priority.id_low
+    priority: Priority = Priority.degree_id
     k1_gathers: int = 0
 
 

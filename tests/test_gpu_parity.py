@@ -244,7 +244,7 @@ def test_rsoc_configs_scaled(oracle_mod, name):
     band of the oracle's multi-threaded RSOC on the same graph."""
     off, cols = graphs.make_config(name, "cuda", scale_down=2 if name != "rmat24" else 6)
     g = gcol.Graph.from_device(off, cols)
-    run = gcol.color_rsoc(g, 1)
+    run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_blocks_per_sm=1))
     hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
     check_run(hg, run, 1)
     o = oracle_mod.CSR(hg.offsets(), hg.adjacency())
