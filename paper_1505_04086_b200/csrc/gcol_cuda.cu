@@ -83,7 +83,9 @@ struct gcol_cuda_graph {
   int* d_heavy = nullptr;
   int* d_marks = nullptr;
   int2* d_pairs = nullptr;
+  int* d_pair_counts = nullptr;
   unsigned long long pair_cap = 0;
+  int max_k1_grid = 0;
   Ctrl* d_ctrl = nullptr;
   cudaEvent_t ev_start = nullptr, ev_k1 = nullptr, ev_end = nullptr;
   std::map<ExecKey, std::pair<cudaGraph_t, cudaGraphExec_t>> execs;
@@ -122,11 +124,19 @@ int ensure_run_buffers(gcol_cuda_graph* g) {
   // handled on the device by scanning all of V.
   g->pair_cap = static_cast<unsigned long long>(g->m / 8 + (1 << 20));
   GCOL_CK(dalloc(&g->d_pairs, g->pair_cap, g->stream));
+  g->max_k1_grid = g->sms * 32;  // >= any K1 grid (occupancy <= 32 CTAs/SM)
+  GCOL_CK(dalloc(&g->d_pair_counts, static_cast<size_t>(g->max_k1_grid), g->stream));
   GCOL_CK(dalloc(&g->d_ctrl, 1, g->stream));
   GCOL_CK(cudaEventCreate(&g->ev_start));
   GCOL_CK(cudaEventCreate(&g->ev_k1));
   GCOL_CK(cudaEventCreate(&g->ev_end));
   return GCOL_OK;
+}
+
+PairLogArgs pair_args(const gcol_cuda_graph* g, int grid1) {
+  const unsigned long long per = g->pair_cap / static_cast<unsigned long long>(grid1);
+  return PairLogArgs{g->d_pairs, static_cast<int>(std::min<unsigned long long>(per, 1u << 30)),
+                     g->d_pair_counts, &g->d_ctrl->pair_overflow};
 }
 
 int k1_grid(const gcol_cuda_graph* g, int blocks_per_sm, const void* kernel) {
@@ -143,18 +153,18 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, cudaGraph_t* out_graph,
   cudaGraph_t graph;
   GCOL_CK(cudaGraphCreate(&graph, 0));
   const int n = static_cast<int>(g->n);
-  PairLog L{g->d_pairs, g->pair_cap, &g->d_ctrl->pair_len, &g->d_ctrl->pair_overflow};
   cudaGraphNode_t n_ev0, n_k1, n_ev1, n_cand, n_while, n_ev2;
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
   auto k1 = k1_tentative<false, kLower, true>;
   const int grid1 = k1_grid(g, k1_blocks, reinterpret_cast<const void*>(k1));
+  const PairLogArgs L = pair_args(g, grid1);
   GCOL_CK(add_kernel(&n_k1, graph, &n_ev0, 1, k1, dim3(grid1), dim3(kBlock), g->d_off,
                      g->d_cols, n, n, static_cast<const int*>(nullptr),
                      static_cast<const int*>(g->d_colors), g->d_colors, g->d_ctrl, L));
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev1, graph, &n_k1, 1, g->ev_k1));
   GCOL_CK(add_kernel(&n_cand, graph, &n_ev1, 1, k_candidates<R>, dim3(g->sms * 4), dim3(kBlock),
-                     g->d_off, g->d_cols, n, static_cast<const int*>(g->d_colors), g->d_ctrl,
-                     static_cast<const int2*>(g->d_pairs), g->pair_cap, g->d_marks));
+                     g->d_off, g->d_cols, n, static_cast<const int*>(g->d_colors), g->d_ctrl, L,
+                     grid1, g->d_marks));
 
   cudaGraphConditionalHandle handle;
   GCOL_CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
@@ -184,16 +194,15 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, cudaGraph_t* out_graph,
 template <int R, bool kLower>
 int run_eager(gcol_cuda_graph* g, int k1_blocks) {
   const int n = static_cast<int>(g->n);
-  PairLog L{g->d_pairs, g->pair_cap, &g->d_ctrl->pair_len, &g->d_ctrl->pair_overflow};
   auto k1 = k1_tentative<false, kLower, true>;
   const int grid1 = k1_grid(g, k1_blocks, reinterpret_cast<const void*>(k1));
+  const PairLogArgs L = pair_args(g, grid1);
   GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
   k1<<<grid1, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, n, nullptr, g->d_colors, g->d_colors,
                                       g->d_ctrl, L);
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
   k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors,
-                                                         g->d_ctrl, g->d_pairs, g->pair_cap,
-                                                         g->d_marks);
+                                                         g->d_ctrl, L, grid1, g->d_marks);
   for (;;) {
     k_list<R, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
                                                             g->d_ctrl, g->d_heavy, g->d_marks);
@@ -491,6 +500,7 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
                     static_cast<void*>(g->d_marks), static_cast<void*>(g->d_pairs),
                     static_cast<void*>(g->d_ctrl)})
       if (p) cudaFreeAsync(p, g->stream);
+    if (g->d_pair_counts) cudaFreeAsync(g->d_pair_counts, g->stream);
     cudaStreamSynchronize(g->stream);
     cudaStreamDestroy(g->stream);
   }
@@ -659,7 +669,7 @@ int gcol_cuda_tentative_snapshot(gcol_cuda_graph* g, const int32_t* colors_in,
     if (int rc = copy_in(g, d_wl, worklist, sizeof(int) * nitems, memory)) return rc;
   }
   if (int rc = reset_ctrl(g, 1, nullptr, nullptr, nullptr, 0)) return rc;
-  PairLog L{};
+  PairLogArgs L{};
   if (nitems > 0) {
     if (lower_only) {
       auto k = k1_tentative<true, true, false>;

@@ -60,10 +60,23 @@ struct Ctrl {
   unsigned long long cpr[kMaxRoundsRecorded];  // conflicts_per_round
 };
 
+// K1 observation log: every read of a lower neighbour that was still
+// uncoloured (in flight) is recorded as (u, v).  Each CTA appends to its own
+// slice of the log with a shared-memory counter, so logging never contends
+// on a global atomic; an overflowing slice sets *overflow and round 1 scans
+// all of V instead.
 struct PairLog {
+  int2* region;   // this CTA's slice
+  int cap;        // slice capacity
+  int* s_count;   // shared-memory fill counter
+  int* overflow;  // global flag
+};
+
+// Kernel-argument form of the log (the per-CTA slice is derived in-kernel).
+struct PairLogArgs {
   int2* pairs;
-  unsigned long long cap;
-  unsigned long long* len;
+  int region_cap;
+  int* counts;      // per-CTA fill counts (written at K1 exit)
   int* overflow;
 };
 
@@ -113,12 +126,12 @@ __device__ __forceinline__ void log_pairs(const PairLog& L, bool pred, int u, in
   if (!m) return;
   const int lane = lane_id();
   const int leader = __ffs(m) - 1;
-  unsigned long long base = 0;
-  if (lane == leader) base = atomicAdd(L.len, (unsigned long long)__popc(m));
+  int base = 0;
+  if (lane == leader) base = atomicAdd(L.s_count, __popc(m));
   base = __shfl_sync(kFull, base, leader);
   if (pred) {
-    const unsigned long long idx = base + __popc(m & ((1u << lane) - 1u));
-    if (idx < L.cap) L.pairs[idx] = make_int2(u, v);
+    const int idx = base + __popc(m & ((1u << lane) - 1u));
+    if (idx < L.cap) L.region[idx] = make_int2(u, v);
     else *L.overflow = 1;
   }
 }

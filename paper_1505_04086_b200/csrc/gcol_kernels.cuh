@@ -14,6 +14,46 @@ namespace gcol {
 namespace dev {
 
 // ---------------------------------------------------------------------------
+// Deferred commit (K1, in-place mode).  A small row that read a lower
+// neighbour still uncoloured does not commit at once: it parks its partial
+// forbidden mask and the ids of the in-flight neighbours in a per-CTA table,
+// and one tile later re-reads only those neighbours, which by then have
+// almost always committed.  What is still uncoloured then is logged for
+// round 1 exactly like an immediate stale read.  This keeps the initial
+// pass close to sequential First-Fit even with ~10^5 vertices in flight.
+// ---------------------------------------------------------------------------
+constexpr int kDeferPairs = 384;
+
+struct DeferTable {
+  int* dv;           // [kBlock] vertex parked in this slot, -1 = none
+  unsigned* dmask;   // [kBlock][2] 64-bit partial forbidden mask
+  unsigned char* ddeg;  // [kBlock] degree (<= 63)
+  int* du;           // [kDeferPairs] in-flight neighbour
+  unsigned char* dslot; // [kDeferPairs] owning slot
+  int* np;           // fill counter
+};
+
+// Warp-aggregated record of stale (u, slot) observations; overflow goes
+// straight to the round-1 log.  All lanes must call.
+__device__ __forceinline__ void defer_pairs(const DeferTable& D, const PairLog& L, bool pred,
+                                            int u, int v, int slot) {
+  const unsigned m = __ballot_sync(kFull, pred);
+  if (!m) return;
+  const int lane = lane_id();
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(D.np, __popc(m));
+  base = __shfl_sync(kFull, base, leader);
+  const int idx = base + __popc(m & ((1u << lane) - 1u));
+  const bool spill = pred && idx >= kDeferPairs;
+  if (pred && !spill) {
+    D.du[idx] = u;
+    D.dslot[idx] = (unsigned char)slot;
+  }
+  log_pairs(L, spill, u, v);
+}
+
+// ---------------------------------------------------------------------------
 // Small rows (1 <= deg <= 63) of one warp's 32 consecutive items: the rows'
 // adjacency is staged in shared memory with coalesced loads, then each lane
 // runs First-Fit over its own row with a 64-bit register mask.  All lanes
@@ -22,7 +62,7 @@ namespace dev {
 template <bool kSnap, bool kLower, bool kLog>
 __device__ void small_rows(const int* __restrict__ cols, const int* csrc, int* cdst, int v,
                            long long b, int deg, bool small, int* stage, uint64_t pol,
-                           const PairLog& L, unsigned& gathers) {
+                           const PairLog& L, const DeferTable& D, unsigned& gathers) {
   const int lane = lane_id();
   const int len = small ? deg : 0;
   int incl = len;
@@ -74,6 +114,7 @@ __device__ void small_rows(const int* __restrict__ cols, const int* csrc, int* c
     const int myk = mine ? len : 0;
     const int maxk = __reduce_max_sync(kFull, (unsigned)myk);
     bool active = mine;
+    bool stale_me = false;
     unsigned long long mask = 0ull;
     const int* row = stage + (excl - lo);
     for (int k = 0; k < maxk; k += 4) {
@@ -93,12 +134,52 @@ __device__ void small_rows(const int* __restrict__ cols, const int* csrc, int* c
       for (int u = 0; u < 4; ++u) {
         gathers += take[u];
         if (c[u] >= 0 && c[u] <= deg) mask |= 1ull << c[u];
-        if (kLog) log_pairs(L, take[u] && c[u] == -1 && w[u] < v, w[u], v);
+        if (kLog) {
+          const bool st = take[u] && c[u] == -1 && w[u] < v;
+          stale_me |= st;
+          defer_pairs(D, L, st, w[u], v, threadIdx.x);
+        }
       }
       if (kLower && !__any_sync(kFull, active)) break;
     }
-    if (mine) st_color(cdst + v, __ffsll((long long)~mask) - 1);
+    if (mine) {
+      if (kLog && stale_me) {  // park: commit after the recheck one tile later
+        D.dv[threadIdx.x] = v;
+        D.dmask[2 * threadIdx.x] = (unsigned)mask;
+        D.dmask[2 * threadIdx.x + 1] = (unsigned)(mask >> 32);
+        D.ddeg[threadIdx.x] = (unsigned char)deg;
+      } else {
+        st_color(cdst + v, __ffsll((long long)~mask) - 1);
+      }
+    }
     __syncwarp();
+  }
+}
+
+// Recheck and commit the rows parked in table D (all CTA threads call).
+__device__ void drain_deferred(const DeferTable& D, const PairLog& L, int* cdst) {
+  const int np = min(*D.np, kDeferPairs);
+  for (int p0 = (threadIdx.x & ~31); p0 < np; p0 += kBlock) {
+    const int p = p0 + lane_id();
+    bool still = false;
+    int u = 0, v = 0;
+    if (p < np) {
+      u = D.du[p];
+      const int slot = D.dslot[p];
+      v = D.dv[slot];
+      const int c = ld_color(cdst + u);
+      if (c >= 0 && c <= (int)D.ddeg[slot]) atomicOr(&D.dmask[2 * slot + (c >> 5)], 1u << (c & 31));
+      still = c == -1;
+    }
+    log_pairs(L, still, u, v);
+  }
+  __syncthreads();
+  const int v = D.dv[threadIdx.x];
+  if (v >= 0) {
+    const unsigned long long mask =
+        (unsigned long long)D.dmask[2 * threadIdx.x] |
+        ((unsigned long long)D.dmask[2 * threadIdx.x + 1] << 32);
+    st_color(cdst + v, __ffsll((long long)~mask) - 1);
   }
 }
 
@@ -107,32 +188,51 @@ __device__ void small_rows(const int* __restrict__ cols, const int* csrc, int* c
 // ascending order from a device cursor (the GPU analog of the reference's
 // ascending chunk claiming, parallel.hpp:76-102).  Per item the width is
 // chosen by degree: thread (<= 63), warp (<= 1023), CTA (larger).
-// In-place mode (kSnap = false) reads and writes the live colour array and
-// logs every lower neighbour it saw uncoloured (an in-flight vertex) so
-// round 1 only re-checks those edges.  Snapshot mode reads csrc, writes cdst.
+// In-place mode (kSnap = false) reads and writes the live colour array,
+// defers small rows that saw an in-flight lower neighbour (above) and logs
+// every still-stale read so round 1 only re-checks those edges.  Snapshot
+// mode reads csrc, writes cdst.
 // ---------------------------------------------------------------------------
 template <bool kSnap, bool kLower, bool kLog>
 __global__ void __launch_bounds__(kBlock) k1_tentative(const long long* __restrict__ off,
                                                        const int* __restrict__ cols, int n,
                                                        int nitems, const int* worklist,
                                                        const int* csrc, int* cdst, Ctrl* ctrl,
-                                                       PairLog L) {
+                                                       PairLogArgs LA) {
   __shared__ int s_stage[kWarps][kStage];
   __shared__ unsigned s_win[kWarps][32];
   __shared__ unsigned s_bwin[kBWinWords];
   __shared__ int s_heavy[kBlock];
-  __shared__ int s_nheavy, s_tile, s_red;
+  __shared__ int s_nheavy, s_tile, s_red, s_npairs;
   __shared__ unsigned s_gathers;
+  // deferral tables (ping-pong: filled in tile t, drained at the end of t+1)
+  __shared__ int s_dv[2][kBlock];
+  __shared__ unsigned s_dmask[2][2 * kBlock];
+  __shared__ unsigned char s_ddeg[2][kBlock];
+  __shared__ int s_du[2][kDeferPairs];
+  __shared__ unsigned char s_dslot[2][kDeferPairs];
+  __shared__ int s_dnp[2];
   const uint64_t pol = policy_evict_first();
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int ntiles = (nitems + kBlock - 1) / kBlock;
+  PairLog L{LA.pairs + (size_t)blockIdx.x * LA.region_cap, LA.region_cap, &s_npairs, LA.overflow};
+  auto table = [&](int i) {
+    return DeferTable{s_dv[i], s_dmask[i], s_ddeg[i], s_du[i], s_dslot[i], &s_dnp[i]};
+  };
   unsigned gathers = 0;
-  if (threadIdx.x == 0) s_gathers = 0;
-  for (;;) {
+  if (threadIdx.x == 0) {
+    s_gathers = 0;
+    s_npairs = 0;
+  }
+  int it = 0;
+  for (;; ++it) {
+    const DeferTable D = table(it & 1);
     if (threadIdx.x == 0) {
       s_tile = (int)atomicAdd(&ctrl->tile_cursor, 1ull);
       s_nheavy = 0;
+      s_dnp[it & 1] = 0;
     }
+    D.dv[threadIdx.x] = -1;
     __syncthreads();
     const int tile = s_tile;
     if (tile >= ntiles) break;
@@ -147,7 +247,7 @@ __global__ void __launch_bounds__(kBlock) k1_tentative(const long long* __restri
     const bool medium = valid && deg > kSmallMax && deg <= kWarpMax;
     if (valid && deg > kWarpMax) s_heavy[atomicAdd(&s_nheavy, 1)] = v;
 
-    small_rows<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, small, s_stage[warp], pol, L,
+    small_rows<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, small, s_stage[warp], pol, L, D,
                                     gathers);
 
     unsigned med = __ballot_sync(kFull, medium);
@@ -171,12 +271,20 @@ __global__ void __launch_bounds__(kBlock) k1_tentative(const long long* __restri
                                                          pol, L, gathers);
       if (threadIdx.x == 0) st_color(cdst + vh, c);
     }
+    if (kLog && it > 0) drain_deferred(table((it + 1) & 1), L, cdst);  // rows parked in tile t-1
     __syncthreads();
   }
+  if (kLog && it > 0) drain_deferred(table((it + 1) & 1), L, cdst);  // the last tile's rows
   const unsigned g = __reduce_add_sync(kFull, gathers);
   if (lane == 0 && g) atomicAdd(&s_gathers, g);
   __syncthreads();
-  if (threadIdx.x == 0 && s_gathers) atomicAdd(&ctrl->k1_gathers, (unsigned long long)s_gathers);
+  if (threadIdx.x == 0) {
+    if (s_gathers) atomicAdd(&ctrl->k1_gathers, (unsigned long long)s_gathers);
+    if (kLog) {
+      LA.counts[blockIdx.x] = min(s_npairs, LA.region_cap);
+      atomicAdd(&ctrl->pair_len, (unsigned long long)s_npairs);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -190,38 +298,38 @@ template <int R>
 __global__ void __launch_bounds__(kBlock) k_candidates(const long long* __restrict__ off,
                                                        const int* __restrict__ cols, int n,
                                                        const int* colors, Ctrl* ctrl,
-                                                       const int2* pairs,
-                                                       unsigned long long pair_cap, int* marks) {
+                                                       PairLogArgs LA, int nregions, int* marks) {
   const uint64_t pol = policy_evict_first();
   int* list = ctrl->in_list;
   int* len = &ctrl->in_len;
   const int lane = lane_id();
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   if (!ctrl->pair_overflow) {
-    unsigned long long np = ctrl->pair_len;
-    if (np > pair_cap) np = pair_cap;
-    for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
-         i0 < np; i0 += stride) {
-      const unsigned long long i = i0 + lane;
-      bool pred = false;
-      int loser = 0;
-      if (i < np) {
-        const int2 p = pairs[i];
-        const int u = min(p.x, p.y), v = max(p.x, p.y);
-        if (ld_color(colors + u) == ld_color(colors + v)) {
-          if (R == kIdLow) {
-            loser = u;
-          } else if (R == kIdHigh || R == kOrdered) {
-            loser = v;
-          } else {
-            const int du = (int)(ld_off(off + u + 1, pol) - ld_off(off + u, pol));
-            const int dv = (int)(ld_off(off + v + 1, pol) - ld_off(off + v, pol));
-            loser = yields_to<R>(u, du, v, dv) ? u : v;
+    for (int rg = blockIdx.x; rg < nregions; rg += gridDim.x) {
+      const int cnt = LA.counts[rg];
+      const int2* pairs = LA.pairs + (size_t)rg * LA.region_cap;
+      for (int i0 = (threadIdx.x & ~31); i0 < cnt; i0 += blockDim.x) {
+        const int i = i0 + lane;
+        bool pred = false;
+        int loser = 0;
+        if (i < cnt) {
+          const int2 p = pairs[i];
+          const int u = min(p.x, p.y), v = max(p.x, p.y);
+          if (ld_color(colors + u) == ld_color(colors + v)) {
+            if (R == kIdLow) {
+              loser = u;
+            } else if (R == kIdHigh || R == kOrdered) {
+              loser = v;
+            } else {
+              const int du = (int)(ld_off(off + u + 1, pol) - ld_off(off + u, pol));
+              const int dv = (int)(ld_off(off + v + 1, pol) - ld_off(off + v, pol));
+              loser = yields_to<R>(u, du, v, dv) ? u : v;
+            }
+            pred = atomicExch(marks + loser, 1) == 0;
           }
-          pred = atomicExch(marks + loser, 1) == 0;
         }
+        append_warp(list, len, pred, loser);
       }
-      append_warp(list, len, pred, loser);
     }
   } else {
     for (long long v0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); v0 < n;
