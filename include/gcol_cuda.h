@@ -92,7 +92,10 @@ typedef struct {
                                 lower-id neighbours' colours; 1: every neighbour,
                                 like smallest_available_color (coloring.hpp:95-106).
                                 Both are valid RSOC initial passes. */
-  int32_t reserved[5];
+  int32_t k1_mega_min_degree; /* rows at least this long are coloured after the rest
+                                 of the initial pass by a multi-CTA kernel reading every
+                                 neighbour; 0 = default (16384) */
+  int32_t reserved[4];
 } gcol_cuda_options;
 
 /* ColoringStats (parallel.hpp:47-57) + device-side instrumentation. */

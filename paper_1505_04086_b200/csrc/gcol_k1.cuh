@@ -1,0 +1,500 @@
+// gcol_k1.cuh -- K1, the tentative-colour pass (parallel.hpp:286-296), v3.
+//
+// Every warp is an independent worker: it pulls 32-vertex sub-tiles in
+// ascending id order (CTAs claim 256-vertex chunks from a global cursor;
+// the warps of a CTA split a chunk through one 64-bit shared-memory word
+// holding {chunk, next sub-tile}), so no CTA-wide barrier ever sits on the
+// critical path.  Per sub-tile:
+//   deg == 0          colour 0 (coloring.hpp:98-105)
+//   1 <= deg <= 63    thread per row over the adjacency staged in shared
+//                     memory with coalesced loads, 64-bit register mask;
+//                     rows that read an in-flight (uncoloured) lower
+//                     neighbour are parked and re-checked one sub-tile later
+//   64 <= deg < mega  edge-parallel across all such rows of the sub-tile,
+//                     per-row forbidden bitmaps in shared memory
+//   deg >= mega       skipped here; k1_mega colours these few hubs after
+//                     K1 with many CTAs per row, reading every neighbour
+// In the initial pass a row gathers only its LOWER neighbours' colours:
+// rows are sorted, every edge is examined by its higher endpoint, and each
+// stale read that survives the re-check is logged for round 1.
+#pragma once
+#include "gcol_device.cuh"
+
+namespace gcol {
+namespace dev {
+
+constexpr int kK1Warps = 8;
+constexpr int kK1Block = kK1Warps * 32;
+constexpr int kSubTiles = kK1Block / 32;  // sub-tiles per claimed chunk
+constexpr int kBmWords = 512;             // per-warp medium-row bitmap pool
+constexpr int kStaleMax = 4;              // stale neighbours remembered per parked row
+constexpr int kMegaDefault = 16384;       // rows >= this go to k1_mega
+
+struct K1Warp {
+  int stage[kStage];                   // staged small-row adjacency (4 KB)
+  unsigned bm[kBmWords];               // medium-row bitmaps (2 KB)
+  unsigned win[32];                    // window for the rare overflow path
+  int dv[2][32];                       // parked row per lane (ping-pong tables)
+  unsigned dmask[2][32][2];
+  unsigned char ddeg[2][32];
+  unsigned char dns[2][32];
+  int dst[2][32][kStaleMax];           // in-flight neighbours to re-check
+};
+
+struct MegaArgs {
+  const unsigned* bits;  // bitmap of rows coloured by k1_mega (nullptr: none)
+  int min_deg;           // rows with deg >= min_deg are mega rows
+};
+
+__device__ __forceinline__ bool is_mega(const MegaArgs& M, int w) {
+  return M.bits && ((__ldg(M.bits + (w >> 5)) >> (w & 31)) & 1u);
+}
+
+// First-Fit restricted to the colour window [wb, wb + 1024) (warp-wide);
+// returns -1 when the window holds no free colour <= deg.  Only used for
+// rows whose first 1024 colours are all forbidden (needs deg >= 1024).
+template <bool kSnap, bool kLower>
+__device__ int warp_ff_window(const int* __restrict__ cols, const int* csrc, int v, long long b,
+                              int deg, int wb, unsigned* win, uint64_t pol) {
+  const int lane = lane_id();
+  win[lane] = 0u;
+  __syncwarp();
+  for (int i = lane; i < deg; i += 32) {
+    const int w = ld_col(cols + b + i, pol);
+    if (kLower && w > v) break;
+    const int c = read_color<kSnap>(csrc, w);
+    if (c >= wb && c < wb + 1024 && c <= deg) atomicOr(&win[(c - wb) >> 5], 1u << ((c - wb) & 31));
+  }
+  __syncwarp();
+  const int lim = deg - wb;  // candidates wb..deg
+  const int bits_here = lim >= 1023 ? 32 : (lim < 0 ? 0 : ((lim >> 5) == lane ? (lim & 31) + 1 : (lane < (lim >> 5) ? 32 : 0)));
+  const unsigned vm = bits_here == 32 ? kFull : ((1u << bits_here) - 1u);
+  const unsigned fr = ~win[lane] & vm;
+  const unsigned nz = __ballot_sync(kFull, fr != 0u);
+  __syncwarp();
+  if (!nz) return -1;
+  const int j = __ffs(nz) - 1;
+  const unsigned fj = __shfl_sync(kFull, fr, j);
+  return wb + j * 32 + __ffs(fj) - 1;
+}
+
+// ---------------------------------------------------------------------------
+// small rows: thread per row, adjacency staged in shared memory
+// ---------------------------------------------------------------------------
+template <bool kSnap, bool kLower, bool kLog>
+__device__ void k1_small(const int* __restrict__ cols, const int* csrc, int* cdst, int v,
+                         long long b, int deg, bool small, K1Warp& W, int table, uint64_t pol,
+                         const PairLog& L, const MegaArgs& M, unsigned& gathers) {
+  const int lane = lane_id();
+  const int len = small ? deg : 0;
+  int incl = len;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const int excl = incl - len;
+  const int total = __shfl_sync(kFull, incl, 31);
+  if (total == 0) return;
+  const long long nb = __shfl_down_sync(kFull, b, 1);
+  const bool contig = __all_sync(kFull, (len == deg) && (lane == 31 || nb == b + deg));
+  const long long b0 = __shfl_sync(kFull, b, 0);
+  const int nbatch = (total + kStageStep - 1) / kStageStep;
+  for (int bt = 0; bt < nbatch; ++bt) {
+    const int lo = bt * kStageStep;
+    const bool mine = small && excl >= lo && excl < lo + kStageStep;
+    if (contig) {
+      const int hi = min(total, lo + kStage);
+      for (int i = lo + lane; i < hi; i += 32 * 4) {
+        int x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = i + u * 32;
+          x[u] = j < hi ? ld_col(cols + b0 + j, pol) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = i + u * 32;
+          if (j < hi) W.stage[j - lo] = x[u];
+        }
+      }
+    } else {
+      unsigned rows = __ballot_sync(kFull, mine);
+      while (rows) {
+        const int r = __ffs(rows) - 1;
+        rows &= rows - 1;
+        const int lr = __shfl_sync(kFull, len, r);
+        const int er = __shfl_sync(kFull, excl, r);
+        const long long br = __shfl_sync(kFull, b, r);
+        for (int t = lane; t < lr; t += 32) W.stage[er - lo + t] = ld_col(cols + br + t, pol);
+      }
+    }
+    __syncwarp();
+    const int maxk = __reduce_max_sync(kFull, (unsigned)(mine ? len : 0));
+    bool active = mine;
+    int ns = 0;
+    unsigned long long mask = 0ull;
+    const int* row = W.stage + (excl - lo);
+    for (int k = 0; k < maxk; k += 4) {
+      int w[4];
+      bool take[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool in = active && (k + u) < len;
+        w[u] = in ? row[k + u] : 0;
+        take[u] = in && (!kLower || w[u] < v);
+        if (kLower && in && w[u] > v) active = false;  // sorted row: the rest is > v
+      }
+      int c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        gathers += take[u];
+        if (c[u] >= 0 && c[u] <= deg) mask |= 1ull << c[u];
+        if (kLog) {
+          const bool st = take[u] && c[u] == -1 && w[u] < v && !is_mega(M, w[u]);
+          const bool keep = st && ns < kStaleMax;
+          if (keep) W.dst[table][lane][ns] = w[u];
+          ns += st ? 1 : 0;
+          log_pairs(L, st && !keep, w[u], v);
+        }
+      }
+      if (kLower && !__any_sync(kFull, active)) break;
+    }
+    if (mine) {
+      if (kLog && ns > 0) {  // park; committed after the re-check one sub-tile later
+        W.dv[table][lane] = v;
+        W.dmask[table][lane][0] = (unsigned)mask;
+        W.dmask[table][lane][1] = (unsigned)(mask >> 32);
+        W.ddeg[table][lane] = (unsigned char)deg;
+        W.dns[table][lane] = (unsigned char)min(ns, kStaleMax);
+      } else {
+        st_color(cdst + v, __ffsll((long long)~mask) - 1);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Re-check and commit the rows parked in `table` (warp-collective).
+__device__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L) {
+  const int lane = lane_id();
+  const int v = W.dv[table][lane];
+  const int ns = v >= 0 ? (int)W.dns[table][lane] : 0;
+  int c[kStaleMax];
+  int u[kStaleMax];
+#pragma unroll
+  for (int k = 0; k < kStaleMax; ++k) {
+    u[k] = k < ns ? W.dst[table][lane][k] : 0;
+    c[k] = k < ns ? ld_color(cdst + u[k]) : -2;
+  }
+  unsigned long long mask = 0ull;
+  int deg = 0;
+  if (v >= 0) {
+    mask = (unsigned long long)W.dmask[table][lane][0] |
+           ((unsigned long long)W.dmask[table][lane][1] << 32);
+    deg = W.ddeg[table][lane];
+  }
+#pragma unroll
+  for (int k = 0; k < kStaleMax; ++k) {
+    if (c[k] >= 0 && c[k] <= deg) mask |= 1ull << c[k];
+    log_pairs(L, k < ns && c[k] == -1, u[k], v);  // still in flight: round 1 checks it
+  }
+  if (v >= 0) {
+    st_color(cdst + v, __ffsll((long long)~mask) - 1);
+    W.dv[table][lane] = -1;
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// medium rows (64 <= deg < mega): edge-parallel over all such rows of the
+// sub-tile; per-row bitmaps of min(deg/32 + 1, 32) words in shared memory.
+// ---------------------------------------------------------------------------
+template <bool kSnap, bool kLower, bool kLog>
+__device__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cdst, int v,
+                          long long b, int deg, bool med, K1Warp& W, uint64_t pol,
+                          const PairLog& L, const MegaArgs& M, unsigned& gathers) {
+  const int lane = lane_id();
+  unsigned medmask = __ballot_sync(kFull, med);
+  while (medmask) {
+    // rows of this batch: take medium rows in lane order while their words fit
+    const int words = med ? min((deg >> 5) + 1, 32) : 0;
+    int wincl = (medmask >> lane) & 1u ? words : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(kFull, wincl, d);
+      if (lane >= d) wincl += y;
+    }
+    const bool inb = ((medmask >> lane) & 1u) && wincl <= kBmWords;
+    const unsigned batch = __ballot_sync(kFull, inb);
+    medmask &= ~batch;
+    const int woff = wincl - words;
+    const int len = inb ? deg : 0;
+    int eincl = len;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(kFull, eincl, d);
+      if (lane >= d) eincl += y;
+    }
+    const int eoff = eincl - len;
+    const int E = __shfl_sync(kFull, eincl, 31);
+    const int Wt = __shfl_sync(kFull, inb ? wincl : 0, 31 - __clz(batch));
+    for (int i = lane; i < Wt; i += 32) W.bm[i] = 0u;
+    __syncwarp();
+    for (int i0 = 0; i0 < E; i0 += 32 * 4) {
+      int w[4], r[4], vr[4], dr[4];
+      bool take[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = i0 + u * 32 + lane;
+        const bool in = idx < E;
+        // row of entry idx: largest r with eoff_r <= idx (5-step search)
+        int lo = 0;
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) {
+          const int e = __shfl_sync(kFull, eoff, lo + s);
+          if (lo + s < 32 && e <= idx) lo += s;
+        }
+        r[u] = lo;
+        const long long br = __shfl_sync(kFull, b, lo);
+        const int er = __shfl_sync(kFull, eoff, lo);
+        vr[u] = __shfl_sync(kFull, v, lo);
+        dr[u] = __shfl_sync(kFull, deg, lo);
+        w[u] = in ? ld_col(cols + br + (idx - er), pol) : 0;
+        take[u] = in && (!kLower || w[u] < vr[u]);
+      }
+      int c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        gathers += take[u];
+        const int wo = __shfl_sync(kFull, woff, r[u]);
+        const bool ok = c[u] >= 0 && c[u] <= dr[u] && c[u] < 1024;
+        if (ok) atomicOr(&W.bm[wo + (c[u] >> 5)], 1u << (c[u] & 31));
+        if (kLog) {
+          const bool st = take[u] && c[u] == -1 && !is_mega(M, w[u]);
+          log_pairs(L, st, w[u], vr[u]);
+        }
+      }
+    }
+    __syncwarp();
+    // first free colour per row
+    int color = -1;
+    if (inb) {
+      for (int k = 0; k < words; ++k) {
+        const unsigned fr = ~W.bm[woff + k];
+        if (fr) {
+          color = k * 32 + __ffs(fr) - 1;
+          break;
+        }
+      }
+      if (color > deg) color = -1;  // cannot happen: <= deg marks among deg+1 slots
+    }
+    // rows whose first 1024 colours are all taken (deg >= 1024 only)
+    unsigned over = __ballot_sync(kFull, inb && color < 0);
+    while (over) {
+      const int rr = __ffs(over) - 1;
+      over &= over - 1;
+      const int vv = __shfl_sync(kFull, v, rr);
+      const long long bb = __shfl_sync(kFull, b, rr);
+      const int dd = __shfl_sync(kFull, deg, rr);
+      int c = -1;
+      for (int wb = 1024; c < 0 && wb <= dd; wb += 1024)
+        c = warp_ff_window<kSnap, kLower>(cols, csrc, vv, bb, dd, wb, W.win, pol);
+      if (lane == rr) color = c;
+    }
+    if (inb) st_color(cdst + v, color);
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1 light kernel
+// ---------------------------------------------------------------------------
+template <bool kSnap, bool kLower, bool kLog>
+__global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict__ off,
+                                                     const int* __restrict__ cols, int n,
+                                                     int nitems, const int* worklist,
+                                                     const int* csrc, int* cdst, Ctrl* ctrl,
+                                                     PairLogArgs LA, MegaArgs M) {
+  extern __shared__ __align__(16) unsigned char k1_smem[];
+  __shared__ unsigned long long s_claim;  // {chunk << 32 | next sub-tile}
+  __shared__ int s_npairs;
+  __shared__ unsigned s_gathers;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  K1Warp& W = reinterpret_cast<K1Warp*>(k1_smem)[warp];
+  const uint64_t pol = policy_evict_first();
+  const int nchunks = (nitems + kK1Block - 1) / kK1Block;
+  if (threadIdx.x == 0) {
+    const int c0 = (int)atomicAdd(&ctrl->tile_cursor, 1ull);
+    s_claim = ((unsigned long long)(unsigned)c0 << 32);
+    s_npairs = 0;
+    s_gathers = 0;
+  }
+  W.dv[0][lane] = -1;
+  W.dv[1][lane] = -1;
+  __syncthreads();
+  PairLog L{LA.pairs + (size_t)blockIdx.x * LA.region_cap, LA.region_cap, &s_npairs, LA.overflow};
+  unsigned gathers = 0;
+  int it = 0;
+  for (;; ++it) {
+    int sub = -1;
+    if (lane == 0) {
+      for (;;) {
+        const unsigned long long x = atomicAdd(&s_claim, 1ull);
+        const int k = (int)(x & 0xffffffffu);
+        const int c = (int)(x >> 32);
+        if (c >= nchunks) break;
+        if (k < kSubTiles) {
+          sub = c * kSubTiles + k;
+          break;
+        }
+        if (k == kSubTiles) {  // first to overflow claims the next chunk for the CTA
+          const int nc = (int)atomicAdd(&ctrl->tile_cursor, 1ull);
+          atomicExch(&s_claim, ((unsigned long long)(unsigned)nc << 32) | 1ull);
+          if (nc < nchunks) sub = nc * kSubTiles;
+          break;
+        }
+        __nanosleep(20);
+      }
+    }
+    sub = __shfl_sync(kFull, sub, 0);
+    if (sub < 0) break;
+    const int table = it & 1;
+    const int item = sub * 32 + lane;
+    const bool valid = item < nitems;
+    const int v = valid ? (worklist ? worklist[item] : item) : n;
+    const long long b = ld_off(off + v, pol);
+    const long long e = valid ? ld_off(off + v + 1, pol) : b;
+    const int deg = (int)(e - b);
+    if (valid && deg == 0) st_color(cdst + v, 0);  // limit 0: only colour 0
+    const bool small = valid && deg >= 1 && deg <= kSmallMax;
+    const bool med = valid && deg > kSmallMax && deg < M.min_deg;
+    k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, small, W, table, pol, L, M,
+                                  gathers);
+    k1_medium<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, med, W, pol, L, M, gathers);
+    if (kLog && it > 0) k1_drain(W, table ^ 1, cdst, L);  // rows parked one sub-tile ago
+  }
+  if (kLog && it > 0) k1_drain(W, (it - 1) & 1, cdst, L);
+  const unsigned g = __reduce_add_sync(kFull, gathers);
+  if (lane == 0 && g) atomicAdd(&s_gathers, g);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_gathers) atomicAdd(&ctrl->k1_gathers, (unsigned long long)s_gathers);
+    if (kLog) {
+      LA.counts[blockIdx.x] = min(s_npairs, LA.region_cap);
+      atomicAdd(&ctrl->pair_len, (unsigned long long)s_npairs);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k1_mega: rows with deg >= mega, many CTAs per row.  Work items are
+// (row, chunk of kMegaChunk entries); each CTA ORs its chunk's forbidden
+// colours into the row's global bitmap, and the last CTA to finish a row
+// takes its first free colour.  In-place mode reads EVERY neighbour (these
+// rows run after all other rows committed) and logs any uncoloured read.
+// ---------------------------------------------------------------------------
+constexpr int kMegaChunk = 8192;
+constexpr int kMegaWords = kBWinWords;  // 16384 colours per row bitmap
+
+struct MegaWork {
+  const int* rows;        // mega row ids
+  const int* item_row;    // work item -> index into rows
+  const int* item_start;  // work item -> first entry offset within the row
+  const int* row_chunks;  // chunks per row
+  int nitems;
+  unsigned* gmask;        // [nrows][kMegaWords]
+  int* gdone;             // [nrows]
+};
+
+template <bool kSnap, bool kLower, bool kLog>
+__global__ void __launch_bounds__(kBlock) k1_mega(const long long* __restrict__ off,
+                                                  const int* __restrict__ cols, const int* csrc,
+                                                  int* cdst, MegaWork MW, PairLogArgs LA,
+                                                  int region0, Ctrl* ctrl) {
+  __shared__ unsigned s_win[kMegaWords];
+  __shared__ int s_last, s_red, s_npairs;
+  __shared__ unsigned s_bwin[kBWinWords];
+  const uint64_t pol = policy_evict_first();
+  if (threadIdx.x == 0) s_npairs = 0;
+  PairLog L{LA.pairs + (size_t)(region0 + blockIdx.x) * LA.region_cap, LA.region_cap, &s_npairs,
+            LA.overflow};
+  unsigned gathers = 0;
+  for (int it = blockIdx.x; it < MW.nitems; it += gridDim.x) {
+    const int ri = MW.item_row[it];
+    const int v = MW.rows[ri];
+    const long long b = ld_off(off + v, pol);
+    const int deg = (int)(ld_off(off + v + 1, pol) - b);
+    const int start = MW.item_start[it];
+    const int end = min(deg, start + kMegaChunk);
+    for (int i = threadIdx.x; i < kMegaWords; i += kBlock) s_win[i] = 0u;
+    __syncthreads();
+    for (int i0 = start; i0 < end; i0 += kBlock * 4) {
+      int w[4], c[4];
+      bool take[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kBlock + threadIdx.x;
+        const bool in = i < end;
+        w[u] = in ? ld_col(cols + b + i, pol) : 0;
+        take[u] = in && (!kSnap || !kLower || w[u] < v);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        gathers += take[u];
+        if (c[u] >= 0 && c[u] <= deg && c[u] < kMegaWords * 32)
+          atomicOr(&s_win[c[u] >> 5], 1u << (c[u] & 31));
+        if (kLog) log_pairs(L, take[u] && c[u] == -1, min(w[u], v), max(w[u], v));
+      }
+    }
+    __syncthreads();
+    unsigned* gm = MW.gmask + (size_t)ri * kMegaWords;
+    for (int i = threadIdx.x; i < kMegaWords; i += kBlock)
+      if (s_win[i]) atomicOr(gm + i, s_win[i]);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(MW.gdone + ri, 1) == MW.row_chunks[ri] - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      if (threadIdx.x == 0) s_red = INT_MAX;
+      __syncthreads();
+      const int nbits = min(deg + 1, kMegaWords * 32);
+      for (int i = threadIdx.x; i * 32 < nbits; i += kBlock) {
+        const int valid = nbits - i * 32;
+        const unsigned vm = valid >= 32 ? kFull : ((1u << valid) - 1u);
+        const unsigned fr = ~ld_color(reinterpret_cast<const int*>(gm + i)) & vm;
+        if (fr) atomicMin(&s_red, i * 32 + __ffs(fr) - 1);
+      }
+      __syncthreads();
+      int color = s_red;
+      if (color == INT_MAX) {  // >= 16384 distinct neighbour colours: windowed rescan
+        PairLog none{};
+        unsigned dummy = 0;
+        color = kLower && kSnap
+                    ? block_first_fit<kSnap, true, false>(cols, csrc, v, b, deg, s_bwin, &s_red,
+                                                          pol, none, dummy)
+                    : block_first_fit<kSnap, false, false>(cols, csrc, v, b, deg, s_bwin, &s_red,
+                                                           pol, none, dummy);
+      }
+      if (threadIdx.x == 0) st_color(cdst + v, color);
+    }
+    __syncthreads();
+  }
+  const unsigned g = __reduce_add_sync(kFull, gathers);
+  if (lane_id() == 0 && g) atomicAdd(&ctrl->k1_gathers, (unsigned long long)g);
+  __syncthreads();
+  if (kLog && threadIdx.x == 0) {
+    LA.counts[region0 + blockIdx.x] = min(s_npairs, LA.region_cap);
+    atomicAdd(&ctrl->pair_len, (unsigned long long)s_npairs);
+  }
+}
+
+}  // namespace dev
+}  // namespace gcol

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--ref-runs", type=int, default=3)
     ap.add_argument("--read-all", action="store_true")
+    ap.add_argument("--mega", nargs="+", type=int, default=[0])
     args = ap.parse_args()
     import torch
     from paper_1505_04086_b200 import gcol, graphs
@@ -49,10 +50,9 @@ def main():
             rec["threads"] = threads
             del R
         print(json.dumps(rec), flush=True)
-        for rule in args.rules:
-            for bps in args.bps:
+        for rule, bps, mega in [(r, b, mg) for r in args.rules for b in args.bps for mg in args.mega]:
                 opt = gcol.ParallelOptions(priority=gcol.Priority[rule], k1_blocks_per_sm=bps,
-                                           k1_read_all=args.read_all)
+                                           k1_read_all=args.read_all, k1_mega_min_degree=mega)
                 out = torch.empty(n, dtype=torch.int32, device="cuda")
                 gcol.color_rsoc(g, 1, opt, colors_out=out)  # warm
                 res = []
@@ -60,7 +60,7 @@ def main():
                     r = gcol.color_rsoc(g, 1, opt, colors_out=out).stats
                     res.append(r)
                 print(json.dumps({
-                    "config": cfg, "rule": rule, "bps": bps,
+                    "config": cfg, "rule": rule, "bps": bps, "mega": mega,
                     "colors": [r.num_colors for r in res], "rounds": [r.rounds for r in res],
                     "ms": [round(r.wall_time_ns / 1e6, 4) for r in res],
                     "k1_ms": [round(r.initial_pass_ns / 1e6, 4) for r in res],
