@@ -92,9 +92,9 @@ typedef struct {
                                 lower-id neighbours' colours; 1: every neighbour,
                                 like smallest_available_color (coloring.hpp:95-106).
                                 Both are valid RSOC initial passes. */
-  int32_t k1_mega_min_degree; /* rows at least this long are coloured after the rest
-                                 of the initial pass by a multi-CTA kernel reading every
-                                 neighbour; 0 = default (16384) */
+  int32_t k1_split_min_degree; /* rows at least this long are split into 1024-entry
+                                  pieces that every warp helps colour; 0 = default
+                                  (1024) */
   int32_t reserved[4];
 } gcol_cuda_options;
 

@@ -45,7 +45,7 @@ class Options(C.Structure):
         ("priority", C.c_int32),
         ("k1_blocks_per_sm", C.c_int32),
         ("k1_read_all", C.c_int32),
-        ("k1_mega_min_degree", C.c_int32),
+        ("k1_split_min_degree", C.c_int32),
         ("reserved", C.c_int32 * 4),
     ]
 

@@ -67,20 +67,18 @@ struct ExecKey {
   }
 };
 
-// Rows with deg >= min_deg, coloured by k1_mega: ids, work items (row,
-// chunk), per-row global bitmaps and finish counters, and a membership
-// bitmap so K1 readers can ignore them while they are still uncoloured.
-struct MegaPlan {
+// Long-row piece queue for one split threshold (sized so it never wraps).
+struct SplitPlan {
   int min_deg = 0;
-  int nrows = 0;
-  int nitems = 0;
-  int* d_rows = nullptr;
-  int* d_item_row = nullptr;
-  int* d_item_start = nullptr;
-  int* d_row_chunks = nullptr;
-  unsigned* d_bits = nullptr;
-  unsigned* d_gmask = nullptr;
-  int* d_gdone = nullptr;
+  int nslots = 0;
+  int npieces = 0;
+  int* d_slot_v = nullptr;
+  int* d_slot_deg = nullptr;
+  int* d_slot_left = nullptr;
+  unsigned* d_slot_bm = nullptr;
+  int2* d_q = nullptr;
+  unsigned* d_q_seq = nullptr;
+  unsigned* d_ctr = nullptr;  // [0] head, [1] tail, [2] slot counter
 };
 
 }  // namespace
@@ -107,7 +105,7 @@ struct gcol_cuda_graph {
   Ctrl* d_ctrl = nullptr;
   cudaEvent_t ev_start = nullptr, ev_k1 = nullptr, ev_end = nullptr;
   std::map<ExecKey, std::pair<cudaGraph_t, cudaGraphExec_t>> execs;
-  std::map<int, MegaPlan> megas;
+  std::map<int, SplitPlan> splits;
 };
 
 namespace {
@@ -152,106 +150,91 @@ int ensure_run_buffers(gcol_cuda_graph* g) {
   return GCOL_OK;
 }
 
-__global__ void k_collect_mega(const long long* __restrict__ off, int n, int min_deg, int* rows,
-                               int* count, unsigned* bits) {
+__global__ void k_count_long(const long long* __restrict__ off, int n, int min_deg,
+                             int piece, unsigned long long* out) {
+  unsigned long long rows = 0, pieces = 0;
   for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (long long)gridDim.x * blockDim.x) {
-    if (off[v + 1] - off[v] >= min_deg) {
-      rows[atomicAdd(count, 1)] = (int)v;
-      atomicOr(bits + (v >> 5), 1u << (v & 31));
+    const long long d = off[v + 1] - off[v];
+    if (d >= min_deg) {
+      rows++;
+      pieces += (unsigned long long)((d + piece - 1) / piece);
     }
+  }
+  if (rows) {
+    atomicAdd(out, rows);
+    atomicAdd(out + 1, pieces);
   }
 }
 
-int get_mega(gcol_cuda_graph* g, int min_deg, MegaPlan** out) {
-  auto it = g->megas.find(min_deg);
-  if (it != g->megas.end()) {
+int get_split(gcol_cuda_graph* g, int min_deg, SplitPlan** out) {
+  auto it = g->splits.find(min_deg);
+  if (it != g->splits.end()) {
     *out = &it->second;
     return GCOL_OK;
   }
-  MegaPlan P;
+  SplitPlan P;
   P.min_deg = min_deg;
-  const int n = static_cast<int>(g->n);
-  if (g->max_degree >= min_deg && n > 0) {
-    int* d_rows = nullptr;
-    int* d_count = nullptr;
-    GCOL_CK(dalloc(&P.d_bits, static_cast<size_t>(n / 32 + 1), g->stream));
-    GCOL_CK(cudaMemsetAsync(P.d_bits, 0, sizeof(unsigned) * (n / 32 + 1), g->stream));
-    GCOL_CK(dalloc(&d_rows, static_cast<size_t>(n), g->stream));
-    GCOL_CK(dalloc(&d_count, 1, g->stream));
-    GCOL_CK(cudaMemsetAsync(d_count, 0, sizeof(int), g->stream));
-    k_collect_mega<<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, n, min_deg, d_rows, d_count,
-                                                          P.d_bits);
+  if (g->max_degree >= min_deg && g->n > 0) {
+    unsigned long long* d_cnt = nullptr;
+    GCOL_CK(dalloc(&d_cnt, 2, g->stream));
+    GCOL_CK(cudaMemsetAsync(d_cnt, 0, 16, g->stream));
+    k_count_long<<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, static_cast<int>(g->n), min_deg,
+                                                        kPiece, d_cnt);
     GCOL_CK(cudaGetLastError());
-    int cnt = 0;
-    GCOL_CK(cudaMemcpyAsync(&cnt, d_count, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+    unsigned long long cnt[2] = {0, 0};
+    GCOL_CK(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, g->stream));
     GCOL_CK(cudaStreamSynchronize(g->stream));
-    std::vector<int> rows(cnt);
-    if (cnt)
-      GCOL_CK(cudaMemcpy(rows.data(), d_rows, sizeof(int) * cnt, cudaMemcpyDeviceToHost));
-    std::sort(rows.begin(), rows.end());
-    std::vector<long long> offs(cnt + 1);
-    std::vector<int> item_row, item_start, row_chunks(cnt);
-    for (int r = 0; r < cnt; ++r) {
-      long long lo = 0, hi = 0;
-      GCOL_CK(cudaMemcpy(&lo, g->d_off + rows[r], sizeof(long long), cudaMemcpyDeviceToHost));
-      GCOL_CK(cudaMemcpy(&hi, g->d_off + rows[r] + 1, sizeof(long long), cudaMemcpyDeviceToHost));
-      const int deg = static_cast<int>(hi - lo);
-      row_chunks[r] = (deg + kMegaChunk - 1) / kMegaChunk;
-      for (int c = 0; c < row_chunks[r]; ++c) {
-        item_row.push_back(r);
-        item_start.push_back(c * kMegaChunk);
-      }
-    }
-    P.nrows = cnt;
-    P.nitems = static_cast<int>(item_row.size());
-    GCOL_CK(cudaFreeAsync(d_rows, g->stream));
-    GCOL_CK(cudaFreeAsync(d_count, g->stream));
-    if (cnt) {
-      GCOL_CK(dalloc(&P.d_rows, cnt, g->stream));
-      GCOL_CK(dalloc(&P.d_row_chunks, cnt, g->stream));
-      GCOL_CK(dalloc(&P.d_item_row, P.nitems, g->stream));
-      GCOL_CK(dalloc(&P.d_item_start, P.nitems, g->stream));
-      GCOL_CK(dalloc(&P.d_gmask, static_cast<size_t>(cnt) * kMegaWords, g->stream));
-      GCOL_CK(dalloc(&P.d_gdone, cnt, g->stream));
-      GCOL_CK(cudaMemcpyAsync(P.d_rows, rows.data(), sizeof(int) * cnt, cudaMemcpyHostToDevice, g->stream));
-      GCOL_CK(cudaMemcpyAsync(P.d_row_chunks, row_chunks.data(), sizeof(int) * cnt, cudaMemcpyHostToDevice, g->stream));
-      GCOL_CK(cudaMemcpyAsync(P.d_item_row, item_row.data(), sizeof(int) * P.nitems, cudaMemcpyHostToDevice, g->stream));
-      GCOL_CK(cudaMemcpyAsync(P.d_item_start, item_start.data(), sizeof(int) * P.nitems, cudaMemcpyHostToDevice, g->stream));
-      GCOL_CK(cudaStreamSynchronize(g->stream));
-    } else {
-      GCOL_CK(cudaFreeAsync(P.d_bits, g->stream));
-      P.d_bits = nullptr;
-    }
+    GCOL_CK(cudaFreeAsync(d_cnt, g->stream));
+    P.nslots = static_cast<int>(cnt[0]);
+    P.npieces = static_cast<int>(cnt[1]);
+    GCOL_CK(dalloc(&P.d_slot_v, P.nslots, g->stream));
+    GCOL_CK(dalloc(&P.d_slot_deg, P.nslots, g->stream));
+    GCOL_CK(dalloc(&P.d_slot_left, P.nslots, g->stream));
+    GCOL_CK(dalloc(&P.d_slot_bm, static_cast<size_t>(P.nslots) * 32, g->stream));
+    GCOL_CK(dalloc(&P.d_q, P.npieces, g->stream));
+    GCOL_CK(dalloc(&P.d_q_seq, P.npieces, g->stream));
   }
-  g->megas[min_deg] = P;
-  *out = &g->megas[min_deg];
+  GCOL_CK(dalloc(&P.d_ctr, 4, g->stream));
+  g->splits[min_deg] = P;
+  *out = &g->splits[min_deg];
   return GCOL_OK;
 }
 
-void free_mega(gcol_cuda_graph* g, MegaPlan& P) {
-  for (void* p : {static_cast<void*>(P.d_rows), static_cast<void*>(P.d_item_row),
-                  static_cast<void*>(P.d_item_start), static_cast<void*>(P.d_row_chunks),
-                  static_cast<void*>(P.d_bits), static_cast<void*>(P.d_gmask),
-                  static_cast<void*>(P.d_gdone)})
+void free_split(gcol_cuda_graph* g, SplitPlan& P) {
+  for (void* p : {static_cast<void*>(P.d_slot_v), static_cast<void*>(P.d_slot_deg),
+                  static_cast<void*>(P.d_slot_left), static_cast<void*>(P.d_slot_bm),
+                  static_cast<void*>(P.d_q), static_cast<void*>(P.d_q_seq),
+                  static_cast<void*>(P.d_ctr)})
     if (p) cudaFreeAsync(p, g->stream);
 }
 
-// Everything one K1 launch needs (grids, log slices, mega work).
+// Clears the per-run queue state (untimed prologue).
+int reset_split(gcol_cuda_graph* g, const SplitPlan* P) {
+  if (!P) return GCOL_OK;
+  GCOL_CK(cudaMemsetAsync(P->d_ctr, 0, sizeof(unsigned) * 4, g->stream));
+  if (P->nslots > 0) {
+    GCOL_CK(cudaMemsetAsync(P->d_slot_bm, 0, sizeof(unsigned) * 32 * static_cast<size_t>(P->nslots),
+                            g->stream));
+    GCOL_CK(cudaMemsetAsync(P->d_q_seq, 0, sizeof(unsigned) * static_cast<size_t>(P->npieces),
+                            g->stream));
+  }
+  return GCOL_OK;
+}
+
+// Everything one K1 launch needs (grid, log slices, long-row queue).
 struct K1Launch {
-  int grid1 = 0;       // k1_light CTAs
-  int grid_mega = 0;   // k1_mega CTAs (0: no mega rows)
-  size_t smem = 0;     // k1_light dynamic shared memory
+  int grid1 = 0;
+  size_t smem = 0;
   PairLogArgs L{};
-  MegaArgs M{};
-  MegaWork MW{};
-  const MegaPlan* plan = nullptr;
+  SplitArgs S{};
+  const SplitPlan* plan = nullptr;
 };
 
 constexpr size_t kK1Smem = sizeof(K1Warp) * kK1Warps;
 
 template <bool kSnap, bool kLower, bool kLog>
-int plan_k1(gcol_cuda_graph* g, int k1_blocks, int mega_min, K1Launch* K) {
+int plan_k1(gcol_cuda_graph* g, int k1_blocks, int split_min, K1Launch* K) {
   auto k1 = k1_light<kSnap, kLower, kLog>;
   GCOL_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k1),
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -262,56 +245,36 @@ int plan_k1(gcol_cuda_graph* g, int k1_blocks, int mega_min, K1Launch* K) {
   const int bps = k1_blocks > 0 ? std::min(k1_blocks, occ) : std::min(2, occ);
   K->grid1 = g->sms * bps;
   K->smem = kK1Smem;
-  MegaPlan* P = nullptr;
-  if (mega_min < INT_MAX) {
-    if (int rc = get_mega(g, mega_min, &P)) return rc;
-  }
+  SplitPlan* P = nullptr;
+  if (int rc = get_split(g, split_min, &P)) return rc;
   K->plan = P;
-  if (P && P->nitems > 0) {
-    K->grid_mega = std::min(P->nitems, g->sms * 2);
-    K->M = MegaArgs{P->d_bits, mega_min};
-    K->MW = MegaWork{P->d_rows, P->d_item_row, P->d_item_start, P->d_row_chunks, P->nitems,
-                     P->d_gmask, P->d_gdone};
-  } else {
-    K->grid_mega = 0;
-    K->M = MegaArgs{nullptr, INT_MAX};
-  }
-  const int nregions = K->grid1 + K->grid_mega;
-  const unsigned long long per = g->pair_cap / static_cast<unsigned long long>(nregions);
+  K->S = SplitArgs{P->nslots > 0 ? split_min : INT_MAX, P->d_slot_v, P->d_slot_deg,
+                   P->d_slot_left, P->d_slot_bm, P->d_q, P->d_q_seq, P->d_ctr, P->d_ctr + 1,
+                   P->d_ctr + 2};
+  const unsigned long long per = g->pair_cap / static_cast<unsigned long long>(K->grid1);
   K->L = PairLogArgs{g->d_pairs, static_cast<int>(std::min<unsigned long long>(per, 1u << 30)),
                      g->d_pair_counts, &g->d_ctrl->pair_overflow};
   return GCOL_OK;
 }
 
-// Clears the per-run mega state (untimed prologue).
-int reset_mega(gcol_cuda_graph* g, const K1Launch& K) {
-  if (K.plan && K.plan->nrows > 0) {
-    GCOL_CK(cudaMemsetAsync(K.plan->d_gmask, 0,
-                            sizeof(unsigned) * static_cast<size_t>(K.plan->nrows) * kMegaWords,
-                            g->stream));
-    GCOL_CK(cudaMemsetAsync(K.plan->d_gdone, 0, sizeof(int) * K.plan->nrows, g->stream));
-  }
-  return GCOL_OK;
-}
-
-int mega_min_of(const gcol_cuda_options& opt) {
-  const int v = opt.k1_mega_min_degree;
-  return v > 0 ? v : kMegaDefault;
+int split_min_of(const gcol_cuda_options& opt) {
+  const int v = opt.k1_split_min_degree;
+  return v > 0 ? std::max(v, kSmallMax + 1) : kSplitDefault;
 }
 
 template <int R, bool kLower>
-int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int mega_min, cudaGraph_t* out_graph,
+int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, cudaGraph_t* out_graph,
                      cudaGraphExec_t* out_exec) {
   K1Launch K;
-  if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, mega_min, &K)) return rc;
+  if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K)) return rc;
   cudaGraph_t graph;
   GCOL_CK(cudaGraphCreate(&graph, 0));
   const int n = static_cast<int>(g->n);
-  cudaGraphNode_t n_ev0, n_k1, n_mega, n_ev1, n_cand, n_while, n_ev2;
+  cudaGraphNode_t n_ev0, n_k1, n_ev1, n_cand, n_while, n_ev2;
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
   {
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), const_cast<int*>(&n),
-                    nullptr, &g->d_colors, &g->d_colors, &g->d_ctrl, &K.L, &K.M};
+                    nullptr, &g->d_colors, &g->d_colors, &g->d_ctrl, &K.L, &K.S};
     const int* wl = nullptr;
     args[4] = &wl;
     cudaKernelNodeParams p{};
@@ -322,17 +285,10 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int mega_min, cudaGraph_
     p.kernelParams = args;
     GCOL_CK(cudaGraphAddKernelNode(&n_k1, graph, &n_ev0, 1, &p));
   }
-  cudaGraphNode_t last = n_k1;
-  if (K.grid_mega > 0) {
-    GCOL_CK(add_kernel(&n_mega, graph, &n_k1, 1, k1_mega<false, kLower, true>, dim3(K.grid_mega),
-                       dim3(kBlock), g->d_off, g->d_cols, static_cast<const int*>(g->d_colors),
-                       g->d_colors, K.MW, K.L, K.grid1, g->d_ctrl));
-    last = n_mega;
-  }
-  GCOL_CK(cudaGraphAddEventRecordNode(&n_ev1, graph, &last, 1, g->ev_k1));
+  GCOL_CK(cudaGraphAddEventRecordNode(&n_ev1, graph, &n_k1, 1, g->ev_k1));
   GCOL_CK(add_kernel(&n_cand, graph, &n_ev1, 1, k_candidates<R>, dim3(g->sms * 4), dim3(kBlock),
                      g->d_off, g->d_cols, n, static_cast<const int*>(g->d_colors), g->d_ctrl, K.L,
-                     K.grid1 + K.grid_mega, g->d_marks));
+                     K.grid1, g->d_marks));
 
   cudaGraphConditionalHandle handle;
   GCOL_CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
@@ -360,21 +316,17 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int mega_min, cudaGraph_
 // loop driven from the host.  Only for profilers that cannot see into
 // conditional graph nodes (GCOL_EAGER=1); the product path is the graph.
 template <int R, bool kLower>
-int run_eager(gcol_cuda_graph* g, int k1_blocks, int mega_min) {
+int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min) {
   K1Launch K;
-  if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, mega_min, &K)) return rc;
-  if (int rc = reset_mega(g, K)) return rc;
+  if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K)) return rc;
+  if (int rc = reset_split(g, K.plan)) return rc;
   const int n = static_cast<int>(g->n);
   GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
   k1_light<false, kLower, true><<<K.grid1, kK1Block, K.smem, g->stream>>>(
-      g->d_off, g->d_cols, n, n, nullptr, g->d_colors, g->d_colors, g->d_ctrl, K.L, K.M);
-  if (K.grid_mega > 0)
-    k1_mega<false, kLower, true><<<K.grid_mega, kBlock, 0, g->stream>>>(
-        g->d_off, g->d_cols, g->d_colors, g->d_colors, K.MW, K.L, K.grid1, g->d_ctrl);
+      g->d_off, g->d_cols, n, n, nullptr, g->d_colors, g->d_colors, g->d_ctrl, K.L, K.S);
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
   k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors,
-                                                         g->d_ctrl, K.L, K.grid1 + K.grid_mega,
-                                                         g->d_marks);
+                                                         g->d_ctrl, K.L, K.grid1, g->d_marks);
   for (;;) {
     k_list<R, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
                                                             g->d_ctrl, g->d_heavy, g->d_marks);
@@ -663,7 +615,7 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
     cudaGraphExecDestroy(kv.second.second);
     cudaGraphDestroy(kv.second.first);
   }
-  for (auto& kv : g->megas) free_mega(g, kv.second);
+  for (auto& kv : g->splits) free_split(g, kv.second);
   if (g->stream) {
     if (g->owns_csr) {
       cudaFreeAsync(g->d_off, g->stream);
@@ -704,7 +656,7 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   const int lower = opt.k1_read_all ? 0 : 1;
   const char* eager_env = std::getenv("GCOL_EAGER");
   const bool eager = eager_env && eager_env[0] == '1';
-  const int mm = mega_min_of(opt);
+  const int mm = split_min_of(opt);
   if (!eager)
     if (int rc = get_exec(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, &exec))
       return rc;
@@ -718,12 +670,9 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   if (eager) {
     if (int rc = launch_eager(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm)) return rc;
   } else {
-    auto mp = g->megas.find(mm);
-    if (mp != g->megas.end()) {
-      K1Launch K;
-      K.plan = &mp->second;
-      if (int rc = reset_mega(g, K)) return rc;
-    }
+    auto sp = g->splits.find(mm);
+    if (sp != g->splits.end())
+      if (int rc = reset_split(g, &sp->second)) return rc;
     GCOL_CK(cudaGraphLaunch(exec, g->stream));
   }
   // Header + conflicts_per_round back in two copies.
@@ -852,27 +801,18 @@ int gcol_cuda_tentative_snapshot(gcol_cuda_graph* g, const int32_t* colors_in,
   }
   if (int rc = reset_ctrl(g, 1, nullptr, nullptr, nullptr, 0)) return rc;
   if (nitems > 0) {
-    // With a worklist every row goes through k1_light (no mega split).
-    const int mm = worklist ? INT_MAX : kMegaDefault;
     K1Launch K;
-    int rc = lower_only ? plan_k1<true, true, false>(g, 0, mm, &K)
-                        : plan_k1<true, false, false>(g, 0, mm, &K);
+    int rc = lower_only ? plan_k1<true, true, false>(g, 0, kSplitDefault, &K)
+                        : plan_k1<true, false, false>(g, 0, kSplitDefault, &K);
     if (rc) return rc;
-    if (int r2 = reset_mega(g, K)) return r2;
+    if (int r2 = reset_split(g, K.plan)) return r2;
     K.L = PairLogArgs{};
-    if (lower_only) {
+    if (lower_only)
       k1_light<true, true, false><<<K.grid1, kK1Block, K.smem, g->stream>>>(
-          g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, K.L, K.M);
-      if (K.grid_mega > 0)
-        k1_mega<true, true, false><<<K.grid_mega, kBlock, 0, g->stream>>>(
-            g->d_off, g->d_cols, d_in, d_out, K.MW, K.L, K.grid1, g->d_ctrl);
-    } else {
+          g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, K.L, K.S);
+    else
       k1_light<true, false, false><<<K.grid1, kK1Block, K.smem, g->stream>>>(
-          g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, K.L, K.M);
-      if (K.grid_mega > 0)
-        k1_mega<true, false, false><<<K.grid_mega, kBlock, 0, g->stream>>>(
-            g->d_off, g->d_cols, d_in, d_out, K.MW, K.L, K.grid1, g->d_ctrl);
-    }
+          g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, K.L, K.S);
   }
   GCOL_CK(cudaGetLastError());
   if (int rc = copy_out(g, colors_out, d_out, sizeof(int) * n, memory)) return rc;

@@ -10,10 +10,14 @@
 //                     memory with coalesced loads, 64-bit register mask;
 //                     rows that read an in-flight (uncoloured) lower
 //                     neighbour are parked and re-checked one sub-tile later
-//   64 <= deg < mega  edge-parallel across all such rows of the sub-tile,
+//   64 <= deg < split edge-parallel across all such rows of the sub-tile,
 //                     per-row forbidden bitmaps in shared memory
-//   deg >= mega       skipped here; k1_mega colours these few hubs after
-//                     K1 with many CTAs per row, reading every neighbour
+//   deg >= split      split into kPiece-entry pieces pushed on a global
+//                     queue; every warp pops pieces before it takes a new
+//                     sub-tile, ORs its piece's forbidden colours into the
+//                     row's global bitmap, and the last piece commits the
+//                     colour -- so a hub is spread over the whole GPU and is
+//                     in flight only briefly, in its ascending-id position
 // In the initial pass a row gathers only its LOWER neighbours' colours:
 // rows are sorted, every edge is examined by its higher endpoint, and each
 // stale read that survives the re-check is logged for round 1.
@@ -28,7 +32,8 @@ constexpr int kK1Block = kK1Warps * 32;
 constexpr int kSubTiles = kK1Block / 32;  // sub-tiles per claimed chunk
 constexpr int kBmWords = 512;             // per-warp medium-row bitmap pool
 constexpr int kStaleMax = 4;              // stale neighbours remembered per parked row
-constexpr int kMegaDefault = 16384;       // rows >= this go to k1_mega
+constexpr int kSplitDefault = 1024;       // rows >= this are split into pieces
+constexpr int kPiece = 1024;              // entries per piece
 
 struct K1Warp {
   int stage[kStage];                   // staged small-row adjacency (4 KB)
@@ -41,14 +46,19 @@ struct K1Warp {
   int dst[2][32][kStaleMax];           // in-flight neighbours to re-check
 };
 
-struct MegaArgs {
-  const unsigned* bits;  // bitmap of rows coloured by k1_mega (nullptr: none)
-  int min_deg;           // rows with deg >= min_deg are mega rows
+// Global piece queue for long rows (sized per graph so it never wraps).
+struct SplitArgs {
+  int min_deg;          // rows with deg >= min_deg are split (INT_MAX: never)
+  int* slot_v;          // [nslots] row of each slot
+  int* slot_deg;
+  int* slot_left;       // pieces still to finish
+  unsigned* slot_bm;    // [nslots][32] forbidden colours 0..1023
+  int2* q;              // [qcap] (slot, first entry)
+  unsigned* q_seq;      // [qcap] = index + 1 once entry is published
+  unsigned* q_head;
+  unsigned* q_tail;
+  unsigned* slot_ctr;
 };
-
-__device__ __forceinline__ bool is_mega(const MegaArgs& M, int w) {
-  return M.bits && ((__ldg(M.bits + (w >> 5)) >> (w & 31)) & 1u);
-}
 
 // First-Fit restricted to the colour window [wb, wb + 1024) (warp-wide);
 // returns -1 when the window holds no free colour <= deg.  Only used for
@@ -84,7 +94,7 @@ __device__ int warp_ff_window(const int* __restrict__ cols, const int* csrc, int
 template <bool kSnap, bool kLower, bool kLog>
 __device__ void k1_small(const int* __restrict__ cols, const int* csrc, int* cdst, int v,
                          long long b, int deg, bool small, K1Warp& W, int table, uint64_t pol,
-                         const PairLog& L, const MegaArgs& M, unsigned& gathers) {
+                         const PairLog& L, unsigned& gathers) {
   const int lane = lane_id();
   const int len = small ? deg : 0;
   int incl = len;
@@ -153,7 +163,7 @@ __device__ void k1_small(const int* __restrict__ cols, const int* csrc, int* cds
         gathers += take[u];
         if (c[u] >= 0 && c[u] <= deg) mask |= 1ull << c[u];
         if (kLog) {
-          const bool st = take[u] && c[u] == -1 && w[u] < v && !is_mega(M, w[u]);
+          const bool st = take[u] && c[u] == -1 && w[u] < v;
           const bool keep = st && ns < kStaleMax;
           if (keep) W.dst[table][lane][ns] = w[u];
           ns += st ? 1 : 0;
@@ -215,7 +225,7 @@ __device__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L) {
 template <bool kSnap, bool kLower, bool kLog>
 __device__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cdst, int v,
                           long long b, int deg, bool med, K1Warp& W, uint64_t pol,
-                          const PairLog& L, const MegaArgs& M, unsigned& gathers) {
+                          const PairLog& L, unsigned& gathers) {
   const int lane = lane_id();
   unsigned medmask = __ballot_sync(kFull, med);
   while (medmask) {
@@ -275,7 +285,7 @@ __device__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cd
         const bool ok = c[u] >= 0 && c[u] <= dr[u] && c[u] < 1024;
         if (ok) atomicOr(&W.bm[wo + (c[u] >> 5)], 1u << (c[u] & 31));
         if (kLog) {
-          const bool st = take[u] && c[u] == -1 && !is_mega(M, w[u]);
+          const bool st = take[u] && c[u] == -1;
           log_pairs(L, st, w[u], vr[u]);
         }
       }
@@ -312,14 +322,152 @@ __device__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cd
 }
 
 // ---------------------------------------------------------------------------
-// K1 light kernel
+// long rows: producer side (warp that meets the row) and piece processing
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned r;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  return r;
+}
+
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+// Publish the pieces of every long row of this sub-tile (warp-collective).
+__device__ void k1_push_long(const SplitArgs& S, int v, int deg, bool islong) {
+  const int lane = lane_id();
+  unsigned rows = __ballot_sync(kFull, islong);
+  while (rows) {
+    const int r = __ffs(rows) - 1;
+    rows &= rows - 1;
+    const int vr = __shfl_sync(kFull, v, r);
+    const int dr = __shfl_sync(kFull, deg, r);
+    const int np = (dr + kPiece - 1) / kPiece;
+    unsigned slot = 0, t = 0;
+    if (lane == 0) {
+      slot = atomicAdd(S.slot_ctr, 1u);
+      S.slot_v[slot] = vr;
+      S.slot_deg[slot] = dr;
+      S.slot_left[slot] = np;
+      t = atomicAdd(S.q_tail, (unsigned)np);
+    }
+    slot = __shfl_sync(kFull, slot, 0);
+    t = __shfl_sync(kFull, t, 0);
+    for (int i = lane; i < np; i += 32) S.q[t + i] = make_int2((int)slot, i * kPiece);
+    __threadfence();
+    __syncwarp();
+    for (int i = lane; i < np; i += 32) st_release_u32(S.q_seq + t + i, t + i + 1);
+  }
+}
+
+// Pop one piece (lane 0 decides, result broadcast); false when the queue is
+// momentarily empty.
+__device__ bool k1_pop(const SplitArgs& S, int& slot, int& start) {
+  int ok = 0, sl = 0, st = 0;
+  if (lane_id() == 0) {
+    unsigned h = ld_acquire_u32(S.q_head);
+    while (h < ld_acquire_u32(S.q_tail)) {
+      const unsigned old = atomicCAS(S.q_head, h, h + 1);
+      if (old == h) {
+        while (ld_acquire_u32(S.q_seq + h) != h + 1) __nanosleep(32);
+        const int2 e = S.q[h];
+        sl = e.x;
+        st = e.y;
+        ok = 1;
+        break;
+      }
+      h = old;
+    }
+  }
+  ok = __shfl_sync(kFull, ok, 0);
+  slot = __shfl_sync(kFull, sl, 0);
+  start = __shfl_sync(kFull, st, 0);
+  return ok != 0;
+}
+
+template <bool kSnap, bool kLower, bool kLog>
+__device__ void k1_piece(const long long* __restrict__ off, const int* __restrict__ cols,
+                         const int* csrc, int* cdst, const SplitArgs& S, int slot, int start,
+                         K1Warp& W, uint64_t pol, const PairLog& L, unsigned& gathers) {
+  constexpr int U = 8;
+  const int lane = lane_id();
+  const int v = S.slot_v[slot];
+  const int deg = S.slot_deg[slot];
+  const long long b = ld_off(off + v, pol);
+  const int end = min(deg, start + kPiece);
+  W.win[lane] = 0u;
+  __syncwarp();
+  unsigned long long reg = 0ull;
+  // a piece that starts above v holds no lower neighbour (sorted row)
+  const bool skip = kLower && ld_col(cols + b + start, pol) > v;
+  if (!skip) {
+    for (int i0 = start; i0 < end; i0 += 32 * U) {
+      int w[U], c[U];
+      bool take[U];
+      bool past = false;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * 32 + lane;
+        const bool in = i < end;
+        w[u] = in ? ld_col(cols + b + i, pol) : 0;
+        take[u] = in && (!kLower || w[u] < v);
+        past |= kLower && in && w[u] > v;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        gathers += take[u];
+        if (c[u] >= 0 && c[u] <= deg) {
+          if (c[u] < 64) reg |= 1ull << c[u];
+          else if (c[u] < 1024) atomicOr(&W.win[c[u] >> 5], 1u << (c[u] & 31));
+        }
+        if (kLog) log_pairs(L, take[u] && c[u] == -1, w[u], v);
+      }
+      if (kLower && __any_sync(kFull, past)) break;
+    }
+  }
+  const unsigned lo = __reduce_or_sync(kFull, (unsigned)reg);
+  const unsigned hi = __reduce_or_sync(kFull, (unsigned)(reg >> 32));
+  __syncwarp();
+  unsigned word = W.win[lane];
+  if (lane == 0) word |= lo;
+  if (lane == 1) word |= hi;
+  if (word) atomicOr(S.slot_bm + (size_t)slot * 32 + lane, word);
+  __threadfence();
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) last = atomicSub(S.slot_left + slot, 1) == 1;
+  last = __shfl_sync(kFull, last, 0);
+  if (last) {
+    __threadfence();
+    const unsigned wd = ld_acquire_u32(S.slot_bm + (size_t)slot * 32 + lane);
+    const unsigned fr = ~wd;  // deg >= 1024: every bit of window 0 is a candidate
+    const unsigned nz = __ballot_sync(kFull, fr != 0u);
+    int color;
+    if (nz) {
+      const int j = __ffs(nz) - 1;
+      color = j * 32 + __ffs(__shfl_sync(kFull, fr, j)) - 1;
+    } else {  // 1024 distinct lower colours: scan the next windows
+      color = -1;
+      for (int wb = 1024; color < 0 && wb <= deg; wb += 1024)
+        color = warp_ff_window<kSnap, kLower>(cols, csrc, v, b, deg, wb, W.win, pol);
+    }
+    if (lane == 0) st_color(cdst + v, color);
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// K1 kernel
 // ---------------------------------------------------------------------------
 template <bool kSnap, bool kLower, bool kLog>
 __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict__ off,
                                                      const int* __restrict__ cols, int n,
                                                      int nitems, const int* worklist,
                                                      const int* csrc, int* cdst, Ctrl* ctrl,
-                                                     PairLogArgs LA, MegaArgs M) {
+                                                     PairLogArgs LA, SplitArgs S) {
   extern __shared__ __align__(16) unsigned char k1_smem[];
   __shared__ unsigned long long s_claim;  // {chunk << 32 | next sub-tile}
   __shared__ int s_npairs;
@@ -341,6 +489,9 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
   unsigned gathers = 0;
   int it = 0;
   for (;; ++it) {
+    int pslot, pstart;
+    while (k1_pop(S, pslot, pstart))  // long-row pieces first
+      k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L, gathers);
     int sub = -1;
     if (lane == 0) {
       for (;;) {
@@ -372,13 +523,18 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
     const int deg = (int)(e - b);
     if (valid && deg == 0) st_color(cdst + v, 0);  // limit 0: only colour 0
     const bool small = valid && deg >= 1 && deg <= kSmallMax;
-    const bool med = valid && deg > kSmallMax && deg < M.min_deg;
-    k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, small, W, table, pol, L, M,
-                                  gathers);
-    k1_medium<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, med, W, pol, L, M, gathers);
+    const bool med = valid && deg > kSmallMax && deg < S.min_deg;
+    k1_push_long(S, v, deg, valid && deg >= S.min_deg);
+    k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, small, W, table, pol, L, gathers);
+    k1_medium<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, med, W, pol, L, gathers);
     if (kLog && it > 0) k1_drain(W, table ^ 1, cdst, L);  // rows parked one sub-tile ago
   }
   if (kLog && it > 0) k1_drain(W, (it - 1) & 1, cdst, L);
+  {
+    int pslot, pstart;
+    while (k1_pop(S, pslot, pstart))  // drain what other warps published
+      k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L, gathers);
+  }
   const unsigned g = __reduce_add_sync(kFull, gathers);
   if (lane == 0 && g) atomicAdd(&s_gathers, g);
   __syncthreads();
@@ -388,111 +544,6 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
       LA.counts[blockIdx.x] = min(s_npairs, LA.region_cap);
       atomicAdd(&ctrl->pair_len, (unsigned long long)s_npairs);
     }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// k1_mega: rows with deg >= mega, many CTAs per row.  Work items are
-// (row, chunk of kMegaChunk entries); each CTA ORs its chunk's forbidden
-// colours into the row's global bitmap, and the last CTA to finish a row
-// takes its first free colour.  In-place mode reads EVERY neighbour (these
-// rows run after all other rows committed) and logs any uncoloured read.
-// ---------------------------------------------------------------------------
-constexpr int kMegaChunk = 8192;
-constexpr int kMegaWords = kBWinWords;  // 16384 colours per row bitmap
-
-struct MegaWork {
-  const int* rows;        // mega row ids
-  const int* item_row;    // work item -> index into rows
-  const int* item_start;  // work item -> first entry offset within the row
-  const int* row_chunks;  // chunks per row
-  int nitems;
-  unsigned* gmask;        // [nrows][kMegaWords]
-  int* gdone;             // [nrows]
-};
-
-template <bool kSnap, bool kLower, bool kLog>
-__global__ void __launch_bounds__(kBlock) k1_mega(const long long* __restrict__ off,
-                                                  const int* __restrict__ cols, const int* csrc,
-                                                  int* cdst, MegaWork MW, PairLogArgs LA,
-                                                  int region0, Ctrl* ctrl) {
-  __shared__ unsigned s_win[kMegaWords];
-  __shared__ int s_last, s_red, s_npairs;
-  __shared__ unsigned s_bwin[kBWinWords];
-  const uint64_t pol = policy_evict_first();
-  if (threadIdx.x == 0) s_npairs = 0;
-  PairLog L{LA.pairs + (size_t)(region0 + blockIdx.x) * LA.region_cap, LA.region_cap, &s_npairs,
-            LA.overflow};
-  unsigned gathers = 0;
-  for (int it = blockIdx.x; it < MW.nitems; it += gridDim.x) {
-    const int ri = MW.item_row[it];
-    const int v = MW.rows[ri];
-    const long long b = ld_off(off + v, pol);
-    const int deg = (int)(ld_off(off + v + 1, pol) - b);
-    const int start = MW.item_start[it];
-    const int end = min(deg, start + kMegaChunk);
-    for (int i = threadIdx.x; i < kMegaWords; i += kBlock) s_win[i] = 0u;
-    __syncthreads();
-    for (int i0 = start; i0 < end; i0 += kBlock * 4) {
-      int w[4], c[4];
-      bool take[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * kBlock + threadIdx.x;
-        const bool in = i < end;
-        w[u] = in ? ld_col(cols + b + i, pol) : 0;
-        take[u] = in && (!kSnap || !kLower || w[u] < v);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        gathers += take[u];
-        if (c[u] >= 0 && c[u] <= deg && c[u] < kMegaWords * 32)
-          atomicOr(&s_win[c[u] >> 5], 1u << (c[u] & 31));
-        if (kLog) log_pairs(L, take[u] && c[u] == -1, min(w[u], v), max(w[u], v));
-      }
-    }
-    __syncthreads();
-    unsigned* gm = MW.gmask + (size_t)ri * kMegaWords;
-    for (int i = threadIdx.x; i < kMegaWords; i += kBlock)
-      if (s_win[i]) atomicOr(gm + i, s_win[i]);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(MW.gdone + ri, 1) == MW.row_chunks[ri] - 1;
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      if (threadIdx.x == 0) s_red = INT_MAX;
-      __syncthreads();
-      const int nbits = min(deg + 1, kMegaWords * 32);
-      for (int i = threadIdx.x; i * 32 < nbits; i += kBlock) {
-        const int valid = nbits - i * 32;
-        const unsigned vm = valid >= 32 ? kFull : ((1u << valid) - 1u);
-        const unsigned fr = ~ld_color(reinterpret_cast<const int*>(gm + i)) & vm;
-        if (fr) atomicMin(&s_red, i * 32 + __ffs(fr) - 1);
-      }
-      __syncthreads();
-      int color = s_red;
-      if (color == INT_MAX) {  // >= 16384 distinct neighbour colours: windowed rescan
-        PairLog none{};
-        unsigned dummy = 0;
-        color = kLower && kSnap
-                    ? block_first_fit<kSnap, true, false>(cols, csrc, v, b, deg, s_bwin, &s_red,
-                                                          pol, none, dummy)
-                    : block_first_fit<kSnap, false, false>(cols, csrc, v, b, deg, s_bwin, &s_red,
-                                                           pol, none, dummy);
-      }
-      if (threadIdx.x == 0) st_color(cdst + v, color);
-    }
-    __syncthreads();
-  }
-  const unsigned g = __reduce_add_sync(kFull, gathers);
-  if (lane_id() == 0 && g) atomicAdd(&ctrl->k1_gathers, (unsigned long long)g);
-  __syncthreads();
-  if (kLog && threadIdx.x == 0) {
-    LA.counts[region0 + blockIdx.x] = min(s_npairs, LA.region_cap);
-    atomicAdd(&ctrl->pair_len, (unsigned long long)s_npairs);
   }
 }
 

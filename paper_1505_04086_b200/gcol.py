@@ -110,7 +110,7 @@ class ParallelOptions:
     priority: Priority = Priority.degree_id  # library default
     k1_blocks_per_sm: int = 0
     k1_read_all: bool = False
-    k1_mega_min_degree: int = 0
+    k1_split_min_degree: int = 0
 
     def to_c(self, thread_count: int) -> _lib.Options:
         o = _lib.Options()
@@ -122,7 +122,7 @@ class ParallelOptions:
         o.priority = int(self.priority)
         o.k1_blocks_per_sm = self.k1_blocks_per_sm
         o.k1_read_all = 1 if self.k1_read_all else 0
-        o.k1_mega_min_degree = self.k1_mega_min_degree
+        o.k1_split_min_degree = self.k1_split_min_degree
         return o
 
 
