@@ -78,7 +78,7 @@ struct SplitPlan {
   unsigned* d_slot_bm = nullptr;
   int2* d_q = nullptr;
   unsigned* d_q_seq = nullptr;
-  unsigned* d_ctr = nullptr;  // [0] head, [1] tail, [2] slot counter
+  unsigned* d_ctr = nullptr;  // [0] pieces allocated, [1] slots, [2] live warps
 };
 
 }  // namespace
@@ -106,6 +106,7 @@ struct gcol_cuda_graph {
   cudaEvent_t ev_start = nullptr, ev_k1 = nullptr, ev_end = nullptr;
   std::map<ExecKey, std::pair<cudaGraph_t, cudaGraphExec_t>> execs;
   std::map<int, SplitPlan> splits;
+  std::map<cudaGraphExec_t, int> k1_warps;  // K1 warps of each instantiated graph
 };
 
 namespace {
@@ -209,10 +210,11 @@ void free_split(gcol_cuda_graph* g, SplitPlan& P) {
     if (p) cudaFreeAsync(p, g->stream);
 }
 
-// Clears the per-run queue state (untimed prologue).
-int reset_split(gcol_cuda_graph* g, const SplitPlan* P) {
+// Clears the per-run queue state (untimed prologue); `warps` = K1 warps.
+int reset_split(gcol_cuda_graph* g, const SplitPlan* P, int warps) {
   if (!P) return GCOL_OK;
-  GCOL_CK(cudaMemsetAsync(P->d_ctr, 0, sizeof(unsigned) * 4, g->stream));
+  const unsigned init[4] = {0u, 0u, static_cast<unsigned>(warps), 0u};
+  GCOL_CK(cudaMemcpyAsync(P->d_ctr, init, sizeof init, cudaMemcpyHostToDevice, g->stream));
   if (P->nslots > 0) {
     GCOL_CK(cudaMemsetAsync(P->d_slot_bm, 0, sizeof(unsigned) * 32 * static_cast<size_t>(P->nslots),
                             g->stream));
@@ -250,7 +252,7 @@ int plan_k1(gcol_cuda_graph* g, int k1_blocks, int split_min, K1Launch* K) {
   K->plan = P;
   K->S = SplitArgs{P->nslots > 0 ? split_min : INT_MAX, P->d_slot_v, P->d_slot_deg,
                    P->d_slot_left, P->d_slot_bm, P->d_q, P->d_q_seq, P->d_ctr, P->d_ctr + 1,
-                   P->d_ctr + 2};
+                   reinterpret_cast<int*>(P->d_ctr + 2), K->grid1};
   const unsigned long long per = g->pair_cap / static_cast<unsigned long long>(K->grid1);
   K->L = PairLogArgs{g->d_pairs, static_cast<int>(std::min<unsigned long long>(per, 1u << 30)),
                      g->d_pair_counts, &g->d_ctrl->pair_overflow};
@@ -308,6 +310,7 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, cudaGraph
   GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle, 1));
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, graph, &n_while, 1, g->ev_end));
   GCOL_CK(cudaGraphInstantiate(out_exec, graph, 0));
+  g->k1_warps[*out_exec] = K.grid1 * kK1Warps;
   *out_graph = graph;
   return GCOL_OK;
 }
@@ -319,7 +322,7 @@ template <int R, bool kLower>
 int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min) {
   K1Launch K;
   if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K)) return rc;
-  if (int rc = reset_split(g, K.plan)) return rc;
+  if (int rc = reset_split(g, K.plan, K.grid1 * kK1Warps)) return rc;
   const int n = static_cast<int>(g->n);
   GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
   k1_light<false, kLower, true><<<K.grid1, kK1Block, K.smem, g->stream>>>(
@@ -672,7 +675,7 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   } else {
     auto sp = g->splits.find(mm);
     if (sp != g->splits.end())
-      if (int rc = reset_split(g, &sp->second)) return rc;
+      if (int rc = reset_split(g, &sp->second, g->k1_warps[exec])) return rc;
     GCOL_CK(cudaGraphLaunch(exec, g->stream));
   }
   // Header + conflicts_per_round back in two copies.
@@ -805,7 +808,7 @@ int gcol_cuda_tentative_snapshot(gcol_cuda_graph* g, const int32_t* colors_in,
     int rc = lower_only ? plan_k1<true, true, false>(g, 0, kSplitDefault, &K)
                         : plan_k1<true, false, false>(g, 0, kSplitDefault, &K);
     if (rc) return rc;
-    if (int r2 = reset_split(g, K.plan)) return r2;
+    if (int r2 = reset_split(g, K.plan, K.grid1 * kK1Warps)) return r2;
     K.L = PairLogArgs{};
     if (lower_only)
       k1_light<true, true, false><<<K.grid1, kK1Block, K.smem, g->stream>>>(

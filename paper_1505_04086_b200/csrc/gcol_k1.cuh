@@ -46,18 +46,22 @@ struct K1Warp {
   int dst[2][32][kStaleMax];           // in-flight neighbours to re-check
 };
 
-// Global piece queue for long rows (sized per graph so it never wraps).
+// Long-row pieces.  Piece p (global allocation order) is delivered to the
+// mailbox of CTA p % G; each CTA drains its own mailbox with a shared-memory
+// head, so no global atomic is contended by consumers.  Sized per graph so
+// the arrays never wrap.
 struct SplitArgs {
   int min_deg;          // rows with deg >= min_deg are split (INT_MAX: never)
   int* slot_v;          // [nslots] row of each slot
   int* slot_deg;
   int* slot_left;       // pieces still to finish
   unsigned* slot_bm;    // [nslots][32] forbidden colours 0..1023
-  int2* q;              // [qcap] (slot, first entry)
-  unsigned* q_seq;      // [qcap] = index + 1 once entry is published
-  unsigned* q_head;
-  unsigned* q_tail;
+  int2* q;              // [npieces] (slot, first entry)
+  unsigned* q_seq;      // [npieces] = 1 once entry p is published
+  unsigned* piece_ctr;  // pieces allocated so far
   unsigned* slot_ctr;
+  int* alive;           // warps that may still publish pieces
+  int G;                // mailboxes (= K1 grid)
 };
 
 // First-Fit restricted to the colour window [wb, wb + 1024) (warp-wide);
@@ -350,39 +354,45 @@ __device__ void k1_push_long(const SplitArgs& S, int v, int deg, bool islong) {
       S.slot_v[slot] = vr;
       S.slot_deg[slot] = dr;
       S.slot_left[slot] = np;
-      t = atomicAdd(S.q_tail, (unsigned)np);
+      t = atomicAdd(S.piece_ctr, (unsigned)np);
     }
     slot = __shfl_sync(kFull, slot, 0);
     t = __shfl_sync(kFull, t, 0);
     for (int i = lane; i < np; i += 32) S.q[t + i] = make_int2((int)slot, i * kPiece);
     __threadfence();
     __syncwarp();
-    for (int i = lane; i < np; i += 32) st_release_u32(S.q_seq + t + i, t + i + 1);
+    for (int i = lane; i < np; i += 32) st_release_u32(S.q_seq + t + i, 1u);
   }
 }
 
-// Pop one piece (lane 0 decides, result broadcast); false when the queue is
-// momentarily empty.
-__device__ bool k1_pop(const SplitArgs& S, int& slot, int& start) {
-  int ok = 0, sl = 0, st = 0;
+// Pop one piece from this CTA's mailbox (lane 0 decides, result broadcast).
+// *exhausted is set when every allocated piece of the mailbox is taken.
+__device__ bool k1_pop(const SplitArgs& S, int* s_mbhead, int& slot, int& start,
+                       bool* exhausted) {
+  int ok = 0, sl = 0, st = 0, ex = 0;
   if (lane_id() == 0) {
-    unsigned h = ld_acquire_u32(S.q_head);
-    while (h < ld_acquire_u32(S.q_tail)) {
-      const unsigned old = atomicCAS(S.q_head, h, h + 1);
-      if (old == h) {
-        while (ld_acquire_u32(S.q_seq + h) != h + 1) __nanosleep(32);
-        const int2 e = S.q[h];
+    const unsigned alloc = ld_acquire_u32(S.piece_ctr);
+    for (;;) {
+      const int j = *reinterpret_cast<volatile int*>(s_mbhead);
+      const unsigned p = (unsigned)j * (unsigned)S.G + blockIdx.x;
+      if (p >= alloc) {
+        ex = 1;
+        break;
+      }
+      if (atomicCAS(s_mbhead, j, j + 1) == j) {
+        while (ld_acquire_u32(S.q_seq + p) == 0u) __nanosleep(32);
+        const int2 e = S.q[p];
         sl = e.x;
         st = e.y;
         ok = 1;
         break;
       }
-      h = old;
     }
   }
   ok = __shfl_sync(kFull, ok, 0);
   slot = __shfl_sync(kFull, sl, 0);
   start = __shfl_sync(kFull, st, 0);
+  *exhausted = __shfl_sync(kFull, ex, 0) != 0;
   return ok != 0;
 }
 
@@ -470,7 +480,7 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
                                                      PairLogArgs LA, SplitArgs S) {
   extern __shared__ __align__(16) unsigned char k1_smem[];
   __shared__ unsigned long long s_claim;  // {chunk << 32 | next sub-tile}
-  __shared__ int s_npairs;
+  __shared__ int s_npairs, s_mbhead;
   __shared__ unsigned s_gathers;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   K1Warp& W = reinterpret_cast<K1Warp*>(k1_smem)[warp];
@@ -481,6 +491,7 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
     s_claim = ((unsigned long long)(unsigned)c0 << 32);
     s_npairs = 0;
     s_gathers = 0;
+    s_mbhead = 0;
   }
   W.dv[0][lane] = -1;
   W.dv[1][lane] = -1;
@@ -490,7 +501,8 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
   int it = 0;
   for (;; ++it) {
     int pslot, pstart;
-    while (k1_pop(S, pslot, pstart))  // long-row pieces first
+    bool ex;
+    while (k1_pop(S, &s_mbhead, pslot, pstart, &ex))  // long-row pieces first
       k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L, gathers);
     int sub = -1;
     if (lane == 0) {
@@ -530,10 +542,26 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
     if (kLog && it > 0) k1_drain(W, table ^ 1, cdst, L);  // rows parked one sub-tile ago
   }
   if (kLog && it > 0) k1_drain(W, (it - 1) & 1, cdst, L);
-  {
+  // This warp publishes nothing more; keep serving the CTA's mailbox until
+  // every warp is done publishing and the mailbox is empty.
+  if (lane == 0) atomicSub(S.alive, 1);
+  for (;;) {
     int pslot, pstart;
-    while (k1_pop(S, pslot, pstart))  // drain what other warps published
+    bool ex;
+    if (k1_pop(S, &s_mbhead, pslot, pstart, &ex)) {
       k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L, gathers);
+      continue;
+    }
+    int done = 0;
+    if (lane == 0) done = ex && ld_acquire_u32(reinterpret_cast<const unsigned*>(S.alive)) == 0u;
+    if (__shfl_sync(kFull, done, 0)) {
+      // alive == 0 was read after the mailbox looked exhausted; re-check once
+      // against the now-final allocation count
+      if (!k1_pop(S, &s_mbhead, pslot, pstart, &ex)) break;
+      k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L, gathers);
+      continue;
+    }
+    __nanosleep(200);
   }
   const unsigned g = __reduce_add_sync(kFull, gathers);
   if (lane == 0 && g) atomicAdd(&s_gathers, g);
