@@ -44,6 +44,8 @@ struct K1Warp {
   unsigned char ddeg[2][32];
   unsigned char dns[2][32];
   int dst[2][32][kStaleMax];           // in-flight neighbours to re-check
+  int redo[2][32];                     // medium rows parked for recomputation
+  int nredo[2];
 };
 
 // Long-row pieces.  Piece p (global allocation order) is delivered to the
@@ -223,19 +225,24 @@ __device__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L) {
 }
 
 // ---------------------------------------------------------------------------
-// medium rows (64 <= deg < mega): edge-parallel over all such rows of the
-// sub-tile; per-row bitmaps of min(deg/32 + 1, 32) words in shared memory.
+// medium rows (64 <= deg < split): edge-parallel over all such rows of the
+// sub-tile; per-row bitmaps of min(deg/32 + 1, 32) words in shared memory
+// plus one flag word.  In park mode (first pass, in-place K1) a row that read
+// an in-flight lower neighbour is not committed: its id goes to `redo`, and
+// one sub-tile later the whole row is recomputed in log mode.
 // ---------------------------------------------------------------------------
 template <bool kSnap, bool kLower, bool kLog>
 __device__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cdst, int v,
                           long long b, int deg, bool med, K1Warp& W, uint64_t pol,
-                          const PairLog& L, unsigned& gathers) {
+                          const PairLog& L, unsigned& gathers, int* redo, int* nredo) {
   const int lane = lane_id();
+  const bool park_mode = kLog && redo != nullptr;
   unsigned medmask = __ballot_sync(kFull, med);
   while (medmask) {
-    // rows of this batch: take medium rows in lane order while their words fit
+    // rows of this batch: medium rows in lane order while their words fit
     const int words = med ? min((deg >> 5) + 1, 32) : 0;
-    int wincl = (medmask >> lane) & 1u ? words : 0;
+    const int need = words + 1;  // + stale flag
+    int wincl = (medmask >> lane) & 1u ? need : 0;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int y = __shfl_up_sync(kFull, wincl, d);
@@ -244,7 +251,10 @@ __device__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cd
     const bool inb = ((medmask >> lane) & 1u) && wincl <= kBmWords;
     const unsigned batch = __ballot_sync(kFull, inb);
     medmask &= ~batch;
-    const int woff = wincl - words;
+    const int woff = wincl - need;
+    // rows of the batch that may park (room reserved in the redo list)
+    const int rank = __popc(batch & ((1u << lane) - 1u));
+    const bool parkable = park_mode && inb && (*nredo + rank) < 32;
     const int len = inb ? deg : 0;
     int eincl = len;
 #pragma unroll
@@ -286,18 +296,23 @@ __device__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cd
       for (int u = 0; u < 4; ++u) {
         gathers += take[u];
         const int wo = __shfl_sync(kFull, woff, r[u]);
+        const int nw = __shfl_sync(kFull, words, r[u]);
+        const bool pk = __shfl_sync(kFull, parkable, r[u]);
         const bool ok = c[u] >= 0 && c[u] <= dr[u] && c[u] < 1024;
         if (ok) atomicOr(&W.bm[wo + (c[u] >> 5)], 1u << (c[u] & 31));
         if (kLog) {
           const bool st = take[u] && c[u] == -1;
-          log_pairs(L, st, w[u], vr[u]);
+          if (st && pk) W.bm[wo + nw] = 1u;      // defer: recompute the row later
+          log_pairs(L, st && !pk, w[u], vr[u]);
         }
       }
     }
     __syncwarp();
     // first free colour per row
     int color = -1;
+    bool park = false;
     if (inb) {
+      park = parkable && W.bm[woff + words] != 0u;
       for (int k = 0; k < words; ++k) {
         const unsigned fr = ~W.bm[woff + k];
         if (fr) {
@@ -308,7 +323,7 @@ __device__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cd
       if (color > deg) color = -1;  // cannot happen: <= deg marks among deg+1 slots
     }
     // rows whose first 1024 colours are all taken (deg >= 1024 only)
-    unsigned over = __ballot_sync(kFull, inb && color < 0);
+    unsigned over = __ballot_sync(kFull, inb && !park && color < 0);
     while (over) {
       const int rr = __ffs(over) - 1;
       over &= over - 1;
@@ -320,9 +335,33 @@ __device__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cd
         c = warp_ff_window<kSnap, kLower>(cols, csrc, vv, bb, dd, wb, W.win, pol);
       if (lane == rr) color = c;
     }
-    if (inb) st_color(cdst + v, color);
+    if (park_mode) {
+      const unsigned pm = __ballot_sync(kFull, park);
+      if (park) redo[*nredo + __popc(pm & ((1u << lane) - 1u))] = v;
+      __syncwarp();
+      if (lane == 0) *nredo += __popc(pm);
+    }
+    if (inb && !park) st_color(cdst + v, color);
     __syncwarp();
   }
+}
+
+// Recompute the rows parked by k1_medium one sub-tile ago (log mode).
+template <bool kLower>
+__device__ void k1_redo(const long long* __restrict__ off, const int* __restrict__ cols,
+                        int* cdst, K1Warp& W, int table, uint64_t pol, const PairLog& L,
+                        unsigned& gathers) {
+  const int lane = lane_id();
+  const int nr = W.nredo[table];
+  if (nr == 0) return;
+  const bool in = lane < nr;
+  const int v = in ? W.redo[table][lane] : 0;
+  const long long b = in ? ld_off(off + v, pol) : 0;
+  const int deg = in ? (int)(ld_off(off + v + 1, pol) - b) : 0;
+  k1_medium<false, kLower, true>(cols, cdst, cdst, v, b, deg, in, W, pol, L, gathers, nullptr,
+                                 nullptr);
+  if (lane == 0) W.nredo[table] = 0;
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
@@ -495,6 +534,7 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
   }
   W.dv[0][lane] = -1;
   W.dv[1][lane] = -1;
+  if (lane < 2) W.nredo[lane] = 0;
   __syncthreads();
   PairLog L{LA.pairs + (size_t)blockIdx.x * LA.region_cap, LA.region_cap, &s_npairs, LA.overflow};
   unsigned gathers = 0;
@@ -538,10 +578,17 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
     const bool med = valid && deg > kSmallMax && deg < S.min_deg;
     k1_push_long(S, v, deg, valid && deg >= S.min_deg);
     k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, small, W, table, pol, L, gathers);
-    k1_medium<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, med, W, pol, L, gathers);
-    if (kLog && it > 0) k1_drain(W, table ^ 1, cdst, L);  // rows parked one sub-tile ago
+    k1_medium<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, med, W, pol, L, gathers,
+                                   kLog ? W.redo[table] : nullptr, &W.nredo[table]);
+    if (kLog && it > 0) {  // rows parked one sub-tile ago
+      k1_drain(W, table ^ 1, cdst, L);
+      k1_redo<kLower>(off, cols, cdst, W, table ^ 1, pol, L, gathers);
+    }
   }
-  if (kLog && it > 0) k1_drain(W, (it - 1) & 1, cdst, L);
+  if (kLog && it > 0) {
+    k1_drain(W, (it - 1) & 1, cdst, L);
+    k1_redo<kLower>(off, cols, cdst, W, (it - 1) & 1, pol, L, gathers);
+  }
   // This warp publishes nothing more; keep serving the CTA's mailbox until
   // every warp is done publishing and the mailbox is empty.
   if (lane == 0) atomicSub(S.alive, 1);
