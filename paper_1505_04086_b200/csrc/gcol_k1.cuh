@@ -70,7 +70,7 @@ struct SplitArgs {
 // returns -1 when the window holds no free colour <= deg.  Only used for
 // rows whose first 1024 colours are all forbidden (needs deg >= 1024).
 template <bool kSnap, bool kLower>
-__device__ int warp_ff_window(const int* __restrict__ cols, const int* csrc, int v, long long b,
+__device__ __noinline__ int warp_ff_window(const int* __restrict__ cols, const int* csrc, int v, long long b,
                               int deg, int wb, unsigned* win, uint64_t pol) {
   const int lane = lane_id();
   win[lane] = 0u;
@@ -95,12 +95,64 @@ __device__ int warp_ff_window(const int* __restrict__ cols, const int* csrc, int
 }
 
 // ---------------------------------------------------------------------------
-// small rows: thread per row, adjacency staged in shared memory
+// Staging.  Rows of consecutive ids are adjacent in memory, so a sub-tile's
+// whole adjacency segment is usually one contiguous run: when it fits in
+// the stage it is copied once with coalesced loads and every row (small and
+// medium) reads shared memory.  Otherwise only small rows are staged, with
+// a compact parallel copy (all loads of a batch issued together).
+// ---------------------------------------------------------------------------
+struct StageInfo {
+  bool all;        // stage holds [base, base + kStage) of the segment
+  long long base;
+};
+
+__device__ __forceinline__ StageInfo k1_stage(const int* __restrict__ cols, long long b, int deg,
+                                              K1Warp& W, uint64_t pol) {
+  const int lane = lane_id();
+  const long long nb = __shfl_down_sync(kFull, b, 1);
+  const bool contig = __all_sync(kFull, lane == 31 || nb == b + deg);
+  const long long b0 = __shfl_sync(kFull, b, 0);
+  const long long bend = __shfl_sync(kFull, b + deg, 31);
+  StageInfo si{contig && bend - b0 <= kStage, b0};
+  if (si.all) {
+    const int len = (int)(bend - b0);
+    for (int i = lane; i < len; i += 32 * 4) {
+      int x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = i + u * 32;
+        x[u] = j < len ? ld_col(cols + b0 + j, pol) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = i + u * 32;
+        if (j < len) W.stage[j] = x[u];
+      }
+    }
+    __syncwarp();
+  }
+  return si;
+}
+
+// Row of compact entry j: largest lane r with excl_r <= j.
+__device__ __forceinline__ int row_of(int excl, int j) {
+  int lo = 0;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const int e = __shfl_sync(kFull, excl, lo + s);
+    if (lo + s < 32 && e <= j) lo += s;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// small rows: thread per row over staged adjacency, 64-bit register mask
 // ---------------------------------------------------------------------------
 template <bool kSnap, bool kLower, bool kLog>
-__device__ void k1_small(const int* __restrict__ cols, const int* csrc, int* cdst, int v,
-                         long long b, int deg, bool small, K1Warp& W, int table, uint64_t pol,
-                         const PairLog& L, unsigned& gathers) {
+__device__ __noinline__ void k1_small(const int* __restrict__ cols, const int* csrc, int* cdst,
+                                      int v, long long b, int deg, bool small, K1Warp& W,
+                                      int table, uint64_t pol, const PairLog& L,
+                                      unsigned& gathers, StageInfo si) {
   const int lane = lane_id();
   const int len = small ? deg : 0;
   int incl = len;
@@ -112,45 +164,35 @@ __device__ void k1_small(const int* __restrict__ cols, const int* csrc, int* cds
   const int excl = incl - len;
   const int total = __shfl_sync(kFull, incl, 31);
   if (total == 0) return;
-  const long long nb = __shfl_down_sync(kFull, b, 1);
-  const bool contig = __all_sync(kFull, (len == deg) && (lane == 31 || nb == b + deg));
-  const long long b0 = __shfl_sync(kFull, b, 0);
-  const int nbatch = (total + kStageStep - 1) / kStageStep;
+  const int nbatch = si.all ? 1 : (total + kStageStep - 1) / kStageStep;
   for (int bt = 0; bt < nbatch; ++bt) {
     const int lo = bt * kStageStep;
-    const bool mine = small && excl >= lo && excl < lo + kStageStep;
-    if (contig) {
+    const bool mine = small && (si.all || (excl >= lo && excl < lo + kStageStep));
+    if (!si.all) {  // compact parallel copy of this batch's small rows
       const int hi = min(total, lo + kStage);
-      for (int i = lo + lane; i < hi; i += 32 * 4) {
+      for (int j0 = lo; j0 < hi; j0 += 32 * 4) {
         int x[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int j = i + u * 32;
-          x[u] = j < hi ? ld_col(cols + b0 + j, pol) : 0;
+          const int j = j0 + u * 32 + lane;
+          const int r = row_of(excl, j);
+          const long long br = __shfl_sync(kFull, b, r);
+          const int er = __shfl_sync(kFull, excl, r);
+          x[u] = j < hi ? ld_col(cols + br + (j - er), pol) : 0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int j = i + u * 32;
+          const int j = j0 + u * 32 + lane;
           if (j < hi) W.stage[j - lo] = x[u];
         }
       }
-    } else {
-      unsigned rows = __ballot_sync(kFull, mine);
-      while (rows) {
-        const int r = __ffs(rows) - 1;
-        rows &= rows - 1;
-        const int lr = __shfl_sync(kFull, len, r);
-        const int er = __shfl_sync(kFull, excl, r);
-        const long long br = __shfl_sync(kFull, b, r);
-        for (int t = lane; t < lr; t += 32) W.stage[er - lo + t] = ld_col(cols + br + t, pol);
-      }
     }
     __syncwarp();
+    const int* row = si.all ? W.stage + (b - si.base) : W.stage + (excl - lo);
     const int maxk = __reduce_max_sync(kFull, (unsigned)(mine ? len : 0));
     bool active = mine;
     int ns = 0;
     unsigned long long mask = 0ull;
-    const int* row = W.stage + (excl - lo);
     for (int k = 0; k < maxk; k += 4) {
       int w[4];
       bool take[4];
@@ -194,7 +236,7 @@ __device__ void k1_small(const int* __restrict__ cols, const int* csrc, int* cds
 }
 
 // Re-check and commit the rows parked in `table` (warp-collective).
-__device__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L) {
+__device__ __noinline__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L) {
   const int lane = lane_id();
   const int v = W.dv[table][lane];
   const int ns = v >= 0 ? (int)W.dns[table][lane] : 0;
@@ -232,9 +274,10 @@ __device__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L) {
 // one sub-tile later the whole row is recomputed in log mode.
 // ---------------------------------------------------------------------------
 template <bool kSnap, bool kLower, bool kLog>
-__device__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cdst, int v,
-                          long long b, int deg, bool med, K1Warp& W, uint64_t pol,
-                          const PairLog& L, unsigned& gathers, int* redo, int* nredo) {
+__device__ __noinline__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cdst,
+                                       int v, long long b, int deg, bool med, K1Warp& W,
+                                       uint64_t pol, const PairLog& L, unsigned& gathers,
+                                       int* redo, int* nredo, StageInfo si) {
   const int lane = lane_id();
   const bool park_mode = kLog && redo != nullptr;
   unsigned medmask = __ballot_sync(kFull, med);
@@ -274,19 +317,14 @@ __device__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cd
       for (int u = 0; u < 4; ++u) {
         const int idx = i0 + u * 32 + lane;
         const bool in = idx < E;
-        // row of entry idx: largest r with eoff_r <= idx (5-step search)
-        int lo = 0;
-#pragma unroll
-        for (int s = 16; s >= 1; s >>= 1) {
-          const int e = __shfl_sync(kFull, eoff, lo + s);
-          if (lo + s < 32 && e <= idx) lo += s;
-        }
+        const int lo = row_of(eoff, idx);
         r[u] = lo;
         const long long br = __shfl_sync(kFull, b, lo);
         const int er = __shfl_sync(kFull, eoff, lo);
         vr[u] = __shfl_sync(kFull, v, lo);
         dr[u] = __shfl_sync(kFull, deg, lo);
-        w[u] = in ? ld_col(cols + br + (idx - er), pol) : 0;
+        w[u] = !in ? 0 : (si.all ? W.stage[br - si.base + (idx - er)]
+                                 : ld_col(cols + br + (idx - er), pol));
         take[u] = in && (!kLower || w[u] < vr[u]);
       }
       int c[4];
@@ -348,7 +386,7 @@ __device__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cd
 
 // Recompute the rows parked by k1_medium one sub-tile ago (log mode).
 template <bool kLower>
-__device__ void k1_redo(const long long* __restrict__ off, const int* __restrict__ cols,
+__device__ __noinline__ void k1_redo(const long long* __restrict__ off, const int* __restrict__ cols,
                         int* cdst, K1Warp& W, int table, uint64_t pol, const PairLog& L,
                         unsigned& gathers) {
   const int lane = lane_id();
@@ -359,7 +397,7 @@ __device__ void k1_redo(const long long* __restrict__ off, const int* __restrict
   const long long b = in ? ld_off(off + v, pol) : 0;
   const int deg = in ? (int)(ld_off(off + v + 1, pol) - b) : 0;
   k1_medium<false, kLower, true>(cols, cdst, cdst, v, b, deg, in, W, pol, L, gathers, nullptr,
-                                 nullptr);
+                                 nullptr, StageInfo{false, 0});
   if (lane == 0) W.nredo[table] = 0;
   __syncwarp();
 }
@@ -373,12 +411,18 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return r;
 }
 
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+  int r;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
+}
+
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
 // Publish the pieces of every long row of this sub-tile (warp-collective).
-__device__ void k1_push_long(const SplitArgs& S, int v, int deg, bool islong) {
+__device__ __noinline__ void k1_push_long(const SplitArgs& S, int v, int deg, bool islong) {
   const int lane = lane_id();
   unsigned rows = __ballot_sync(kFull, islong);
   while (rows) {
@@ -398,8 +442,7 @@ __device__ void k1_push_long(const SplitArgs& S, int v, int deg, bool islong) {
     slot = __shfl_sync(kFull, slot, 0);
     t = __shfl_sync(kFull, t, 0);
     for (int i = lane; i < np; i += 32) S.q[t + i] = make_int2((int)slot, i * kPiece);
-    __threadfence();
-    __syncwarp();
+    __syncwarp();  // slot fields (lane 0) before every lane's release store
     for (int i = lane; i < np; i += 32) st_release_u32(S.q_seq + t + i, 1u);
   }
 }
@@ -436,7 +479,7 @@ __device__ bool k1_pop(const SplitArgs& S, int* s_mbhead, int& slot, int& start,
 }
 
 template <bool kSnap, bool kLower, bool kLog>
-__device__ void k1_piece(const long long* __restrict__ off, const int* __restrict__ cols,
+__device__ __noinline__ void k1_piece(const long long* __restrict__ off, const int* __restrict__ cols,
                          const int* csrc, int* cdst, const SplitArgs& S, int slot, int start,
                          K1Warp& W, uint64_t pol, const PairLog& L, unsigned& gathers) {
   constexpr int U = 8;
@@ -484,13 +527,11 @@ __device__ void k1_piece(const long long* __restrict__ off, const int* __restric
   if (lane == 0) word |= lo;
   if (lane == 1) word |= hi;
   if (word) atomicOr(S.slot_bm + (size_t)slot * 32 + lane, word);
-  __threadfence();
   __syncwarp();
   int last = 0;
-  if (lane == 0) last = atomicSub(S.slot_left + slot, 1) == 1;
+  if (lane == 0) last = atom_add_acq_rel(S.slot_left + slot, -1) == 1;
   last = __shfl_sync(kFull, last, 0);
   if (last) {
-    __threadfence();
     const unsigned wd = ld_acquire_u32(S.slot_bm + (size_t)slot * 32 + lane);
     const unsigned fr = ~wd;  // deg >= 1024: every bit of window 0 is a candidate
     const unsigned nz = __ballot_sync(kFull, fr != 0u);
@@ -577,9 +618,11 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
     const bool small = valid && deg >= 1 && deg <= kSmallMax;
     const bool med = valid && deg > kSmallMax && deg < S.min_deg;
     k1_push_long(S, v, deg, valid && deg >= S.min_deg);
-    k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, small, W, table, pol, L, gathers);
+    const StageInfo si = k1_stage(cols, b, deg, W, pol);
+    k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, small, W, table, pol, L, gathers,
+                                  si);
     k1_medium<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, med, W, pol, L, gathers,
-                                   kLog ? W.redo[table] : nullptr, &W.nredo[table]);
+                                   kLog ? W.redo[table] : nullptr, &W.nredo[table], si);
     if (kLog && it > 0) {  // rows parked one sub-tile ago
       k1_drain(W, table ^ 1, cdst, L);
       k1_redo<kLower>(off, cols, cdst, W, table ^ 1, pol, L, gathers);
