@@ -17,7 +17,6 @@ REPO = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgcol_cuda.so")
 SOURCES = ["gcol_cuda.cu"]
-DEPS = SOURCES + ["gcol_device.cuh", "gcol_kernels.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -40,8 +39,8 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, d) for d in DEPS] + [os.path.join(REPO, "include", "gcol_cuda.h"),
-                                                     os.path.abspath(__file__)]
+    deps = [os.path.join(CSRC, d) for d in os.listdir(CSRC) if d.endswith((".cu", ".cuh", ".h"))]
+    deps += [os.path.join(REPO, "include", "gcol_cuda.h"), os.path.abspath(__file__)]
     return any(os.path.getmtime(d) > t for d in deps)
 
 

@@ -451,9 +451,14 @@ __device__ __noinline__ void k1_push_long(const SplitArgs& S, int v, int deg, bo
 // *exhausted is set when every allocated piece of the mailbox is taken.
 __device__ bool k1_pop(const SplitArgs& S, int* s_mbhead, int& slot, int& start,
                        bool* exhausted) {
-  int ok = 0, sl = 0, st = 0, ex = 0;
+  int ok = 0, sl = 0, st = 0, ex = 1;
+  if (S.min_deg == INT_MAX) {  // no long rows in this graph
+    *exhausted = true;
+    return false;
+  }
+  ex = 0;
   if (lane_id() == 0) {
-    const unsigned alloc = ld_acquire_u32(S.piece_ctr);
+    const unsigned alloc = *reinterpret_cast<volatile const unsigned*>(S.piece_ctr);
     for (;;) {
       const int j = *reinterpret_cast<volatile int*>(s_mbhead);
       const unsigned p = (unsigned)j * (unsigned)S.G + blockIdx.x;
@@ -635,7 +640,7 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
   // This warp publishes nothing more; keep serving the CTA's mailbox until
   // every warp is done publishing and the mailbox is empty.
   if (lane == 0) atomicSub(S.alive, 1);
-  for (;;) {
+  for (; S.min_deg != INT_MAX;) {
     int pslot, pstart;
     bool ex;
     if (k1_pop(S, &s_mbhead, pslot, pstart, &ex)) {
