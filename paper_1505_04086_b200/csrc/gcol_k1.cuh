@@ -44,6 +44,11 @@ struct K1Warp {
   unsigned char ddeg[2][32];
   unsigned char dns[2][32];
   int dst[2][32][kStaleMax];           // in-flight neighbours to re-check
+  int cv[32];                          // second-chance slot per lane (carry)
+  unsigned cmask[32][2];
+  unsigned char cdeg[32];
+  unsigned char cns[32];
+  int cst[32][kStaleMax];
   int redo[2][32];                     // medium rows parked for recomputation
   int nredo[2];
 };
@@ -235,32 +240,66 @@ __device__ __noinline__ void k1_small(const int* __restrict__ cols, const int* c
   }
 }
 
-// Re-check and commit the rows parked in `table` (warp-collective).
+// Re-check the rows parked in `table` (warp-collective).  A row whose
+// in-flight neighbours have all committed is committed now; otherwise it
+// gets one more sub-tile in the lane's carry slot, and whatever is still
+// uncoloured at that second check is logged for round 1.
 __device__ __noinline__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L) {
   const int lane = lane_id();
+  // (1) carry slot: final check
+  {
+    const int v = W.cv[lane];
+    const int ns = v >= 0 ? (int)W.cns[lane] : 0;
+    int c[kStaleMax], u[kStaleMax];
+#pragma unroll
+    for (int k = 0; k < kStaleMax; ++k) {
+      u[k] = k < ns ? W.cst[lane][k] : 0;
+      c[k] = k < ns ? ld_color(cdst + u[k]) : -2;
+    }
+    unsigned long long mask = 0ull;
+    int deg = 0;
+    if (v >= 0) {
+      mask = (unsigned long long)W.cmask[lane][0] | ((unsigned long long)W.cmask[lane][1] << 32);
+      deg = W.cdeg[lane];
+    }
+#pragma unroll
+    for (int k = 0; k < kStaleMax; ++k) {
+      if (c[k] >= 0 && c[k] <= deg) mask |= 1ull << c[k];
+      log_pairs(L, k < ns && c[k] == -1, u[k], v);  // still in flight: round 1 checks it
+    }
+    if (v >= 0) {
+      st_color(cdst + v, __ffsll((long long)~mask) - 1);
+      W.cv[lane] = -1;
+    }
+  }
+  // (2) rows parked one sub-tile ago
   const int v = W.dv[table][lane];
   const int ns = v >= 0 ? (int)W.dns[table][lane] : 0;
-  int c[kStaleMax];
-  int u[kStaleMax];
+  int c[kStaleMax], u[kStaleMax];
 #pragma unroll
   for (int k = 0; k < kStaleMax; ++k) {
     u[k] = k < ns ? W.dst[table][lane][k] : 0;
     c[k] = k < ns ? ld_color(cdst + u[k]) : -2;
   }
-  unsigned long long mask = 0ull;
-  int deg = 0;
   if (v >= 0) {
-    mask = (unsigned long long)W.dmask[table][lane][0] |
-           ((unsigned long long)W.dmask[table][lane][1] << 32);
-    deg = W.ddeg[table][lane];
-  }
+    unsigned long long mask = (unsigned long long)W.dmask[table][lane][0] |
+                              ((unsigned long long)W.dmask[table][lane][1] << 32);
+    const int deg = W.ddeg[table][lane];
+    int left = 0;
 #pragma unroll
-  for (int k = 0; k < kStaleMax; ++k) {
-    if (c[k] >= 0 && c[k] <= deg) mask |= 1ull << c[k];
-    log_pairs(L, k < ns && c[k] == -1, u[k], v);  // still in flight: round 1 checks it
-  }
-  if (v >= 0) {
-    st_color(cdst + v, __ffsll((long long)~mask) - 1);
+    for (int k = 0; k < kStaleMax; ++k) {
+      if (c[k] >= 0 && c[k] <= deg) mask |= 1ull << c[k];
+      if (k < ns && c[k] == -1) W.cst[lane][left++] = u[k];
+    }
+    if (left == 0) {
+      st_color(cdst + v, __ffsll((long long)~mask) - 1);
+    } else {  // second chance
+      W.cv[lane] = v;
+      W.cmask[lane][0] = (unsigned)mask;
+      W.cmask[lane][1] = (unsigned)(mask >> 32);
+      W.cdeg[lane] = (unsigned char)deg;
+      W.cns[lane] = (unsigned char)left;
+    }
     W.dv[table][lane] = -1;
   }
   __syncwarp();
@@ -580,6 +619,7 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
   }
   W.dv[0][lane] = -1;
   W.dv[1][lane] = -1;
+  W.cv[lane] = -1;
   if (lane < 2) W.nredo[lane] = 0;
   __syncthreads();
   PairLog L{LA.pairs + (size_t)blockIdx.x * LA.region_cap, LA.region_cap, &s_npairs, LA.overflow};
@@ -636,6 +676,7 @@ __global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict
   if (kLog && it > 0) {
     k1_drain(W, (it - 1) & 1, cdst, L);
     k1_redo<kLower>(off, cols, cdst, W, (it - 1) & 1, pol, L, gathers);
+    k1_drain(W, it & 1, cdst, L);  // table it&1 is empty: this flushes the carry slots
   }
   // This warp publishes nothing more; keep serving the CTA's mailbox until
   // every warp is done publishing and the mailbox is empty.
