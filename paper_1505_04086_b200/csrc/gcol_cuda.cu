@@ -78,7 +78,7 @@ struct SplitPlan {
   unsigned* d_slot_bm = nullptr;
   int2* d_q = nullptr;
   unsigned* d_q_seq = nullptr;
-  unsigned* d_ctr = nullptr;  // [0] pieces allocated, [1] slots, [2] live warps
+  unsigned* d_ctr = nullptr;  // [0] pieces allocated, [1] slots, [2] live warps, [3] chunks done
 };
 
 }  // namespace
@@ -213,7 +213,7 @@ void free_split(gcol_cuda_graph* g, SplitPlan& P) {
 // Clears the per-run queue state (untimed prologue); `warps` = K1 warps.
 int reset_split(gcol_cuda_graph* g, const SplitPlan* P, int warps) {
   if (!P) return GCOL_OK;
-  const unsigned init[4] = {0u, 0u, static_cast<unsigned>(warps), 0u};
+  const unsigned init[4] = {0u, 0u, static_cast<unsigned>(warps), 0u};  // warps = consumer warps
   GCOL_CK(cudaMemcpyAsync(P->d_ctr, init, sizeof init, cudaMemcpyHostToDevice, g->stream));
   if (P->nslots > 0) {
     GCOL_CK(cudaMemsetAsync(P->d_slot_bm, 0, sizeof(unsigned) * 32 * static_cast<size_t>(P->nslots),
@@ -233,26 +233,29 @@ struct K1Launch {
   const SplitPlan* plan = nullptr;
 };
 
-constexpr size_t kK1Smem = sizeof(K1Warp) * kK1Warps;
+constexpr size_t kK1Smem = sizeof(K1Smem);
 
 template <bool kSnap, bool kLower, bool kLog>
 int plan_k1(gcol_cuda_graph* g, int k1_blocks, int split_min, K1Launch* K) {
-  auto k1 = k1_light<kSnap, kLower, kLog>;
+  auto k1 = k1_pipe<kSnap, kLower, kLog>;
   GCOL_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k1),
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(kK1Smem)));
   int occ = 1;
-  GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1, kK1Block, kK1Smem));
+  GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1, kK1Threads, kK1Smem));
   if (occ < 1) occ = 1;
-  const int bps = k1_blocks > 0 ? std::min(k1_blocks, occ) : std::min(2, occ);
-  K->grid1 = g->sms * bps;
+  const int bps = k1_blocks > 0 ? std::min(k1_blocks, occ) : 1;
+  // small graphs: fewer CTAs, so the ~256 x CTAs vertices in flight stay a
+  // small share of the graph (colour quality)
+  const long long want = std::max(1LL, g->n / (kChunk * 24LL));
+  K->grid1 = static_cast<int>(std::min<long long>(g->sms * bps, want));
   K->smem = kK1Smem;
   SplitPlan* P = nullptr;
   if (int rc = get_split(g, split_min, &P)) return rc;
   K->plan = P;
   K->S = SplitArgs{P->nslots > 0 ? split_min : INT_MAX, P->d_slot_v, P->d_slot_deg,
                    P->d_slot_left, P->d_slot_bm, P->d_q, P->d_q_seq, P->d_ctr, P->d_ctr + 1,
-                   reinterpret_cast<int*>(P->d_ctr + 2), K->grid1};
+                   reinterpret_cast<int*>(P->d_ctr + 2), K->grid1, P->d_ctr + 3};
   const unsigned long long per = g->pair_cap / static_cast<unsigned long long>(K->grid1);
   K->L = PairLogArgs{g->d_pairs, static_cast<int>(std::min<unsigned long long>(per, 1u << 30)),
                      g->d_pair_counts, &g->d_ctrl->pair_overflow};
@@ -275,14 +278,15 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, cudaGraph
   cudaGraphNode_t n_ev0, n_k1, n_ev1, n_cand, n_while, n_ev2;
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
   {
+    int drift = kDriftDefault;
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), const_cast<int*>(&n),
-                    nullptr, &g->d_colors, &g->d_colors, &g->d_ctrl, &K.L, &K.S};
+                    nullptr, &g->d_colors, &g->d_colors, &g->d_ctrl, &K.L, &K.S, &drift};
     const int* wl = nullptr;
     args[4] = &wl;
     cudaKernelNodeParams p{};
-    p.func = reinterpret_cast<void*>(k1_light<false, kLower, true>);
+    p.func = reinterpret_cast<void*>(k1_pipe<false, kLower, true>);
     p.gridDim = dim3(K.grid1);
-    p.blockDim = dim3(kK1Block);
+    p.blockDim = dim3(kK1Threads);
     p.sharedMemBytes = static_cast<unsigned>(K.smem);
     p.kernelParams = args;
     GCOL_CK(cudaGraphAddKernelNode(&n_k1, graph, &n_ev0, 1, &p));
@@ -310,7 +314,7 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, cudaGraph
   GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle, 1));
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, graph, &n_while, 1, g->ev_end));
   GCOL_CK(cudaGraphInstantiate(out_exec, graph, 0));
-  g->k1_warps[*out_exec] = K.grid1 * kK1Warps;
+  g->k1_warps[*out_exec] = K.grid1 * kCW;
   *out_graph = graph;
   return GCOL_OK;
 }
@@ -322,11 +326,12 @@ template <int R, bool kLower>
 int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min) {
   K1Launch K;
   if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K)) return rc;
-  if (int rc = reset_split(g, K.plan, K.grid1 * kK1Warps)) return rc;
+  if (int rc = reset_split(g, K.plan, K.grid1 * kCW)) return rc;
   const int n = static_cast<int>(g->n);
   GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
-  k1_light<false, kLower, true><<<K.grid1, kK1Block, K.smem, g->stream>>>(
-      g->d_off, g->d_cols, n, n, nullptr, g->d_colors, g->d_colors, g->d_ctrl, K.L, K.S);
+  k1_pipe<false, kLower, true><<<K.grid1, kK1Threads, K.smem, g->stream>>>(
+      g->d_off, g->d_cols, n, n, nullptr, g->d_colors, g->d_colors, g->d_ctrl, K.L, K.S,
+      kDriftDefault);
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
   k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors,
                                                          g->d_ctrl, K.L, K.grid1, g->d_marks);
@@ -808,14 +813,16 @@ int gcol_cuda_tentative_snapshot(gcol_cuda_graph* g, const int32_t* colors_in,
     int rc = lower_only ? plan_k1<true, true, false>(g, 0, kSplitDefault, &K)
                         : plan_k1<true, false, false>(g, 0, kSplitDefault, &K);
     if (rc) return rc;
-    if (int r2 = reset_split(g, K.plan, K.grid1 * kK1Warps)) return r2;
+    if (int r2 = reset_split(g, K.plan, K.grid1 * kCW)) return r2;
     K.L = PairLogArgs{};
     if (lower_only)
-      k1_light<true, true, false><<<K.grid1, kK1Block, K.smem, g->stream>>>(
-          g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, K.L, K.S);
+      k1_pipe<true, true, false><<<K.grid1, kK1Threads, K.smem, g->stream>>>(
+          g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, K.L, K.S,
+          0);
     else
-      k1_light<true, false, false><<<K.grid1, kK1Block, K.smem, g->stream>>>(
-          g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, K.L, K.S);
+      k1_pipe<true, false, false><<<K.grid1, kK1Threads, K.smem, g->stream>>>(
+          g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, K.L, K.S,
+          0);
   }
   GCOL_CK(cudaGetLastError());
   if (int rc = copy_out(g, colors_out, d_out, sizeof(int) * n, memory)) return rc;

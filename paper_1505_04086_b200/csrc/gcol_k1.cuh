@@ -27,17 +27,20 @@
 namespace gcol {
 namespace dev {
 
-constexpr int kK1Warps = 8;
-constexpr int kK1Block = kK1Warps * 32;
-constexpr int kSubTiles = kK1Block / 32;  // sub-tiles per claimed chunk
+constexpr int kCW = 8;                    // consumer warps per CTA
+constexpr int kK1Threads = (kCW + 1) * 32;  // + one producer warp
+constexpr int kChunk = kCW * 32;          // vertices per chunk (one sub-tile per consumer)
+constexpr int kSlots = 3;                 // staged chunks in flight per CTA
+constexpr int kSlotStage = 7168;          // adjacency entries staged per chunk (28 KB)
 constexpr int kBmWords = 512;             // per-warp medium-row bitmap pool
 constexpr int kStaleMax = 4;              // stale neighbours remembered per parked row
 constexpr int kSplitDefault = 1024;       // rows >= this are split into pieces
 constexpr int kPiece = 1024;              // entries per piece
+constexpr int kDriftDefault = 2;          // max rounds a CTA may run ahead
 
+// Per consumer warp: forbidden-colour scratch and the deferral state.
 struct K1Warp {
-  int stage[kStage];                   // staged small-row adjacency (4 KB)
-  unsigned bm[kBmWords];               // medium-row bitmaps (2 KB)
+  unsigned bm[kBmWords];               // medium-row bitmaps
   unsigned win[32];                    // window for the rare overflow path
   int dv[2][32];                       // parked row per lane (ping-pong tables)
   unsigned dmask[2][32][2];
@@ -51,6 +54,32 @@ struct K1Warp {
   int cst[32][kStaleMax];
   int redo[2][32];                     // medium rows parked for recomputation
   int nredo[2];
+};
+
+// One staged chunk: its rows and (a window of) their adjacency.
+struct K1Slot {
+  long long b[kChunk];                 // row starts
+  int v[kChunk];                       // vertex ids (-1: none)
+  int deg[kChunk];
+  int stage[kSlotStage];               // cols[base .. base + len)
+  long long base;
+  int len;
+};
+
+struct K1Smem {
+  K1Slot slot[kSlots];
+  K1Warp cw[kCW];
+};
+
+// Adjacency window in shared memory: rows lying inside read it, the rest
+// read global memory.
+struct StageWin {
+  const int* stage;
+  long long base;
+  int len;
+  __device__ __forceinline__ bool has(long long b, int deg) const {
+    return b >= base && b + deg <= base + len;
+  }
 };
 
 // Long-row pieces.  Piece p (global allocation order) is delivered to the
@@ -67,8 +96,9 @@ struct SplitArgs {
   unsigned* q_seq;      // [npieces] = 1 once entry p is published
   unsigned* piece_ctr;  // pieces allocated so far
   unsigned* slot_ctr;
-  int* alive;           // warps that may still publish pieces
+  int* alive;           // consumer warps that may still publish pieces
   int G;                // mailboxes (= K1 grid)
+  unsigned* done_chunks;  // chunks fully consumed (drift bound)
 };
 
 // First-Fit restricted to the colour window [wb, wb + 1024) (warp-wide);
@@ -99,46 +129,6 @@ __device__ __noinline__ int warp_ff_window(const int* __restrict__ cols, const i
   return wb + j * 32 + __ffs(fj) - 1;
 }
 
-// ---------------------------------------------------------------------------
-// Staging.  Rows of consecutive ids are adjacent in memory, so a sub-tile's
-// whole adjacency segment is usually one contiguous run: when it fits in
-// the stage it is copied once with coalesced loads and every row (small and
-// medium) reads shared memory.  Otherwise only small rows are staged, with
-// a compact parallel copy (all loads of a batch issued together).
-// ---------------------------------------------------------------------------
-struct StageInfo {
-  bool all;        // stage holds [base, base + kStage) of the segment
-  long long base;
-};
-
-__device__ __forceinline__ StageInfo k1_stage(const int* __restrict__ cols, long long b, int deg,
-                                              K1Warp& W, uint64_t pol) {
-  const int lane = lane_id();
-  const long long nb = __shfl_down_sync(kFull, b, 1);
-  const bool contig = __all_sync(kFull, lane == 31 || nb == b + deg);
-  const long long b0 = __shfl_sync(kFull, b, 0);
-  const long long bend = __shfl_sync(kFull, b + deg, 31);
-  StageInfo si{contig && bend - b0 <= kStage, b0};
-  if (si.all) {
-    const int len = (int)(bend - b0);
-    for (int i = lane; i < len; i += 32 * 4) {
-      int x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = i + u * 32;
-        x[u] = j < len ? ld_col(cols + b0 + j, pol) : 0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = i + u * 32;
-        if (j < len) W.stage[j] = x[u];
-      }
-    }
-    __syncwarp();
-  }
-  return si;
-}
-
 // Row of compact entry j: largest lane r with excl_r <= j.
 __device__ __forceinline__ int row_of(int excl, int j) {
   int lo = 0;
@@ -151,100 +141,66 @@ __device__ __forceinline__ int row_of(int excl, int j) {
 }
 
 // ---------------------------------------------------------------------------
-// small rows: thread per row over staged adjacency, 64-bit register mask
+// small rows: thread per row over the staged adjacency, 64-bit register mask
 // ---------------------------------------------------------------------------
 template <bool kSnap, bool kLower, bool kLog>
-__device__ __noinline__ void k1_small(const int* __restrict__ cols, const int* csrc, int* cdst,
-                                      int v, long long b, int deg, bool small, K1Warp& W,
-                                      int table, uint64_t pol, const PairLog& L,
-                                      unsigned& gathers, StageInfo si) {
+__device__ __forceinline__ void k1_small(const int* __restrict__ cols, const int* csrc,
+                                         int* cdst, int v, long long b, int deg, bool small,
+                                         K1Warp& W, int table, uint64_t pol, const PairLog& L,
+                                         unsigned& gathers, const StageWin& sw) {
   const int lane = lane_id();
-  const int len = small ? deg : 0;
-  int incl = len;
+  const bool inwin = sw.has(b, deg);
+  const int* rs = sw.stage + (b - sw.base);  // valid when inwin
+  const int maxk = __reduce_max_sync(kFull, (unsigned)(small ? deg : 0));
+  bool active = small;
+  int ns = 0;
+  unsigned long long mask = 0ull;
+  for (int k = 0; k < maxk; k += 4) {
+    int w[4];
+    bool take[4];
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int y = __shfl_up_sync(kFull, incl, d);
-    if (lane >= d) incl += y;
+    for (int u = 0; u < 4; ++u) {
+      const bool in = active && (k + u) < deg;
+      w[u] = in ? (inwin ? rs[k + u] : ld_col(cols + b + k + u, pol)) : 0;
+      take[u] = in && (!kLower || w[u] < v);
+      if (kLower && in && w[u] > v) active = false;  // sorted row: the rest is > v
+    }
+    int c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      gathers += take[u];
+      if (c[u] >= 0 && c[u] <= deg) mask |= 1ull << c[u];
+      if (kLog) {
+        const bool st = take[u] && c[u] == -1 && w[u] < v;
+        const bool keep = st && ns < kStaleMax;
+        if (keep) W.dst[table][lane][ns] = w[u];
+        ns += st ? 1 : 0;
+        log_pairs(L, st && !keep, w[u], v);
+      }
+    }
+    if (kLower && !__any_sync(kFull, active)) break;
   }
-  const int excl = incl - len;
-  const int total = __shfl_sync(kFull, incl, 31);
-  if (total == 0) return;
-  const int nbatch = si.all ? 1 : (total + kStageStep - 1) / kStageStep;
-  for (int bt = 0; bt < nbatch; ++bt) {
-    const int lo = bt * kStageStep;
-    const bool mine = small && (si.all || (excl >= lo && excl < lo + kStageStep));
-    if (!si.all) {  // compact parallel copy of this batch's small rows
-      const int hi = min(total, lo + kStage);
-      for (int j0 = lo; j0 < hi; j0 += 32 * 4) {
-        int x[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = j0 + u * 32 + lane;
-          const int r = row_of(excl, j);
-          const long long br = __shfl_sync(kFull, b, r);
-          const int er = __shfl_sync(kFull, excl, r);
-          x[u] = j < hi ? ld_col(cols + br + (j - er), pol) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = j0 + u * 32 + lane;
-          if (j < hi) W.stage[j - lo] = x[u];
-        }
-      }
+  if (small) {
+    if (kLog && ns > 0) {  // park; committed after the re-check one chunk later
+      W.dv[table][lane] = v;
+      W.dmask[table][lane][0] = (unsigned)mask;
+      W.dmask[table][lane][1] = (unsigned)(mask >> 32);
+      W.ddeg[table][lane] = (unsigned char)deg;
+      W.dns[table][lane] = (unsigned char)min(ns, kStaleMax);
+    } else {
+      st_color(cdst + v, __ffsll((long long)~mask) - 1);
     }
-    __syncwarp();
-    const int* row = si.all ? W.stage + (b - si.base) : W.stage + (excl - lo);
-    const int maxk = __reduce_max_sync(kFull, (unsigned)(mine ? len : 0));
-    bool active = mine;
-    int ns = 0;
-    unsigned long long mask = 0ull;
-    for (int k = 0; k < maxk; k += 4) {
-      int w[4];
-      bool take[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const bool in = active && (k + u) < len;
-        w[u] = in ? row[k + u] : 0;
-        take[u] = in && (!kLower || w[u] < v);
-        if (kLower && in && w[u] > v) active = false;  // sorted row: the rest is > v
-      }
-      int c[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        gathers += take[u];
-        if (c[u] >= 0 && c[u] <= deg) mask |= 1ull << c[u];
-        if (kLog) {
-          const bool st = take[u] && c[u] == -1 && w[u] < v;
-          const bool keep = st && ns < kStaleMax;
-          if (keep) W.dst[table][lane][ns] = w[u];
-          ns += st ? 1 : 0;
-          log_pairs(L, st && !keep, w[u], v);
-        }
-      }
-      if (kLower && !__any_sync(kFull, active)) break;
-    }
-    if (mine) {
-      if (kLog && ns > 0) {  // park; committed after the re-check one sub-tile later
-        W.dv[table][lane] = v;
-        W.dmask[table][lane][0] = (unsigned)mask;
-        W.dmask[table][lane][1] = (unsigned)(mask >> 32);
-        W.ddeg[table][lane] = (unsigned char)deg;
-        W.dns[table][lane] = (unsigned char)min(ns, kStaleMax);
-      } else {
-        st_color(cdst + v, __ffsll((long long)~mask) - 1);
-      }
-    }
-    __syncwarp();
   }
+  __syncwarp();
 }
 
 // Re-check the rows parked in `table` (warp-collective).  A row whose
 // in-flight neighbours have all committed is committed now; otherwise it
 // gets one more sub-tile in the lane's carry slot, and whatever is still
 // uncoloured at that second check is logged for round 1.
-__device__ __noinline__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L) {
+__device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L) {
   const int lane = lane_id();
   // (1) carry slot: final check
   {
@@ -313,12 +269,14 @@ __device__ __noinline__ void k1_drain(K1Warp& W, int table, int* cdst, const Pai
 // one sub-tile later the whole row is recomputed in log mode.
 // ---------------------------------------------------------------------------
 template <bool kSnap, bool kLower, bool kLog>
-__device__ __noinline__ void k1_medium(const int* __restrict__ cols, const int* csrc, int* cdst,
-                                       int v, long long b, int deg, bool med, K1Warp& W,
-                                       uint64_t pol, const PairLog& L, unsigned& gathers,
-                                       int* redo, int* nredo, StageInfo si) {
+__device__ __forceinline__ void k1_medium(const int* __restrict__ cols, const int* csrc,
+                                          int* cdst, int v, long long b, int deg, bool med,
+                                          K1Warp& W, uint64_t pol, const PairLog& L,
+                                          unsigned& gathers, int* redo, int* nredo,
+                                          const StageWin& sw) {
   const int lane = lane_id();
   const bool park_mode = kLog && redo != nullptr;
+  const bool inwin = sw.has(b, deg);
   unsigned medmask = __ballot_sync(kFull, med);
   while (medmask) {
     // rows of this batch: medium rows in lane order while their words fit
@@ -360,10 +318,11 @@ __device__ __noinline__ void k1_medium(const int* __restrict__ cols, const int* 
         r[u] = lo;
         const long long br = __shfl_sync(kFull, b, lo);
         const int er = __shfl_sync(kFull, eoff, lo);
+        const bool iw = __shfl_sync(kFull, inwin, lo);
         vr[u] = __shfl_sync(kFull, v, lo);
         dr[u] = __shfl_sync(kFull, deg, lo);
-        w[u] = !in ? 0 : (si.all ? W.stage[br - si.base + (idx - er)]
-                                 : ld_col(cols + br + (idx - er), pol));
+        w[u] = !in ? 0 : (iw ? sw.stage[br - sw.base + (idx - er)]
+                             : ld_col(cols + br + (idx - er), pol));
         take[u] = in && (!kLower || w[u] < vr[u]);
       }
       int c[4];
@@ -423,24 +382,6 @@ __device__ __noinline__ void k1_medium(const int* __restrict__ cols, const int* 
   }
 }
 
-// Recompute the rows parked by k1_medium one sub-tile ago (log mode).
-template <bool kLower>
-__device__ __noinline__ void k1_redo(const long long* __restrict__ off, const int* __restrict__ cols,
-                        int* cdst, K1Warp& W, int table, uint64_t pol, const PairLog& L,
-                        unsigned& gathers) {
-  const int lane = lane_id();
-  const int nr = W.nredo[table];
-  if (nr == 0) return;
-  const bool in = lane < nr;
-  const int v = in ? W.redo[table][lane] : 0;
-  const long long b = in ? ld_off(off + v, pol) : 0;
-  const int deg = in ? (int)(ld_off(off + v + 1, pol) - b) : 0;
-  k1_medium<false, kLower, true>(cols, cdst, cdst, v, b, deg, in, W, pol, L, gathers, nullptr,
-                                 nullptr, StageInfo{false, 0});
-  if (lane == 0) W.nredo[table] = 0;
-  __syncwarp();
-}
-
 // ---------------------------------------------------------------------------
 // long rows: producer side (warp that meets the row) and piece processing
 // ---------------------------------------------------------------------------
@@ -461,7 +402,7 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
 }
 
 // Publish the pieces of every long row of this sub-tile (warp-collective).
-__device__ __noinline__ void k1_push_long(const SplitArgs& S, int v, int deg, bool islong) {
+__device__ __forceinline__ void k1_push_long(const SplitArgs& S, int v, int deg, bool islong) {
   const int lane = lane_id();
   unsigned rows = __ballot_sync(kFull, islong);
   while (rows) {
@@ -523,7 +464,7 @@ __device__ bool k1_pop(const SplitArgs& S, int* s_mbhead, int& slot, int& start,
 }
 
 template <bool kSnap, bool kLower, bool kLog>
-__device__ __noinline__ void k1_piece(const long long* __restrict__ off, const int* __restrict__ cols,
+__device__ __forceinline__ void k1_piece(const long long* __restrict__ off, const int* __restrict__ cols,
                          const int* csrc, int* cdst, const SplitArgs& S, int slot, int start,
                          K1Warp& W, uint64_t pol, const PairLog& L, unsigned& gathers) {
   constexpr int U = 8;
@@ -593,115 +534,228 @@ __device__ __noinline__ void k1_piece(const long long* __restrict__ off, const i
   __syncwarp();
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
-// K1 kernel
+// K1 kernel.  One CTA per SM: a producer warp stages chunks (256 rows:
+// offsets + a window of their adjacency) into a ring of shared-memory slots
+// with cp.async, up to kSlots chunks ahead; eight consumer warps colour them.
+// Chunks are assigned round-robin (chunk c -> CTA c % G), so the producer
+// can prefetch without claiming anything: the vertices in flight are only
+// those being coloured (about G x 256), which is what governs the stale
+// reads and hence the colour count.  A CTA may not run more than `drift`
+// rounds ahead of the slowest one.
 // ---------------------------------------------------------------------------
 template <bool kSnap, bool kLower, bool kLog>
-__global__ void __launch_bounds__(kK1Block) k1_light(const long long* __restrict__ off,
-                                                     const int* __restrict__ cols, int n,
-                                                     int nitems, const int* worklist,
-                                                     const int* csrc, int* cdst, Ctrl* ctrl,
-                                                     PairLogArgs LA, SplitArgs S) {
-  extern __shared__ __align__(16) unsigned char k1_smem[];
-  __shared__ unsigned long long s_claim;  // {chunk << 32 | next sub-tile}
+__global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restrict__ off,
+                                                      const int* __restrict__ cols, int n,
+                                                      int nitems, const int* worklist,
+                                                      const int* csrc, int* cdst, Ctrl* ctrl,
+                                                      PairLogArgs LA, SplitArgs S, int drift) {
+  extern __shared__ __align__(16) unsigned char k1_raw[];
+  K1Smem& sm = *reinterpret_cast<K1Smem*>(k1_raw);
+  __shared__ int s_ready[kSlots];
+  __shared__ int s_consumed[kSlots];
   __shared__ int s_npairs, s_mbhead;
   __shared__ unsigned s_gathers;
   const int warp = threadIdx.x >> 5, lane = lane_id();
-  K1Warp& W = reinterpret_cast<K1Warp*>(k1_smem)[warp];
   const uint64_t pol = policy_evict_first();
-  const int nchunks = (nitems + kK1Block - 1) / kK1Block;
+  const int G = gridDim.x;
+  const int nchunks = (nitems + kChunk - 1) / kChunk;
+  if (threadIdx.x < kSlots) {
+    s_ready[threadIdx.x] = -1;
+    s_consumed[threadIdx.x] = 0;
+  }
   if (threadIdx.x == 0) {
-    const int c0 = (int)atomicAdd(&ctrl->tile_cursor, 1ull);
-    s_claim = ((unsigned long long)(unsigned)c0 << 32);
     s_npairs = 0;
     s_gathers = 0;
     s_mbhead = 0;
   }
-  W.dv[0][lane] = -1;
-  W.dv[1][lane] = -1;
-  W.cv[lane] = -1;
-  if (lane < 2) W.nredo[lane] = 0;
+  if (warp < kCW) {
+    K1Warp& W = sm.cw[warp];
+    W.dv[0][lane] = -1;
+    W.dv[1][lane] = -1;
+    W.cv[lane] = -1;
+    if (lane < 2) W.nredo[lane] = 0;
+  }
   __syncthreads();
+
+  if (warp == kCW) {
+    // ----------------------------- producer ------------------------------
+    for (int k = 0;; ++k) {
+      const int c = blockIdx.x + k * G;
+      const int si = k % kSlots;
+      K1Slot& sl = sm.slot[si];
+      if (k >= kSlots)  // previous use of this slot fully consumed
+        while (*reinterpret_cast<volatile int*>(&s_consumed[si]) < kCW * (k / kSlots))
+          __nanosleep(64);
+      if (c >= nchunks) {
+        __syncwarp();
+        if (lane == 0) *reinterpret_cast<volatile int*>(&s_ready[si]) = INT_MAX;
+        break;
+      }
+      if (drift > 0 && k > drift && lane == 0)
+        while (ld_acquire_u32(S.done_chunks) < (unsigned)((k - drift) * G)) __nanosleep(128);
+      __syncwarp();
+      long long blo = LLONG_MAX, bhi = 0;
+      bool contig = worklist == nullptr;
+#pragma unroll
+      for (int j = 0; j < kChunk / 32; ++j) {
+        const int i = lane + 32 * j;
+        const int item = c * kChunk + i;
+        const bool valid = item < nitems;
+        const int v = valid ? (worklist ? worklist[item] : item) : -1;
+        const long long bb = valid ? ld_off(off + v, pol) : 0;
+        const long long ee = valid ? ld_off(off + v + 1, pol) : 0;
+        sl.v[i] = v;
+        sl.b[i] = bb;
+        sl.deg[i] = (int)(ee - bb);
+        if (valid) {
+          blo = min(blo, bb);
+          bhi = max(bhi, ee);
+        }
+      }
+      // window [A, A + len): A aligned down to 16 B, capped at kSlotStage
+      for (int o = 16; o >= 1; o >>= 1) {
+        blo = min(blo, __shfl_xor_sync(kFull, blo, o));
+        bhi = max(bhi, __shfl_xor_sync(kFull, bhi, o));
+      }
+      long long A = 0;
+      int len = 0;
+      if (contig && bhi > blo) {
+        A = blo & ~3LL;
+        len = (int)min(bhi - A, (long long)kSlotStage);
+        const int body = len & ~3;  // 16-byte copies, then 4-byte tail
+        for (int j = lane * 4; j < body; j += 128) cp_async16(&sl.stage[j], cols + A + j);
+        for (int j = body + lane; j < len; j += 32) cp_async4(&sl.stage[j], cols + A + j);
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      if (lane == 0) {
+        sl.base = A;
+        sl.len = len;
+        __threadfence_block();
+        *reinterpret_cast<volatile int*>(&s_ready[si]) = c;
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  // ------------------------------- consumers ---------------------------------
+  K1Warp& W = sm.cw[warp];
   PairLog L{LA.pairs + (size_t)blockIdx.x * LA.region_cap, LA.region_cap, &s_npairs, LA.overflow};
   unsigned gathers = 0;
-  int it = 0;
-  for (;; ++it) {
-    int pslot, pstart;
-    bool ex;
-    while (k1_pop(S, &s_mbhead, pslot, pstart, &ex))  // long-row pieces first
-      k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L, gathers);
-    int sub = -1;
-    if (lane == 0) {
-      for (;;) {
-        const unsigned long long x = atomicAdd(&s_claim, 1ull);
-        const int k = (int)(x & 0xffffffffu);
-        const int c = (int)(x >> 32);
-        if (c >= nchunks) break;
-        if (k < kSubTiles) {
-          sub = c * kSubTiles + k;
-          break;
+  bool finished = false;  // no more chunks for this warp
+  bool retired = false;   // decremented S.alive
+  for (int k = 0;;) {
+    // long-row pieces first (one call site)
+    {
+      int pslot, pstart;
+      bool ex;
+      if (k1_pop(S, &s_mbhead, pslot, pstart, &ex)) {
+        k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L,
+                                      gathers);
+        continue;
+      }
+      if (retired) {
+        int stop = 1;
+        if (S.min_deg != INT_MAX && lane == 0)
+          stop = ex && ld_acquire_u32(reinterpret_cast<const unsigned*>(S.alive)) == 0u;
+        if (__shfl_sync(kFull, stop, 0)) {
+          if (S.min_deg == INT_MAX) break;
+          // alive hit 0 after the mailbox looked empty: one last look
+          if (!k1_pop(S, &s_mbhead, pslot, pstart, &ex)) break;
+          k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L,
+                                        gathers);
+          continue;
         }
-        if (k == kSubTiles) {  // first to overflow claims the next chunk for the CTA
-          const int nc = (int)atomicAdd(&ctrl->tile_cursor, 1ull);
-          atomicExch(&s_claim, ((unsigned long long)(unsigned)nc << 32) | 1ull);
-          if (nc < nchunks) sub = nc * kSubTiles;
-          break;
-        }
-        __nanosleep(20);
+        __nanosleep(200);
+        continue;
       }
     }
-    sub = __shfl_sync(kFull, sub, 0);
-    if (sub < 0) break;
-    const int table = it & 1;
-    const int item = sub * 32 + lane;
-    const bool valid = item < nitems;
-    const int v = valid ? (worklist ? worklist[item] : item) : n;
-    const long long b = ld_off(off + v, pol);
-    const long long e = valid ? ld_off(off + v + 1, pol) : b;
-    const int deg = (int)(e - b);
+    const int si = k % kSlots;
+    const int expect = blockIdx.x + k * G;
+    int rdy = 0;
+    if (!finished) {
+      if (lane == 0) rdy = *reinterpret_cast<volatile int*>(&s_ready[si]);
+      rdy = __shfl_sync(kFull, rdy, 0);
+      if (rdy != expect && rdy != INT_MAX) {
+        __nanosleep(32);
+        continue;
+      }
+      __threadfence_block();
+      if (rdy == INT_MAX) finished = true;
+    }
+    const K1Slot& sl = sm.slot[si];
+    const int i = warp * 32 + lane;
+    const int v = finished ? -1 : sl.v[i];
+    const bool valid = v >= 0;
+    const long long b = valid ? sl.b[i] : 0;
+    const int deg = valid ? sl.deg[i] : 0;
+    const StageWin sw{sl.stage, finished ? 0 : sl.base, finished ? 0 : sl.len};
+    const int table = k & 1;
     if (valid && deg == 0) st_color(cdst + v, 0);  // limit 0: only colour 0
-    const bool small = valid && deg >= 1 && deg <= kSmallMax;
-    const bool med = valid && deg > kSmallMax && deg < S.min_deg;
     k1_push_long(S, v, deg, valid && deg >= S.min_deg);
-    const StageInfo si = k1_stage(cols, b, deg, W, pol);
-    k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, small, W, table, pol, L, gathers,
-                                  si);
-    k1_medium<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg, med, W, pol, L, gathers,
-                                   kLog ? W.redo[table] : nullptr, &W.nredo[table], si);
-    if (kLog && it > 0) {  // rows parked one sub-tile ago
-      k1_drain(W, table ^ 1, cdst, L);
-      k1_redo<kLower>(off, cols, cdst, W, table ^ 1, pol, L, gathers);
+    k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg,
+                                  valid && deg >= 1 && deg <= kSmallMax, W, table, pol, L,
+                                  gathers, sw);
+    // medium rows of this chunk (park mode), then the rows parked one chunk ago
+    for (int pass = 0; pass < (kLog ? 2 : 1); ++pass) {
+      int pv = v, pdeg = deg;
+      long long pb = b;
+      bool pm = valid && deg > kSmallMax && deg < S.min_deg;
+      StageWin psw = sw;
+      if (pass == 1) {
+        const int nr = W.nredo[table ^ 1];
+        pm = lane < nr;
+        pv = pm ? W.redo[table ^ 1][lane] : 0;
+        pb = pm ? ld_off(off + pv, pol) : 0;
+        pdeg = pm ? (int)(ld_off(off + pv + 1, pol) - pb) : 0;
+        psw = StageWin{sl.stage, 0, 0};
+        if (__ballot_sync(kFull, pm) == 0u) break;
+      }
+      k1_medium<kSnap, kLower, kLog>(cols, csrc, cdst, pv, pb, pdeg, pm, W, pol, L, gathers,
+                                     (kLog && pass == 0) ? W.redo[table] : nullptr,
+                                     &W.nredo[table], psw);
+      if (pass == 1 && lane == 0) W.nredo[table ^ 1] = 0;
+      __syncwarp();
     }
-  }
-  if (kLog && it > 0) {
-    k1_drain(W, (it - 1) & 1, cdst, L);
-    k1_redo<kLower>(off, cols, cdst, W, (it - 1) & 1, pol, L, gathers);
-    k1_drain(W, it & 1, cdst, L);  // table it&1 is empty: this flushes the carry slots
-  }
-  // This warp publishes nothing more; keep serving the CTA's mailbox until
-  // every warp is done publishing and the mailbox is empty.
-  if (lane == 0) atomicSub(S.alive, 1);
-  for (; S.min_deg != INT_MAX;) {
-    int pslot, pstart;
-    bool ex;
-    if (k1_pop(S, &s_mbhead, pslot, pstart, &ex)) {
-      k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L, gathers);
-      continue;
+    if (kLog)  // small rows parked one chunk ago (twice on exit: flushes the carry)
+      for (int rep = 0; rep < (finished ? 2 : 1); ++rep)
+        k1_drain(W, rep == 0 ? table ^ 1 : table, cdst, L);
+    if (!finished) {
+      __syncwarp();
+      if (lane == 0) {
+        const int old = atomicAdd(&s_consumed[si], 1);
+        if (old % kCW == kCW - 1 && S.done_chunks) atomicAdd(S.done_chunks, 1u);
+      }
+      ++k;
+    } else {
+      retired = true;
+      if (lane == 0 && S.min_deg != INT_MAX) atomicSub(S.alive, 1);
     }
-    int done = 0;
-    if (lane == 0) done = ex && ld_acquire_u32(reinterpret_cast<const unsigned*>(S.alive)) == 0u;
-    if (__shfl_sync(kFull, done, 0)) {
-      // alive == 0 was read after the mailbox looked exhausted; re-check once
-      // against the now-final allocation count
-      if (!k1_pop(S, &s_mbhead, pslot, pstart, &ex)) break;
-      k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L, gathers);
-      continue;
-    }
-    __nanosleep(200);
   }
   const unsigned g = __reduce_add_sync(kFull, gathers);
   if (lane == 0 && g) atomicAdd(&s_gathers, g);
-  __syncthreads();
+  // the producer warp has returned: count only consumer warps from here on
+  asm volatile("bar.sync 1, %0;" ::"n"(kCW * 32));
   if (threadIdx.x == 0) {
     if (s_gathers) atomicAdd(&ctrl->k1_gathers, (unsigned long long)s_gathers);
     if (kLog) {
