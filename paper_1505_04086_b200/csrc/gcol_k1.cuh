@@ -28,10 +28,11 @@ namespace gcol {
 namespace dev {
 
 constexpr int kCW = 8;                    // consumer warps per CTA
-constexpr int kK1Threads = (kCW + 1) * 32;  // + one producer warp
+constexpr int kPW = 2;                    // producer warps (alternate chunks)
+constexpr int kK1Threads = (kCW + kPW) * 32;
 constexpr int kChunk = kCW * 32;          // vertices per chunk (one sub-tile per consumer)
-constexpr int kSlots = 3;                 // staged chunks in flight per CTA
-constexpr int kSlotStage = 7168;          // adjacency entries staged per chunk (28 KB)
+constexpr int kSlots = 4;                 // staged chunks in flight per CTA (multiple of kPW)
+constexpr int kSlotStage = 6144;          // adjacency entries staged per chunk (24 KB)
 constexpr int kBmWords = 512;             // per-warp medium-row bitmap pool
 constexpr int kStaleMax = 4;              // stale neighbours remembered per parked row
 constexpr int kSplitDefault = 1024;       // rows >= this are split into pieces
@@ -596,9 +597,10 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
   }
   __syncthreads();
 
-  if (warp == kCW) {
-    // ----------------------------- producer ------------------------------
-    for (int k = 0;; ++k) {
+  if (warp >= kCW) {
+    // ----------------------------- producers -----------------------------
+    // producer warp p stages chunks k = p, p + kPW, ... (slots k % kSlots)
+    for (int k = warp - kCW;; k += kPW) {
       const int c = blockIdx.x + k * G;
       const int si = k % kSlots;
       K1Slot& sl = sm.slot[si];
@@ -754,7 +756,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
   }
   const unsigned g = __reduce_add_sync(kFull, gathers);
   if (lane == 0 && g) atomicAdd(&s_gathers, g);
-  // the producer warp has returned: count only consumer warps from here on
+  // the producer warps have returned: count only consumer warps from here on
   asm volatile("bar.sync 1, %0;" ::"n"(kCW * 32));
   if (threadIdx.x == 0) {
     if (s_gathers) atomicAdd(&ctrl->k1_gathers, (unsigned long long)s_gathers);
