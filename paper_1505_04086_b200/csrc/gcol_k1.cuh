@@ -156,22 +156,21 @@ __device__ __forceinline__ void k1_small(const int* __restrict__ cols, const int
   bool active = small;
   int ns = 0;
   unsigned long long mask = 0ull;
-  constexpr int U = 8;
-  for (int k = 0; k < maxk; k += U) {
-    int w[U];
-    bool take[U];
+  for (int k = 0; k < maxk; k += 4) {
+    int w[4];
+    bool take[4];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const bool in = active && (k + u) < deg;
       w[u] = in ? (inwin ? rs[k + u] : ld_col(cols + b + k + u, pol)) : 0;
       take[u] = in && (!kLower || w[u] < v);
       if (kLower && in && w[u] > v) active = false;  // sorted row: the rest is > v
     }
-    int c[U];
+    int c[4];
 #pragma unroll
-    for (int u = 0; u < U; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
+    for (int u = 0; u < 4; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < 4; ++u) {
       gathers += take[u];
       if (c[u] >= 0 && c[u] <= deg) mask |= 1ull << c[u];
       if (kLog) {
@@ -198,37 +197,22 @@ __device__ __forceinline__ void k1_small(const int* __restrict__ cols, const int
   __syncwarp();
 }
 
-// Re-check of parked rows, split in two so the colour loads of the check
-// (k1_drain_load) are in flight together with the next chunk's gathers.
-struct DrainLoads {
-  int cc[kStaleMax];  // carry slot
-  int ct[kStaleMax];  // table slot
-};
-
-__device__ __forceinline__ DrainLoads k1_drain_load(const K1Warp& W, int table, const int* cdst) {
+// Re-check the rows parked in `table` (warp-collective).  A row whose
+// in-flight neighbours have all committed is committed now; otherwise it
+// gets one more sub-tile in the lane's carry slot, and whatever is still
+// uncoloured at that second check is logged for round 1.
+__device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L) {
   const int lane = lane_id();
-  DrainLoads D;
-  const int vc = W.cv[lane];
-  const int nc = vc >= 0 ? (int)W.cns[lane] : 0;
-  const int vt = W.dv[table][lane];
-  const int nt = vt >= 0 ? (int)W.dns[table][lane] : 0;
-#pragma unroll
-  for (int k = 0; k < kStaleMax; ++k) {
-    D.cc[k] = k < nc ? ld_color(cdst + W.cst[lane][k]) : -2;
-    D.ct[k] = k < nt ? ld_color(cdst + W.dst[table][lane][k]) : -2;
-  }
-  return D;
-}
-
-// A row whose in-flight neighbours have all committed is committed now;
-// otherwise it gets one more chunk in the lane's carry slot, and whatever
-// is still uncoloured at that second check is logged for round 1.
-__device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L,
-                                         const DrainLoads& D) {
-  const int lane = lane_id();
-  {  // (1) carry slot: final check
+  // (1) carry slot: final check
+  {
     const int v = W.cv[lane];
     const int ns = v >= 0 ? (int)W.cns[lane] : 0;
+    int c[kStaleMax], u[kStaleMax];
+#pragma unroll
+    for (int k = 0; k < kStaleMax; ++k) {
+      u[k] = k < ns ? W.cst[lane][k] : 0;
+      c[k] = k < ns ? ld_color(cdst + u[k]) : -2;
+    }
     unsigned long long mask = 0ull;
     int deg = 0;
     if (v >= 0) {
@@ -237,18 +221,23 @@ __device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const 
     }
 #pragma unroll
     for (int k = 0; k < kStaleMax; ++k) {
-      const int c = D.cc[k];
-      if (c >= 0 && c <= deg) mask |= 1ull << c;
-      log_pairs(L, k < ns && c == -1, k < ns ? W.cst[lane][k] : 0, v);
+      if (c[k] >= 0 && c[k] <= deg) mask |= 1ull << c[k];
+      log_pairs(L, k < ns && c[k] == -1, u[k], v);  // still in flight: round 1 checks it
     }
     if (v >= 0) {
       st_color(cdst + v, __ffsll((long long)~mask) - 1);
       W.cv[lane] = -1;
     }
   }
-  // (2) rows parked one chunk ago
+  // (2) rows parked one sub-tile ago
   const int v = W.dv[table][lane];
   const int ns = v >= 0 ? (int)W.dns[table][lane] : 0;
+  int c[kStaleMax], u[kStaleMax];
+#pragma unroll
+  for (int k = 0; k < kStaleMax; ++k) {
+    u[k] = k < ns ? W.dst[table][lane][k] : 0;
+    c[k] = k < ns ? ld_color(cdst + u[k]) : -2;
+  }
   if (v >= 0) {
     unsigned long long mask = (unsigned long long)W.dmask[table][lane][0] |
                               ((unsigned long long)W.dmask[table][lane][1] << 32);
@@ -256,9 +245,8 @@ __device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const 
     int left = 0;
 #pragma unroll
     for (int k = 0; k < kStaleMax; ++k) {
-      const int c = D.ct[k];
-      if (c >= 0 && c <= deg) mask |= 1ull << c;
-      if (k < ns && c == -1) W.cst[lane][left++] = W.dst[table][lane][k];
+      if (c[k] >= 0 && c[k] <= deg) mask |= 1ull << c[k];
+      if (k < ns && c[k] == -1) W.cst[lane][left++] = u[k];
     }
     if (left == 0) {
       st_color(cdst + v, __ffsll((long long)~mask) - 1);
@@ -726,8 +714,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
     const StageWin sw{sl.stage, finished ? 0 : sl.base, finished ? 0 : sl.len};
     const int table = k & 1;
     if (valid && deg == 0) st_color(cdst + v, 0);  // limit 0: only colour 0
-    DrainLoads dl;
-    if (kLog) dl = k1_drain_load(W, table ^ 1, cdst);  // in flight with this chunk's gathers
     k1_push_long(S, v, deg, valid && deg >= S.min_deg);
     k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg,
                                   valid && deg >= 1 && deg <= kSmallMax, W, table, pol, L,
@@ -754,10 +740,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
       __syncwarp();
     }
     if (kLog)  // small rows parked one chunk ago (twice on exit: flushes the carry)
-      for (int rep = 0; rep < (finished ? 2 : 1); ++rep) {
-        if (rep == 1) dl = k1_drain_load(W, table, cdst);
-        k1_drain(W, rep == 0 ? table ^ 1 : table, cdst, L, dl);
-      }
+      for (int rep = 0; rep < (finished ? 2 : 1); ++rep)
+        k1_drain(W, rep == 0 ? table ^ 1 : table, cdst, L);
     if (!finished) {
       __syncwarp();
       if (lane == 0) {
