@@ -694,6 +694,17 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
   GCOL_CK(cudaStreamSynchronize(g->stream));
   const int rounds = hdr.round;
+  if (std::getenv("GCOL_K1_PROFILE")) {
+    const double ch = hdr.prof[5] ? static_cast<double>(hdr.prof[5]) : 1.0;
+    const double pc = hdr.prof[11] ? static_cast<double>(hdr.prof[11]) : 1.0;
+    std::fprintf(stderr,
+                 "[k1 profile] consumer cycles/chunk: wait %.0f piece %.0f small %.0f medium %.0f "
+                 "drain %.0f (chunks %llu) | producer cycles/chunk: slot %.0f drift %.0f load %.0f "
+                 "(chunks %llu)\n",
+                 hdr.prof[0] / ch, hdr.prof[1] / ch, hdr.prof[2] / ch, hdr.prof[3] / ch,
+                 hdr.prof[4] / ch, static_cast<unsigned long long>(hdr.prof[5]), hdr.prof[8] / pc,
+                 hdr.prof[9] / pc, hdr.prof[10] / pc, static_cast<unsigned long long>(hdr.prof[11]));
+  }
   std::vector<unsigned long long> cpr(std::min(rounds, kMaxRoundsRecorded));
   if (!cpr.empty())
     GCOL_CK(cudaMemcpyAsync(cpr.data(), g->d_ctrl->cpr, sizeof(unsigned long long) * cpr.size(),

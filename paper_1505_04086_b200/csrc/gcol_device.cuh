@@ -57,6 +57,7 @@ struct Ctrl {
   int capped;
   int cand_total;                   // round-1 candidates
   int done;                         // loop exit flag (eager mode reads it)
+  unsigned long long prof[16];      // K1 phase cycle counters (GCOL_K1_PROFILE)
   unsigned long long cpr[kMaxRoundsRecorded];  // conflicts_per_round
 };
 

@@ -600,13 +600,17 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
   if (warp >= kCW) {
     // ----------------------------- producers -----------------------------
     // producer warp p stages chunks k = p, p + kPW, ... (slots k % kSlots)
+    long long pt_slot = 0, pt_drift = 0, pt_load = 0, pchunks = 0;
     for (int k = warp - kCW;; k += kPW) {
       const int c = blockIdx.x + k * G;
       const int si = k % kSlots;
       K1Slot& sl = sm.slot[si];
+      long long t0 = clock64();
       if (k >= kSlots)  // previous use of this slot fully consumed
         while (*reinterpret_cast<volatile int*>(&s_consumed[si]) < kCW * (k / kSlots))
           __nanosleep(64);
+      long long t1 = clock64();
+      pt_slot += t1 - t0;
       if (c >= nchunks) {
         __syncwarp();
         if (lane == 0) *reinterpret_cast<volatile int*>(&s_ready[si]) = INT_MAX;
@@ -615,6 +619,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
       if (drift > 0 && k > drift && lane == 0)
         while (ld_acquire_u32(S.done_chunks) < (unsigned)((k - drift) * G)) __nanosleep(128);
       __syncwarp();
+      long long t2 = clock64();
+      pt_drift += t2 - t1;
       long long blo = LLONG_MAX, bhi = 0;
       bool contig = worklist == nullptr;
 #pragma unroll
@@ -656,6 +662,14 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
         *reinterpret_cast<volatile int*>(&s_ready[si]) = c;
       }
       __syncwarp();
+      pt_load += clock64() - t2;
+      ++pchunks;
+    }
+    if (lane == 0) {
+      atomicAdd(&ctrl->prof[8], (unsigned long long)pt_slot);
+      atomicAdd(&ctrl->prof[9], (unsigned long long)pt_drift);
+      atomicAdd(&ctrl->prof[10], (unsigned long long)pt_load);
+      atomicAdd(&ctrl->prof[11], (unsigned long long)pchunks);
     }
     return;
   }
@@ -666,14 +680,18 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
   unsigned gathers = 0;
   bool finished = false;  // no more chunks for this warp
   bool retired = false;   // decremented S.alive
+  long long ct_wait = 0, ct_piece = 0, ct_small = 0, ct_med = 0, ct_drain = 0, cchunks = 0;
+  long long tw = clock64();
   for (int k = 0;;) {
     // long-row pieces first (one call site)
     {
       int pslot, pstart;
       bool ex;
       if (k1_pop(S, &s_mbhead, pslot, pstart, &ex)) {
+        const long long tp = clock64();
         k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L,
                                       gathers);
+        ct_piece += clock64() - tp;
         continue;
       }
       if (retired) {
@@ -705,6 +723,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
       __threadfence_block();
       if (rdy == INT_MAX) finished = true;
     }
+    long long ta = clock64();
+    ct_wait += ta - tw;
     const K1Slot& sl = sm.slot[si];
     const int i = warp * 32 + lane;
     const int v = finished ? -1 : sl.v[i];
@@ -718,6 +738,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
     k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg,
                                   valid && deg >= 1 && deg <= kSmallMax, W, table, pol, L,
                                   gathers, sw);
+    long long tb = clock64();
+    ct_small += tb - ta;
     // medium rows of this chunk (park mode), then the rows parked one chunk ago
     for (int pass = 0; pass < (kLog ? 2 : 1); ++pass) {
       int pv = v, pdeg = deg;
@@ -739,9 +761,14 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
       if (pass == 1 && lane == 0) W.nredo[table ^ 1] = 0;
       __syncwarp();
     }
+    long long tc = clock64();
+    ct_med += tc - tb;
     if (kLog)  // small rows parked one chunk ago (twice on exit: flushes the carry)
       for (int rep = 0; rep < (finished ? 2 : 1); ++rep)
         k1_drain(W, rep == 0 ? table ^ 1 : table, cdst, L);
+    tw = clock64();
+    ct_drain += tw - tc;
+    ++cchunks;
     if (!finished) {
       __syncwarp();
       if (lane == 0) {
@@ -753,6 +780,14 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
       retired = true;
       if (lane == 0 && S.min_deg != INT_MAX) atomicSub(S.alive, 1);
     }
+  }
+  if (lane == 0) {
+    atomicAdd(&ctrl->prof[0], (unsigned long long)ct_wait);
+    atomicAdd(&ctrl->prof[1], (unsigned long long)ct_piece);
+    atomicAdd(&ctrl->prof[2], (unsigned long long)ct_small);
+    atomicAdd(&ctrl->prof[3], (unsigned long long)ct_med);
+    atomicAdd(&ctrl->prof[4], (unsigned long long)ct_drain);
+    atomicAdd(&ctrl->prof[5], (unsigned long long)cchunks);
   }
   const unsigned g = __reduce_add_sync(kFull, gathers);
   if (lane == 0 && g) atomicAdd(&s_gathers, g);
