@@ -28,7 +28,7 @@ namespace gcol {
 namespace dev {
 
 constexpr int kCW = 8;                    // consumer warps per CTA
-constexpr int kPW = 2;                    // producer warps (alternate chunks)
+constexpr int kPW = 1;                    // producer warp (TMA bulk copies)
 constexpr int kK1Threads = (kCW + kPW) * 32;
 constexpr int kChunk = kCW * 32;          // vertices per chunk (one sub-tile per consumer)
 constexpr int kSlots = 4;                 // staged chunks in flight per CTA (multiple of kPW)
@@ -58,16 +58,20 @@ struct K1Warp {
 };
 
 // One staged chunk: its rows and (a window of) their adjacency.
-struct K1Slot {
-  long long b[kChunk];                 // row starts
-  int v[kChunk];                       // vertex ids (-1: none)
-  int deg[kChunk];
-  int stage[kSlotStage];               // cols[base .. base + len)
+struct alignas(16) K1Slot {
+  alignas(16) long long offs[kChunk + 2];          // contiguous mode: off[c0 .. c0 + rows]; worklist: b[]
+  int wv[kChunk];                      // worklist mode: vertex ids
+  int wdeg[kChunk];                    // worklist mode: degrees
+  alignas(16) int stage[kSlotStage];   // cols[base .. base + len)
   long long base;
   int len;
+  int chunk;                           // chunk index, -1: no more chunks
+  int rows;
+  unsigned long long full;             // mbarrier: slot staged (TMA tx + producer arrive)
+  unsigned long long offb;             // mbarrier: offsets staged (producer only)
 };
 
-struct K1Smem {
+struct alignas(16) K1Smem {
   K1Slot slot[kSlots];
   K1Warp cw[kCW];
 };
@@ -535,6 +539,46 @@ __device__ __forceinline__ void k1_piece(const long long* __restrict__ off, cons
   __syncwarp();
 }
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// 1-D TMA bulk copy global -> shared, completion counted on `bar`.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                    static_cast<unsigned>(__cvta_generic_to_shared(smem))),
@@ -582,7 +626,10 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
   if (threadIdx.x < kSlots) {
     s_ready[threadIdx.x] = -1;
     s_consumed[threadIdx.x] = 0;
+    mbar_init(&sm.slot[threadIdx.x].full, 1);
+    mbar_init(&sm.slot[threadIdx.x].offb, 1);
   }
+  if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   if (threadIdx.x == 0) {
     s_npairs = 0;
     s_gathers = 0;
@@ -598,71 +645,93 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
   __syncthreads();
 
   if (warp >= kCW) {
-    // ----------------------------- producers -----------------------------
-    // producer warp p stages chunks k = p, p + kPW, ... (slots k % kSlots)
+    // ------------------------------ producer ------------------------------
+    // Lane 0 drives TMA: per chunk one bulk copy of its offsets (waited for
+    // here) and one of its adjacency window (waited for by the consumers on
+    // the slot's `full` barrier).  Offsets of chunk k+1 are requested before
+    // the adjacency of chunk k is published, so both stay in flight.
     long long pt_slot = 0, pt_drift = 0, pt_load = 0, pchunks = 0;
-    for (int k = warp - kCW;; k += kPW) {
+    const bool contig = worklist == nullptr;
+    auto request_offsets = [&](int k) {  // lane 0 only, contiguous mode
+      const int c = blockIdx.x + k * G;
+      if (c >= nchunks) return;
+      K1Slot& sl = sm.slot[k % kSlots];
+      const int c0 = c * kChunk;
+      const int rows = min(kChunk, nitems - c0);
+      const int cnt = rows + 1;           // off[c0 .. c0 + rows]
+      const int bulk = cnt & ~1;          // whole 16-byte pairs
+      if (cnt & 1) sl.offs[cnt - 1] = ld_off(off + c0 + cnt - 1, pol);
+      mbar_arrive_expect_tx(&sl.offb, (unsigned)(bulk * 8));
+      tma_load_1d(sl.offs, off + c0, (unsigned)(bulk * 8), &sl.offb);
+    };
+    if (lane == 0 && contig) request_offsets(0);
+    for (int k = 0;; ++k) {
       const int c = blockIdx.x + k * G;
       const int si = k % kSlots;
       K1Slot& sl = sm.slot[si];
+      const unsigned par = (unsigned)((k / kSlots) & 1);
       long long t0 = clock64();
-      if (k >= kSlots)  // previous use of this slot fully consumed
-        while (*reinterpret_cast<volatile int*>(&s_consumed[si]) < kCW * (k / kSlots))
-          __nanosleep(64);
-      long long t1 = clock64();
-      pt_slot += t1 - t0;
       if (c >= nchunks) {
-        __syncwarp();
-        if (lane == 0) *reinterpret_cast<volatile int*>(&s_ready[si]) = INT_MAX;
+        if (lane == 0) {
+          if (k >= kSlots)
+            while (*reinterpret_cast<volatile int*>(&s_consumed[si]) < kCW * (k / kSlots))
+              __nanosleep(64);
+          sl.chunk = -1;
+          mbar_arrive_expect_tx(&sl.full, 0u);
+        }
         break;
       }
       if (drift > 0 && k > drift && lane == 0)
         while (ld_acquire_u32(S.done_chunks) < (unsigned)((k - drift) * G)) __nanosleep(128);
-      __syncwarp();
-      long long t2 = clock64();
-      pt_drift += t2 - t1;
-      long long blo = LLONG_MAX, bhi = 0;
-      bool contig = worklist == nullptr;
-#pragma unroll
-      for (int j = 0; j < kChunk / 32; ++j) {
-        const int i = lane + 32 * j;
-        const int item = c * kChunk + i;
-        const bool valid = item < nitems;
-        const int v = valid ? (worklist ? worklist[item] : item) : -1;
-        const long long bb = valid ? ld_off(off + v, pol) : 0;
-        const long long ee = valid ? ld_off(off + v + 1, pol) : 0;
-        sl.v[i] = v;
-        sl.b[i] = bb;
-        sl.deg[i] = (int)(ee - bb);
-        if (valid) {
-          blo = min(blo, bb);
-          bhi = max(bhi, ee);
+      long long t1 = clock64();
+      pt_drift += t1 - t0;
+      const int c0 = c * kChunk;
+      const int rows = min(kChunk, nitems - c0);
+      if (contig) {
+        if (lane == 0) {
+          mbar_wait(&sl.offb, par);            // offsets of chunk k
+          // next chunk's offsets go out now (its slot must be free)
+          const int kn = k + 1;
+          if (kn >= kSlots)
+            while (*reinterpret_cast<volatile int*>(&s_consumed[kn % kSlots]) <
+                   kCW * (kn / kSlots))
+              __nanosleep(64);
+          request_offsets(kn);
+          const long long blo = sl.offs[0], bhi = sl.offs[rows];
+          const long long A = blo & ~3LL;
+          const int len = (int)min(bhi - A, (long long)kSlotStage);
+          const int bulk = len & ~3;
+          for (int j = bulk; j < len; ++j) sl.stage[j] = ld_col(cols + A + j, pol);
+          sl.base = A;
+          sl.len = len;
+          sl.rows = rows;
+          sl.chunk = c;
+          mbar_arrive_expect_tx(&sl.full, (unsigned)(bulk * 4));
+          if (bulk) tma_load_1d(sl.stage, cols + A, (unsigned)(bulk * 4), &sl.full);
+        }
+      } else {  // worklist mode: per-row loads, nothing staged
+        if (k >= kSlots)
+          while (*reinterpret_cast<volatile int*>(&s_consumed[si]) < kCW * (k / kSlots))
+            __nanosleep(64);
+        for (int i = lane; i < kChunk; i += 32) {
+          const bool valid = i < rows;
+          const int v = valid ? worklist[c0 + i] : -1;
+          const long long bb = valid ? ld_off(off + v, pol) : 0;
+          sl.wv[i] = v;
+          sl.offs[i] = bb;
+          sl.wdeg[i] = valid ? (int)(ld_off(off + v + 1, pol) - bb) : 0;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          sl.base = 0;
+          sl.len = 0;
+          sl.rows = rows;
+          sl.chunk = c;
+          mbar_arrive_expect_tx(&sl.full, 0u);
         }
       }
-      // window [A, A + len): A aligned down to 16 B, capped at kSlotStage
-      for (int o = 16; o >= 1; o >>= 1) {
-        blo = min(blo, __shfl_xor_sync(kFull, blo, o));
-        bhi = max(bhi, __shfl_xor_sync(kFull, bhi, o));
-      }
-      long long A = 0;
-      int len = 0;
-      if (contig && bhi > blo) {
-        A = blo & ~3LL;
-        len = (int)min(bhi - A, (long long)kSlotStage);
-        const int body = len & ~3;  // 16-byte copies, then 4-byte tail
-        for (int j = lane * 4; j < body; j += 128) cp_async16(&sl.stage[j], cols + A + j);
-        for (int j = body + lane; j < len; j += 32) cp_async4(&sl.stage[j], cols + A + j);
-      }
-      cp_async_wait_all();
       __syncwarp();
-      if (lane == 0) {
-        sl.base = A;
-        sl.len = len;
-        __threadfence_block();
-        *reinterpret_cast<volatile int*>(&s_ready[si]) = c;
-      }
-      __syncwarp();
-      pt_load += clock64() - t2;
+      pt_load += clock64() - t1;
       ++pchunks;
     }
     if (lane == 0) {
@@ -711,26 +780,33 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
       }
     }
     const int si = k % kSlots;
-    const int expect = blockIdx.x + k * G;
-    int rdy = 0;
     if (!finished) {
-      if (lane == 0) rdy = *reinterpret_cast<volatile int*>(&s_ready[si]);
-      rdy = __shfl_sync(kFull, rdy, 0);
-      if (rdy != expect && rdy != INT_MAX) {
+      int ok = 0;
+      if (lane == 0) ok = mbar_try_wait(&sm.slot[si].full, (unsigned)((k / kSlots) & 1));
+      if (!__shfl_sync(kFull, ok, 0)) {
         __nanosleep(32);
         continue;
       }
-      __threadfence_block();
-      if (rdy == INT_MAX) finished = true;
+      if (sm.slot[si].chunk < 0) finished = true;
     }
     long long ta = clock64();
     ct_wait += ta - tw;
     const K1Slot& sl = sm.slot[si];
     const int i = warp * 32 + lane;
-    const int v = finished ? -1 : sl.v[i];
-    const bool valid = v >= 0;
-    const long long b = valid ? sl.b[i] : 0;
-    const int deg = valid ? sl.deg[i] : 0;
+    const bool valid = !finished && i < sl.rows;
+    int v = -1, deg = 0;
+    long long b = 0;
+    if (valid) {
+      if (worklist) {
+        v = sl.wv[i];
+        b = sl.offs[i];
+        deg = sl.wdeg[i];
+      } else {
+        v = sl.chunk * kChunk + i;
+        b = sl.offs[i];
+        deg = (int)(sl.offs[i + 1] - b);
+      }
+    }
     const StageWin sw{sl.stage, finished ? 0 : sl.base, finished ? 0 : sl.len};
     const int table = k & 1;
     if (valid && deg == 0) st_color(cdst + v, 0);  // limit 0: only colour 0
