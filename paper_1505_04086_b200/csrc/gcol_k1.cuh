@@ -35,7 +35,6 @@ constexpr int kSlots = 4;                 // staged chunks in flight per CTA (mu
 constexpr int kSlotStage = 6144;          // adjacency entries staged per chunk (24 KB)
 constexpr int kBmWords = 512;             // per-warp medium-row bitmap pool
 constexpr int kStaleMax = 4;              // stale neighbours remembered per parked row
-constexpr int kDT = 3;                    // deferral tables: parked at chunk k, re-checked at k+2
 constexpr int kSplitDefault = 1024;       // rows >= this are split into pieces
 constexpr int kPiece = 1024;              // entries per piece
 constexpr int kDriftDefault = 2;          // max rounds a CTA may run ahead
@@ -44,11 +43,11 @@ constexpr int kDriftDefault = 2;          // max rounds a CTA may run ahead
 struct K1Warp {
   unsigned bm[kBmWords];               // medium-row bitmaps
   unsigned win[32];                    // window for the rare overflow path
-  int dv[kDT][32];                     // parked row per lane (rotating tables)
-  unsigned dmask[kDT][32][2];
-  unsigned char ddeg[kDT][32];
-  unsigned char dns[kDT][32];
-  int dst[kDT][32][kStaleMax];         // in-flight neighbours to re-check
+  int dv[2][32];                       // parked row per lane (ping-pong tables)
+  unsigned dmask[2][32][2];
+  unsigned char ddeg[2][32];
+  unsigned char dns[2][32];
+  int dst[2][32][kStaleMax];           // in-flight neighbours to re-check
   int cv[32];                          // second-chance slot per lane (carry)
   unsigned cmask[32][2];
   unsigned char cdeg[32];
@@ -161,22 +160,21 @@ __device__ __forceinline__ void k1_small(const int* __restrict__ cols, const int
   bool active = small;
   int ns = 0;
   unsigned long long mask = 0ull;
-  constexpr int U = 16;  // one round trip covers the lower half of rows up to degree ~32
-  for (int k = 0; k < maxk; k += U) {
-    int w[U];
-    bool take[U];
+  for (int k = 0; k < maxk; k += 4) {
+    int w[4];
+    bool take[4];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const bool in = active && (k + u) < deg;
       w[u] = in ? (inwin ? rs[k + u] : ld_col(cols + b + k + u, pol)) : 0;
       take[u] = in && (!kLower || w[u] < v);
       if (kLower && in && w[u] > v) active = false;  // sorted row: the rest is > v
     }
-    int c[U];
+    int c[4];
 #pragma unroll
-    for (int u = 0; u < U; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
+    for (int u = 0; u < 4; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < 4; ++u) {
       gathers += take[u];
       if (c[u] >= 0 && c[u] <= deg) mask |= 1ull << c[u];
       if (kLog) {
@@ -203,37 +201,22 @@ __device__ __forceinline__ void k1_small(const int* __restrict__ cols, const int
   __syncwarp();
 }
 
-// Re-check of parked rows, split in two so the colour loads of the check
-// (k1_drain_load) are in flight together with the current chunk's gathers.
-struct DrainLoads {
-  int cc[kStaleMax];  // carry slot
-  int ct[kStaleMax];  // table slot
-};
-
-__device__ __forceinline__ DrainLoads k1_drain_load(const K1Warp& W, int table, const int* cdst) {
+// Re-check the rows parked in `table` (warp-collective).  A row whose
+// in-flight neighbours have all committed is committed now; otherwise it
+// gets one more sub-tile in the lane's carry slot, and whatever is still
+// uncoloured at that second check is logged for round 1.
+__device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L) {
   const int lane = lane_id();
-  DrainLoads D;
-  const int vc = W.cv[lane];
-  const int nc = vc >= 0 ? (int)W.cns[lane] : 0;
-  const int vt = W.dv[table][lane];
-  const int nt = vt >= 0 ? (int)W.dns[table][lane] : 0;
-#pragma unroll
-  for (int k = 0; k < kStaleMax; ++k) {
-    D.cc[k] = k < nc ? ld_color(cdst + W.cst[lane][k]) : -2;
-    D.ct[k] = k < nt ? ld_color(cdst + W.dst[table][lane][k]) : -2;
-  }
-  return D;
-}
-
-// A parked row whose in-flight neighbours have all committed is committed;
-// otherwise it gets one more chunk in the lane's carry slot, and whatever
-// is still uncoloured at that last check is logged for round 1.
-__device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L,
-                                         const DrainLoads& D) {
-  const int lane = lane_id();
-  {  // (1) carry slot: final check
+  // (1) carry slot: final check
+  {
     const int v = W.cv[lane];
     const int ns = v >= 0 ? (int)W.cns[lane] : 0;
+    int c[kStaleMax], u[kStaleMax];
+#pragma unroll
+    for (int k = 0; k < kStaleMax; ++k) {
+      u[k] = k < ns ? W.cst[lane][k] : 0;
+      c[k] = k < ns ? ld_color(cdst + u[k]) : -2;
+    }
     unsigned long long mask = 0ull;
     int deg = 0;
     if (v >= 0) {
@@ -242,18 +225,23 @@ __device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const 
     }
 #pragma unroll
     for (int k = 0; k < kStaleMax; ++k) {
-      const int c = D.cc[k];
-      if (c >= 0 && c <= deg) mask |= 1ull << c;
-      log_pairs(L, k < ns && c == -1, k < ns ? W.cst[lane][k] : 0, v);
+      if (c[k] >= 0 && c[k] <= deg) mask |= 1ull << c[k];
+      log_pairs(L, k < ns && c[k] == -1, u[k], v);  // still in flight: round 1 checks it
     }
     if (v >= 0) {
       st_color(cdst + v, __ffsll((long long)~mask) - 1);
       W.cv[lane] = -1;
     }
   }
-  // (2) rows of `table`
+  // (2) rows parked one sub-tile ago
   const int v = W.dv[table][lane];
   const int ns = v >= 0 ? (int)W.dns[table][lane] : 0;
+  int c[kStaleMax], u[kStaleMax];
+#pragma unroll
+  for (int k = 0; k < kStaleMax; ++k) {
+    u[k] = k < ns ? W.dst[table][lane][k] : 0;
+    c[k] = k < ns ? ld_color(cdst + u[k]) : -2;
+  }
   if (v >= 0) {
     unsigned long long mask = (unsigned long long)W.dmask[table][lane][0] |
                               ((unsigned long long)W.dmask[table][lane][1] << 32);
@@ -261,9 +249,8 @@ __device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const 
     int left = 0;
 #pragma unroll
     for (int k = 0; k < kStaleMax; ++k) {
-      const int c = D.ct[k];
-      if (c >= 0 && c <= deg) mask |= 1ull << c;
-      if (k < ns && c == -1) W.cst[lane][left++] = W.dst[table][lane][k];
+      if (c[k] >= 0 && c[k] <= deg) mask |= 1ull << c[k];
+      if (k < ns && c[k] == -1) W.cst[lane][left++] = u[k];
     }
     if (left == 0) {
       st_color(cdst + v, __ffsll((long long)~mask) - 1);
@@ -325,12 +312,11 @@ __device__ __forceinline__ void k1_medium(const int* __restrict__ cols, const in
     const int Wt = __shfl_sync(kFull, inb ? wincl : 0, 31 - __clz(batch));
     for (int i = lane; i < Wt; i += 32) W.bm[i] = 0u;
     __syncwarp();
-    constexpr int UM = 8;
-    for (int i0 = 0; i0 < E; i0 += 32 * UM) {
-      int w[UM], r[UM], vr[UM], dr[UM];
-      bool take[UM];
+    for (int i0 = 0; i0 < E; i0 += 32 * 4) {
+      int w[4], r[4], vr[4], dr[4];
+      bool take[4];
 #pragma unroll
-      for (int u = 0; u < UM; ++u) {
+      for (int u = 0; u < 4; ++u) {
         const int idx = i0 + u * 32 + lane;
         const bool in = idx < E;
         const int lo = row_of(eoff, idx);
@@ -344,11 +330,11 @@ __device__ __forceinline__ void k1_medium(const int* __restrict__ cols, const in
                              : ld_col(cols + br + (idx - er), pol));
         take[u] = in && (!kLower || w[u] < vr[u]);
       }
-      int c[UM];
+      int c[4];
 #pragma unroll
-      for (int u = 0; u < UM; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
+      for (int u = 0; u < 4; ++u) c[u] = take[u] ? read_color<kSnap>(csrc, w[u]) : -2;
 #pragma unroll
-      for (int u = 0; u < UM; ++u) {
+      for (int u = 0; u < 4; ++u) {
         gathers += take[u];
         const int wo = __shfl_sync(kFull, woff, r[u]);
         const int nw = __shfl_sync(kFull, words, r[u]);
@@ -622,7 +608,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // rounds ahead of the slowest one.
 // ---------------------------------------------------------------------------
 template <bool kSnap, bool kLower, bool kLog>
-__global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __restrict__ off,
+__global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restrict__ off,
                                                       const int* __restrict__ cols, int n,
                                                       int nitems, const int* worklist,
                                                       const int* csrc, int* cdst, Ctrl* ctrl,
@@ -651,7 +637,8 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __rest
   }
   if (warp < kCW) {
     K1Warp& W = sm.cw[warp];
-    for (int t = 0; t < kDT; ++t) W.dv[t][lane] = -1;
+    W.dv[0][lane] = -1;
+    W.dv[1][lane] = -1;
     W.cv[lane] = -1;
     if (lane < 2) W.nredo[lane] = 0;
   }
@@ -821,12 +808,8 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __rest
       }
     }
     const StageWin sw{sl.stage, finished ? 0 : sl.base, finished ? 0 : sl.len};
-    const int table = k % kDT;          // rows parked now
-    const int dtab = (k + 1) % kDT;     // rows parked two chunks ago: re-checked now
-    const int rtab = k & 1;             // medium redo ping-pong
+    const int table = k & 1;
     if (valid && deg == 0) st_color(cdst + v, 0);  // limit 0: only colour 0
-    DrainLoads dl;
-    if (kLog) dl = k1_drain_load(W, dtab, cdst);  // in flight with this chunk's gathers
     k1_push_long(S, v, deg, valid && deg >= S.min_deg);
     k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg,
                                   valid && deg >= 1 && deg <= kSmallMax, W, table, pol, L,
@@ -834,36 +817,31 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __rest
     long long tb = clock64();
     ct_small += tb - ta;
     // medium rows of this chunk (park mode), then the rows parked one chunk ago
-    const bool med0 = valid && deg > kSmallMax && deg < S.min_deg;
-    if (__any_sync(kFull, med0) || (kLog && W.nredo[rtab ^ 1] > 0))
-      for (int pass = 0; pass < (kLog ? 2 : 1); ++pass) {
-        int pv = v, pdeg = deg;
-        long long pb = b;
-        bool pm = med0;
-        StageWin psw = sw;
-        if (pass == 1) {
-          const int nr = W.nredo[rtab ^ 1];
-          pm = lane < nr;
-          pv = pm ? W.redo[rtab ^ 1][lane] : 0;
-          pb = pm ? ld_off(off + pv, pol) : 0;
-          pdeg = pm ? (int)(ld_off(off + pv + 1, pol) - pb) : 0;
-          psw = StageWin{sl.stage, 0, 0};
-          if (__ballot_sync(kFull, pm) == 0u) break;
-        }
-        k1_medium<kSnap, kLower, kLog>(cols, csrc, cdst, pv, pb, pdeg, pm, W, pol, L, gathers,
-                                       (kLog && pass == 0) ? W.redo[rtab] : nullptr,
-                                       &W.nredo[rtab], psw);
-        if (pass == 1 && lane == 0) W.nredo[rtab ^ 1] = 0;
-        __syncwarp();
+    for (int pass = 0; pass < (kLog ? 2 : 1); ++pass) {
+      int pv = v, pdeg = deg;
+      long long pb = b;
+      bool pm = valid && deg > kSmallMax && deg < S.min_deg;
+      StageWin psw = sw;
+      if (pass == 1) {
+        const int nr = W.nredo[table ^ 1];
+        pm = lane < nr;
+        pv = pm ? W.redo[table ^ 1][lane] : 0;
+        pb = pm ? ld_off(off + pv, pol) : 0;
+        pdeg = pm ? (int)(ld_off(off + pv + 1, pol) - pb) : 0;
+        psw = StageWin{sl.stage, 0, 0};
+        if (__ballot_sync(kFull, pm) == 0u) break;
       }
+      k1_medium<kSnap, kLower, kLog>(cols, csrc, cdst, pv, pb, pdeg, pm, W, pol, L, gathers,
+                                     (kLog && pass == 0) ? W.redo[table] : nullptr,
+                                     &W.nredo[table], psw);
+      if (pass == 1 && lane == 0) W.nredo[table ^ 1] = 0;
+      __syncwarp();
+    }
     long long tc = clock64();
     ct_med += tc - tb;
-    if (kLog)  // rows parked two chunks ago; on exit also the younger tables + carry
-      for (int rep = 0; rep < (finished ? kDT : 1); ++rep) {
-        const int t = (dtab + rep) % kDT;
-        if (rep > 0) dl = k1_drain_load(W, t, cdst);
-        k1_drain(W, t, cdst, L, dl);
-      }
+    if (kLog)  // small rows parked one chunk ago (twice on exit: flushes the carry)
+      for (int rep = 0; rep < (finished ? 2 : 1); ++rep)
+        k1_drain(W, rep == 0 ? table ^ 1 : table, cdst, L);
     tw = clock64();
     ct_drain += tw - tc;
     ++cchunks;
