@@ -608,7 +608,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // rounds ahead of the slowest one.
 // ---------------------------------------------------------------------------
 template <bool kSnap, bool kLower, bool kLog>
-__global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restrict__ off,
+__global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __restrict__ off,
                                                       const int* __restrict__ cols, int n,
                                                       int nitems, const int* worklist,
                                                       const int* csrc, int* cdst, Ctrl* ctrl,
@@ -817,7 +817,9 @@ __global__ void __launch_bounds__(kK1Threads) k1_pipe(const long long* __restric
     long long tb = clock64();
     ct_small += tb - ta;
     // medium rows of this chunk (park mode), then the rows parked one chunk ago
-    for (int pass = 0; pass < (kLog ? 2 : 1); ++pass) {
+    const bool any_med = __any_sync(kFull, valid && deg > kSmallMax && deg < S.min_deg) ||
+                         (kLog && W.nredo[table ^ 1] > 0);
+    for (int pass = 0; any_med && pass < (kLog ? 2 : 1); ++pass) {
       int pv = v, pdeg = deg;
       long long pb = b;
       bool pm = valid && deg > kSmallMax && deg < S.min_deg;
