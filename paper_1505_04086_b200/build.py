@@ -62,3 +62,29 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+
+
+ADAPTER_SRC = os.path.join(REPO, "tests", "cpp", "adapter_check.cpp")
+ADAPTER_BIN = os.path.join(REPO, "tests", "cpp", "adapter_check")
+REF_INCLUDE = os.environ.get("GCOL_REF_INCLUDE", "/root/reference/proj/include")
+
+
+def build_adapter_check() -> str | None:
+    """C++ program using the reference's own headers + include/gcol_cuda.hpp
+    against libgcol_cuda.so (only where the reference headers exist; the
+    binary travels to the GPU box)."""
+    if not os.path.isdir(os.path.join(REF_INCLUDE, "gcol")):
+        return None
+    lib = build()
+    if os.path.exists(ADAPTER_BIN) and os.path.getmtime(ADAPTER_BIN) > max(
+            os.path.getmtime(lib), os.path.getmtime(ADAPTER_SRC),
+            os.path.getmtime(os.path.join(REPO, "include", "gcol_cuda.hpp"))):
+        return ADAPTER_BIN
+    cmd = ["g++", "-std=c++20", "-O2", "-I", REF_INCLUDE, "-I", os.path.join(REPO, "include"),
+           ADAPTER_SRC, "-o", ADAPTER_BIN, "-L", HERE, "-lgcol_cuda",
+           "-Wl,-rpath,$ORIGIN/../../paper_1505_04086_b200"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("building tests/cpp/adapter_check failed")
+    return ADAPTER_BIN

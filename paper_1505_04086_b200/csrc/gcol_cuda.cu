@@ -235,10 +235,13 @@ struct K1Launch {
 
 constexpr size_t kK1Smem = sizeof(K1Smem);
 
-// K1 drift bound in rounds (GCOL_K1_DRIFT overrides for experiments; 0 = off).
-int drift_rounds() {
+// K1 drift bound in rounds: on for skewed-degree graphs, where CTAs run at
+// uneven speeds and the colour count is sensitive to it; off for bounded
+// degree (GCOL_K1_DRIFT overrides for experiments; 0 = off).
+int drift_rounds(const gcol_cuda_graph* g) {
   const char* e = std::getenv("GCOL_K1_DRIFT");
-  return e ? std::atoi(e) : kDriftDefault;
+  if (e) return std::atoi(e);
+  return g->max_degree > 64 ? kDriftDefault : 0;
 }
 
 template <bool kSnap, bool kLower, bool kLog>
@@ -284,7 +287,7 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, cudaGraph
   cudaGraphNode_t n_ev0, n_k1, n_ev1, n_cand, n_while, n_ev2;
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
   {
-    int drift = drift_rounds();
+    int drift = drift_rounds(g);
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), const_cast<int*>(&n),
                     nullptr, &g->d_colors, &g->d_colors, &g->d_ctrl, &K.L, &K.S, &drift};
     const int* wl = nullptr;
@@ -337,7 +340,7 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min) {
   GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
   k1_pipe<false, kLower, true><<<K.grid1, kK1Threads, K.smem, g->stream>>>(
       g->d_off, g->d_cols, n, n, nullptr, g->d_colors, g->d_colors, g->d_ctrl, K.L, K.S,
-      drift_rounds());
+      drift_rounds(g));
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
   k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors,
                                                          g->d_ctrl, K.L, K.grid1, g->d_marks);
