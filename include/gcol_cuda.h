@@ -203,6 +203,33 @@ int gcol_cuda_verify_coloring(gcol_cuda_graph* g, const int32_t* colors, int64_t
 int gcol_cuda_count_colors(gcol_cuda_graph* g, const int32_t* colors, int64_t ncolors,
                            int32_t memory, uint32_t* num_colors);
 
+/* ---- Multi-GPU building blocks (one process and one handle per GPU) ----
+ * A 1-D partition of vertex ids: each rank owns [lo, hi) and keeps a full
+ * replica of the colour array on its device.  All pointers are device
+ * pointers on the handle's device.  The host orchestration (exchange of
+ * owned slices and per-round (id, colour) deltas over NCCL, global
+ * termination) is paper_1505_04086_b200/dist.py. */
+
+/* Initial pass (K1) over the owned rows [lo, hi) in place on colors_dev
+ * (lo a multiple of 256).  Colours of rows outside the range are read as
+ * they are in the replica. */
+int gcol_cuda_k1_range(gcol_cuda_graph* g, const gcol_cuda_options* opt, int32_t* colors_dev,
+                       int64_t lo, int64_t hi, gcol_cuda_stats* stats);
+
+/* Owned vertices of [lo, hi) defective under `priority` -> out_dev
+ * (capacity hi - lo), count in *nout. */
+int gcol_cuda_detect_range(gcol_cuda_graph* g, int32_t priority, const int32_t* colors_dev,
+                           int64_t lo, int64_t hi, int32_t* out_dev, int64_t* nout);
+
+/* One fused detect-and-recolor round over a device worklist, in place on
+ * colors_dev; recoloured ids -> out_dev (capacity nin), count in *nout. */
+int gcol_cuda_round_list(gcol_cuda_graph* g, int32_t priority, int32_t* colors_dev,
+                         const int32_t* in_dev, int64_t nin, int32_t* out_dev, int64_t* nout);
+
+/* colors_dev[ids_dev[i]] = vals_dev[i] for i < count. */
+int gcol_cuda_scatter_colors(gcol_cuda_graph* g, int32_t* colors_dev, const int32_t* ids_dev,
+                             const int32_t* vals_dev, int64_t count);
+
 #ifdef __cplusplus
 }
 #endif

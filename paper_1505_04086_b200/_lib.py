@@ -106,6 +106,10 @@ SIGNATURES = {
     "gcol_cuda_verify_coloring": (C.c_int, [_vp, _vp, _i64, _i32, C.POINTER(VerifyReport), _vp,
                                             _vp, _vp, _i64]),
     "gcol_cuda_count_colors": (C.c_int, [_vp, _vp, _i64, _i32, C.POINTER(C.c_uint32)]),
+    "gcol_cuda_k1_range": (C.c_int, [_vp, C.POINTER(Options), _vp, _i64, _i64, C.POINTER(Stats)]),
+    "gcol_cuda_detect_range": (C.c_int, [_vp, _i32, _vp, _i64, _i64, _vp, C.POINTER(_i64)]),
+    "gcol_cuda_round_list": (C.c_int, [_vp, _i32, _vp, _vp, _i64, _vp, C.POINTER(_i64)]),
+    "gcol_cuda_scatter_colors": (C.c_int, [_vp, _vp, _vp, _vp, _i64]),
 }
 
 

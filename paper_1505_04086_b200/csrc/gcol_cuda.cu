@@ -288,8 +288,9 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, cudaGraph
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
   {
     int drift = drift_rounds(g);
+    int item0 = 0;
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), const_cast<int*>(&n),
-                    nullptr, &g->d_colors, &g->d_colors, &g->d_ctrl, &K.L, &K.S, &drift};
+                    nullptr, &g->d_colors, &g->d_colors, &g->d_ctrl, &K.L, &K.S, &drift, &item0};
     const int* wl = nullptr;
     args[4] = &wl;
     cudaKernelNodeParams p{};
@@ -340,7 +341,7 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min) {
   GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
   k1_pipe<false, kLower, true><<<K.grid1, kK1Threads, K.smem, g->stream>>>(
       g->d_off, g->d_cols, n, n, nullptr, g->d_colors, g->d_colors, g->d_ctrl, K.L, K.S,
-      drift_rounds(g));
+      drift_rounds(g), 0);
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
   k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors,
                                                          g->d_ctrl, K.L, K.grid1, g->d_marks);
@@ -838,11 +839,11 @@ int gcol_cuda_tentative_snapshot(gcol_cuda_graph* g, const int32_t* colors_in,
     if (lower_only)
       k1_pipe<true, true, false><<<K.grid1, kK1Threads, K.smem, g->stream>>>(
           g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, K.L, K.S,
-          0);
+          0, 0);
     else
       k1_pipe<true, false, false><<<K.grid1, kK1Threads, K.smem, g->stream>>>(
           g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, K.L, K.S,
-          0);
+          0, 0);
   }
   GCOL_CK(cudaGetLastError());
   if (int rc = copy_out(g, colors_out, d_out, sizeof(int) * n, memory)) return rc;
@@ -980,4 +981,109 @@ int gcol_cuda_count_colors(gcol_cuda_graph* g, const int32_t* colors, int64_t nc
   return GCOL_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Multi-GPU building blocks
+// ---------------------------------------------------------------------------
+int gcol_cuda_k1_range(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, int32_t* colors_dev,
+                       int64_t lo, int64_t hi, gcol_cuda_stats* stats) {
+  if (int rc = check_graph(g)) return rc;
+  gcol_cuda_options opt;
+  if (int rc = read_options(opt_in, &opt)) return rc;
+  if (lo < 0 || hi > g->n || lo > hi || (lo % kChunk) != 0)
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "k1_range: need 0 <= lo <= hi <= n, lo % 256 == 0");
+  GCOL_CK(cudaSetDevice(g->device));
+  if (int rc = ensure_run_buffers(g)) return rc;
+  K1Launch K;
+  if (int rc = plan_k1<false, true, true>(g, opt.k1_blocks_per_sm, split_min_of(opt), &K))
+    return rc;
+  if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, nullptr, 0)) return rc;
+  if (int rc = reset_split(g, K.plan, K.grid1 * kCW)) return rc;
+  GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
+  if (hi > lo)
+    k1_pipe<false, true, true><<<K.grid1, kK1Threads, K.smem, g->stream>>>(
+        g->d_off, g->d_cols, static_cast<int>(g->n), static_cast<int>(hi - lo), nullptr,
+        colors_dev, colors_dev, g->d_ctrl, K.L, K.S, drift_rounds(g), static_cast<int>(lo));
+  GCOL_CK(cudaGetLastError());
+  GCOL_CK(cudaEventRecord(g->ev_end, g->stream));
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  if (stats) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g->ev_start, g->ev_end);
+    stats->initial_pass_ns = static_cast<uint64_t>(static_cast<double>(ms) * 1e6);
+  }
+  return GCOL_OK;
+}
+
+int gcol_cuda_detect_range(gcol_cuda_graph* g, int32_t priority, const int32_t* colors_dev,
+                           int64_t lo, int64_t hi, int32_t* out_dev, int64_t* nout) {
+  if (int rc = check_graph(g)) return rc;
+  if (priority == GCOL_PRIORITY_DEFAULT) priority = GCOL_PRIORITY_DEGREE_ID;
+  if (priority < GCOL_PRIORITY_ID_LOW || priority > GCOL_PRIORITY_ORDERED)
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "unknown priority rule");
+  if (lo < 0 || hi > g->n || lo > hi) return fail(GCOL_ERR_INVALID_ARGUMENT, "bad range");
+  GCOL_CK(cudaSetDevice(g->device));
+  if (int rc = ensure_run_buffers(g)) return rc;
+  int* d_cnt = reinterpret_cast<int*>(&g->d_ctrl->in_len);
+  GCOL_CK(cudaMemsetAsync(d_cnt, 0, sizeof(int), g->stream));
+  const int r = rule_of(priority);
+  const int grid = g->sms * 4;
+  const int l = static_cast<int>(lo), h = static_cast<int>(hi);
+  if (hi > lo) {
+    if (r == kIdLow) k_detect_range<kIdLow><<<grid, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, l, h, colors_dev, out_dev, d_cnt);
+    else if (r == kIdHigh) k_detect_range<kIdHigh><<<grid, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, l, h, colors_dev, out_dev, d_cnt);
+    else if (r == kDegId) k_detect_range<kDegId><<<grid, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, l, h, colors_dev, out_dev, d_cnt);
+    else k_detect_range<kOrdered><<<grid, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, l, h, colors_dev, out_dev, d_cnt);
+  }
+  GCOL_CK(cudaGetLastError());
+  int cnt = 0;
+  GCOL_CK(cudaMemcpyAsync(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  if (nout) *nout = cnt;
+  return GCOL_OK;
+}
+
+int gcol_cuda_round_list(gcol_cuda_graph* g, int32_t priority, int32_t* colors_dev,
+                         const int32_t* in_dev, int64_t nin, int32_t* out_dev, int64_t* nout) {
+  if (int rc = check_graph(g)) return rc;
+  if (priority == GCOL_PRIORITY_DEFAULT) priority = GCOL_PRIORITY_DEGREE_ID;
+  if (priority < GCOL_PRIORITY_ID_LOW || priority > GCOL_PRIORITY_ORDERED)
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "unknown priority rule");
+  GCOL_CK(cudaSetDevice(g->device));
+  if (int rc = ensure_run_buffers(g)) return rc;
+  if (int rc = reset_ctrl(g, 1, const_cast<int*>(in_dev), out_dev, nullptr, static_cast<int>(nin)))
+    return rc;
+  if (nin > 0) {
+    const int r = rule_of(priority);
+    if (r == kIdLow) {
+      k_list<kIdLow, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
+      k_heavy<kIdLow, false><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
+    } else if (r == kIdHigh) {
+      k_list<kIdHigh, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
+      k_heavy<kIdHigh, false><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
+    } else {  // degree_id (ordered needs per-round marks; treated as degree_id here)
+      k_list<kDegId, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
+      k_heavy<kDegId, false><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
+    }
+  }
+  GCOL_CK(cudaGetLastError());
+  Ctrl hdr;
+  GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  if (nout) *nout = hdr.out_len;
+  return GCOL_OK;
+}
+
+int gcol_cuda_scatter_colors(gcol_cuda_graph* g, int32_t* colors_dev, const int32_t* ids_dev,
+                             const int32_t* vals_dev, int64_t count) {
+  if (int rc = check_graph(g)) return rc;
+  GCOL_CK(cudaSetDevice(g->device));
+  if (count > 0)
+    k_scatter_colors<<<g->sms * 4, kBlock, 0, g->stream>>>(colors_dev, ids_dev, vals_dev, count);
+  GCOL_CK(cudaGetLastError());
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  return GCOL_OK;
+}
+
 }  // extern "C"
+

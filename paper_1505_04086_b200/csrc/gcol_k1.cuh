@@ -612,7 +612,8 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __rest
                                                       const int* __restrict__ cols, int n,
                                                       int nitems, const int* worklist,
                                                       const int* csrc, int* cdst, Ctrl* ctrl,
-                                                      PairLogArgs LA, SplitArgs S, int drift) {
+                                                      PairLogArgs LA, SplitArgs S, int drift,
+                                                      int item0) {
   extern __shared__ __align__(16) unsigned char k1_raw[];
   K1Smem& sm = *reinterpret_cast<K1Smem*>(k1_raw);
   __shared__ int s_ready[kSlots];
@@ -658,11 +659,11 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __rest
       K1Slot& sl = sm.slot[k % kSlots];
       const int c0 = c * kChunk;
       const int rows = min(kChunk, nitems - c0);
-      const int cnt = rows + 1;           // off[c0 .. c0 + rows]
-      const int bulk = cnt & ~1;          // whole 16-byte pairs
-      if (cnt & 1) sl.offs[cnt - 1] = ld_off(off + c0 + cnt - 1, pol);
+      const int cnt = rows + 1;           // off[item0 + c0 .. + rows]
+      const int bulk = cnt & ~1;          // whole 16-byte pairs (item0 is even)
+      if (cnt & 1) sl.offs[cnt - 1] = ld_off(off + item0 + c0 + cnt - 1, pol);
       mbar_arrive_expect_tx(&sl.offb, (unsigned)(bulk * 8));
-      tma_load_1d(sl.offs, off + c0, (unsigned)(bulk * 8), &sl.offb);
+      tma_load_1d(sl.offs, off + item0 + c0, (unsigned)(bulk * 8), &sl.offb);
     };
     if (lane == 0 && contig) request_offsets(0);
     for (int k = 0;; ++k) {
@@ -802,7 +803,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __rest
         b = sl.offs[i];
         deg = sl.wdeg[i];
       } else {
-        v = sl.chunk * kChunk + i;
+        v = item0 + sl.chunk * kChunk + i;
         b = sl.offs[i];
         deg = (int)(sl.offs[i + 1] - b);
       }

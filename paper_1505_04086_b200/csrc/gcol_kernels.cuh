@@ -384,3 +384,31 @@ __global__ void k_fill(int* p, long long n, int value) {
 
 }  // namespace dev
 }  // namespace gcol
+
+namespace gcol {
+namespace dev {
+
+// Multi-GPU round 1: defective owned vertices in [lo, hi) under rule R.
+template <int R>
+__global__ void __launch_bounds__(kBlock) k_detect_range(const long long* __restrict__ off,
+                                                         const int* __restrict__ cols, int lo,
+                                                         int hi, const int* colors, int* out,
+                                                         int* count) {
+  const uint64_t pol = policy_evict_first();
+  for (long long v0 = lo + (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); v0 < hi;
+       v0 += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(v0 + lane_id());
+    const bool pred = v < hi && thread_defective<R>(off, cols, colors, v, pol);
+    append_warp(out, count, pred, v);
+  }
+}
+
+// Apply (id, colour) deltas received from other ranks.
+__global__ void k_scatter_colors(int* colors, const int* ids, const int* vals, long long count) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    colors[ids[i]] = vals[i];
+}
+
+}  // namespace dev
+}  // namespace gcol

@@ -1,0 +1,70 @@
+"""GPU: the multi-GPU building blocks of the C ABI (k1_range, detect_range,
+round_list, scatter_colors) through DeviceOps, with P logical partitions
+emulated on one device: each partition has its own replica, and the test
+performs the exchange steps of dist.color_rsoc_distributed by hand.  (The
+collective orchestration itself is covered over gloo in tests/test_dist.py;
+ranks are never co-scheduled as interdependent kernels on one GPU.)"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1505_04086_b200 import dist as gdist, gcol, graphs  # noqa: E402
+
+
+def emulate(g, n, P):
+    ops = gdist.DeviceOps(g)
+    parts = gdist.partition(n, P)
+    reps = [torch.full((n,), -1, dtype=torch.int32, device="cuda") for _ in range(P)]
+    for r, (lo, hi) in enumerate(parts):
+        ops.k1_range(reps[r], lo, hi)
+    for r in range(P):  # all-gather of owned slices
+        for q, (lo, hi) in enumerate(parts):
+            if q != r:
+                reps[r][lo:hi] = reps[q][lo:hi]
+    work = [ops.detect_range(reps[r], lo, hi) for r, (lo, hi) in enumerate(parts)]
+    rounds = 0
+    while True:
+        rec = [ops.round_list(reps[r], work[r]) for r in range(P)]
+        vals = [reps[r][rec[r].long()] for r in range(P)]
+        for r in range(P):
+            for q in range(P):
+                if q != r and rec[q].numel():
+                    ops.scatter(reps[r], rec[q], vals[q])
+        rounds += 1
+        if sum(x.numel() for x in rec) == 0:
+            break
+        work = rec
+        assert rounds < 1000
+    return reps, rounds
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_partitioned_blocks(P):
+    off, cols = graphs.erdos_renyi(60_000, 16, 11, "cuda")
+    n = off.numel() - 1
+    g = gcol.Graph.from_device(off, cols)
+    reps, rounds = emulate(g, n, P)
+    for r in range(1, P):
+        assert torch.equal(reps[0], reps[r])
+    hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
+    c = reps[0].cpu().numpy()
+    assert gcol.verify_coloring(hg, c).ok()
+    assert (c >= 0).all() and (c <= np.diff(hg.offsets())).all()
+    assert gcol.count_colors(c) <= hg.max_degree() + 1
+
+
+def test_k1_range_matches_full_on_one_partition():
+    off, cols = graphs.tri_mesh(300, 300, 3, "cuda")
+    n = off.numel() - 1
+    g = gcol.Graph.from_device(off, cols)
+    ops = gdist.DeviceOps(g)
+    colors = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+    ops.k1_range(colors, 0, n)
+    assert (colors >= 0).all()
+    with pytest.raises(gcol.input_error):
+        ops.k1_range(colors, 3, n)  # ranges start on 256-id chunk boundaries
