@@ -51,6 +51,7 @@ struct CudaOptions {
   int k1_blocks_per_sm = 0;
   bool k1_read_all = false;
   int k1_split_min_degree = 0;
+  int k1_wide = 0;
 };
 
 // A gcol::Graph uploaded once to the device (reuse it across runs, like the
@@ -89,6 +90,7 @@ inline gcol_cuda_options to_c(unsigned thread_count, const ParallelOptions& opt,
   o.k1_blocks_per_sm = co.k1_blocks_per_sm;
   o.k1_read_all = co.k1_read_all ? 1 : 0;
   o.k1_split_min_degree = co.k1_split_min_degree;
+  o.k1_wide = co.k1_wide;
   return o;
 }
 

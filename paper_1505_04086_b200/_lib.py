@@ -46,7 +46,8 @@ class Options(C.Structure):
         ("k1_blocks_per_sm", C.c_int32),
         ("k1_read_all", C.c_int32),
         ("k1_split_min_degree", C.c_int32),
-        ("reserved", C.c_int32 * 4),
+        ("k1_wide", C.c_int32),
+        ("reserved", C.c_int32 * 3),
     ]
 
 

@@ -60,10 +60,10 @@ cudaError_t add_kernel(cudaGraphNode_t* node, cudaGraph_t g, const cudaGraphNode
 }
 
 struct ExecKey {
-  int rule, lower, k1_blocks, mega_min;
+  int rule, lower, k1_blocks, mega_min, wide;
   bool operator<(const ExecKey& o) const {
-    return std::tie(rule, lower, k1_blocks, mega_min) <
-           std::tie(o.rule, o.lower, o.k1_blocks, o.mega_min);
+    return std::tie(rule, lower, k1_blocks, mega_min, wide) <
+           std::tie(o.rule, o.lower, o.k1_blocks, o.mega_min, o.wide);
   }
 };
 
@@ -227,13 +227,12 @@ int reset_split(gcol_cuda_graph* g, const SplitPlan* P, int warps) {
 // Everything one K1 launch needs (grid, log slices, long-row queue).
 struct K1Launch {
   int grid1 = 0;
+  int cw = kCW;       // consumer warps per CTA (8 narrow, 16 wide)
   size_t smem = 0;
   PairLogArgs L{};
   SplitArgs S{};
   const SplitPlan* plan = nullptr;
 };
-
-constexpr size_t kK1Smem = sizeof(K1Smem);
 
 // K1 drift bound in rounds: on for skewed-degree graphs, where CTAs run at
 // uneven speeds and the colour count is sensitive to it; off for bounded
@@ -244,21 +243,32 @@ int drift_rounds(const gcol_cuda_graph* g) {
   return g->max_degree > 64 ? kDriftDefault : 0;
 }
 
-template <bool kSnap, bool kLower, bool kLog>
-int plan_k1(gcol_cuda_graph* g, int k1_blocks, int split_min, K1Launch* K) {
-  auto k1 = k1_pipe<kSnap, kLower, kLog>;
+// Wide K1 (16 consumer warps per CTA, twice the vertices in flight) where
+// the palette is bounded by a small maximum degree and the colour count
+// cannot drift (option k1_wide: 0 auto, 1 narrow, 2 wide).
+bool use_wide(const gcol_cuda_graph* g, int k1_wide) {
+  if (k1_wide == 1) return false;
+  if (k1_wide == 2) return true;
+  return g->max_degree <= 16;
+}
+
+template <bool kSnap, bool kLower, bool kLog, int CW>
+int plan_k1_cw(gcol_cuda_graph* g, int k1_blocks, int split_min, long long nitems, K1Launch* K) {
+  auto k1 = k1_pipe<kSnap, kLower, kLog, CW>;
+  const size_t smem = sizeof(K1Smem<CW>);
   GCOL_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k1),
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(kK1Smem)));
+                               static_cast<int>(smem)));
   int occ = 1;
-  GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1, kK1Threads, kK1Smem));
+  GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1, (CW + 1) * 32, smem));
   if (occ < 1) occ = 1;
   const int bps = k1_blocks > 0 ? std::min(k1_blocks, occ) : 1;
-  // small graphs: fewer CTAs, so the ~256 x CTAs vertices in flight stay a
-  // small share of the graph (colour quality)
-  const long long want = std::max(1LL, g->n / (kChunk * 24LL));
+  // small graphs: fewer CTAs, so the ~(32 CW) x CTAs vertices in flight stay
+  // a small share of the graph (colour quality)
+  const long long want = std::max(1LL, nitems / (CW * 32 * 24LL));
   K->grid1 = static_cast<int>(std::min<long long>(g->sms * bps, want));
-  K->smem = kK1Smem;
+  K->cw = CW;
+  K->smem = smem;
   SplitPlan* P = nullptr;
   if (int rc = get_split(g, split_min, &P)) return rc;
   K->plan = P;
@@ -271,16 +281,37 @@ int plan_k1(gcol_cuda_graph* g, int k1_blocks, int split_min, K1Launch* K) {
   return GCOL_OK;
 }
 
+template <bool kSnap, bool kLower, bool kLog>
+int plan_k1(gcol_cuda_graph* g, int k1_blocks, int split_min, K1Launch* K, bool wide = false,
+            long long nitems = -1) {
+  if (nitems < 0) nitems = g->n;
+  return wide ? plan_k1_cw<kSnap, kLower, kLog, kCWWide>(g, k1_blocks, split_min, nitems, K)
+              : plan_k1_cw<kSnap, kLower, kLog, kCW>(g, k1_blocks, split_min, nitems, K);
+}
+
+// Launch of the planned K1 variant on `stream`.
+template <bool kSnap, bool kLower, bool kLog>
+void launch_k1(const K1Launch& K, cudaStream_t stream, const long long* off, const int* cols,
+               int n, int nitems, const int* wl, const int* csrc, int* cdst, Ctrl* ctrl,
+               int drift, int item0) {
+  if (K.cw == kCWWide)
+    k1_pipe<kSnap, kLower, kLog, kCWWide><<<K.grid1, (kCWWide + 1) * 32, K.smem, stream>>>(
+        off, cols, n, nitems, wl, csrc, cdst, ctrl, K.L, K.S, drift, item0);
+  else
+    k1_pipe<kSnap, kLower, kLog, kCW><<<K.grid1, (kCW + 1) * 32, K.smem, stream>>>(
+        off, cols, n, nitems, wl, csrc, cdst, ctrl, K.L, K.S, drift, item0);
+}
+
 int split_min_of(const gcol_cuda_options& opt) {
   const int v = opt.k1_split_min_degree;
   return v > 0 ? std::max(v, kSmallMax + 1) : kSplitDefault;
 }
 
 template <int R, bool kLower>
-int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, cudaGraph_t* out_graph,
-                     cudaGraphExec_t* out_exec) {
+int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, bool wide,
+                     cudaGraph_t* out_graph, cudaGraphExec_t* out_exec) {
   K1Launch K;
-  if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K)) return rc;
+  if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K, wide)) return rc;
   cudaGraph_t graph;
   GCOL_CK(cudaGraphCreate(&graph, 0));
   const int n = static_cast<int>(g->n);
@@ -294,9 +325,10 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, cudaGraph
     const int* wl = nullptr;
     args[4] = &wl;
     cudaKernelNodeParams p{};
-    p.func = reinterpret_cast<void*>(k1_pipe<false, kLower, true>);
+    p.func = K.cw == kCWWide ? reinterpret_cast<void*>(k1_pipe<false, kLower, true, kCWWide>)
+                             : reinterpret_cast<void*>(k1_pipe<false, kLower, true, kCW>);
     p.gridDim = dim3(K.grid1);
-    p.blockDim = dim3(kK1Threads);
+    p.blockDim = dim3((K.cw + 1) * 32);
     p.sharedMemBytes = static_cast<unsigned>(K.smem);
     p.kernelParams = args;
     GCOL_CK(cudaGraphAddKernelNode(&n_k1, graph, &n_ev0, 1, &p));
@@ -324,7 +356,7 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, cudaGraph
   GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle, 1));
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, graph, &n_while, 1, g->ev_end));
   GCOL_CK(cudaGraphInstantiate(out_exec, graph, 0));
-  g->k1_warps[*out_exec] = K.grid1 * kCW;
+  g->k1_warps[*out_exec] = K.grid1 * K.cw;
   *out_graph = graph;
   return GCOL_OK;
 }
@@ -333,15 +365,14 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, cudaGraph
 // loop driven from the host.  Only for profilers that cannot see into
 // conditional graph nodes (GCOL_EAGER=1); the product path is the graph.
 template <int R, bool kLower>
-int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min) {
+int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, bool wide) {
   K1Launch K;
-  if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K)) return rc;
-  if (int rc = reset_split(g, K.plan, K.grid1 * kCW)) return rc;
+  if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K, wide)) return rc;
+  if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
   const int n = static_cast<int>(g->n);
   GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
-  k1_pipe<false, kLower, true><<<K.grid1, kK1Threads, K.smem, g->stream>>>(
-      g->d_off, g->d_cols, n, n, nullptr, g->d_colors, g->d_colors, g->d_ctrl, K.L, K.S,
-      drift_rounds(g), 0);
+  launch_k1<false, kLower, true>(K, g->stream, g->d_off, g->d_cols, n, n, nullptr, g->d_colors,
+                                 g->d_colors, g->d_ctrl, drift_rounds(g), 0);
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
   k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors,
                                                          g->d_ctrl, K.L, K.grid1, g->d_marks);
@@ -362,16 +393,16 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min) {
   return GCOL_OK;
 }
 
-int launch_eager(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, int mm) {
-  if (rule == kIdLow) return lower ? run_eager<kIdLow, true>(g, k1_blocks, mm) : run_eager<kIdLow, false>(g, k1_blocks, mm);
-  if (rule == kIdHigh) return lower ? run_eager<kIdHigh, true>(g, k1_blocks, mm) : run_eager<kIdHigh, false>(g, k1_blocks, mm);
-  if (rule == kDegId) return lower ? run_eager<kDegId, true>(g, k1_blocks, mm) : run_eager<kDegId, false>(g, k1_blocks, mm);
-  return lower ? run_eager<kOrdered, true>(g, k1_blocks, mm) : run_eager<kOrdered, false>(g, k1_blocks, mm);
+int launch_eager(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, int mm, bool w) {
+  if (rule == kIdLow) return lower ? run_eager<kIdLow, true>(g, k1_blocks, mm, w) : run_eager<kIdLow, false>(g, k1_blocks, mm, w);
+  if (rule == kIdHigh) return lower ? run_eager<kIdHigh, true>(g, k1_blocks, mm, w) : run_eager<kIdHigh, false>(g, k1_blocks, mm, w);
+  if (rule == kDegId) return lower ? run_eager<kDegId, true>(g, k1_blocks, mm, w) : run_eager<kDegId, false>(g, k1_blocks, mm, w);
+  return lower ? run_eager<kOrdered, true>(g, k1_blocks, mm, w) : run_eager<kOrdered, false>(g, k1_blocks, mm, w);
 }
 
-int get_exec(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, int mm,
+int get_exec(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, int mm, bool w,
              cudaGraphExec_t* exec) {
-  ExecKey key{rule, lower, k1_blocks, mm};
+  ExecKey key{rule, lower, k1_blocks, mm, w ? 1 : 0};
   auto it = g->execs.find(key);
   if (it != g->execs.end()) {
     *exec = it->second.second;
@@ -381,17 +412,17 @@ int get_exec(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, int mm,
   cudaGraphExec_t ex = nullptr;
   int rc;
   if (rule == kIdLow)
-    rc = lower ? build_rsoc_graph<kIdLow, true>(g, k1_blocks, mm, &graph, &ex)
-               : build_rsoc_graph<kIdLow, false>(g, k1_blocks, mm, &graph, &ex);
+    rc = lower ? build_rsoc_graph<kIdLow, true>(g, k1_blocks, mm, w, &graph, &ex)
+               : build_rsoc_graph<kIdLow, false>(g, k1_blocks, mm, w, &graph, &ex);
   else if (rule == kIdHigh)
-    rc = lower ? build_rsoc_graph<kIdHigh, true>(g, k1_blocks, mm, &graph, &ex)
-               : build_rsoc_graph<kIdHigh, false>(g, k1_blocks, mm, &graph, &ex);
+    rc = lower ? build_rsoc_graph<kIdHigh, true>(g, k1_blocks, mm, w, &graph, &ex)
+               : build_rsoc_graph<kIdHigh, false>(g, k1_blocks, mm, w, &graph, &ex);
   else if (rule == kDegId)
-    rc = lower ? build_rsoc_graph<kDegId, true>(g, k1_blocks, mm, &graph, &ex)
-               : build_rsoc_graph<kDegId, false>(g, k1_blocks, mm, &graph, &ex);
+    rc = lower ? build_rsoc_graph<kDegId, true>(g, k1_blocks, mm, w, &graph, &ex)
+               : build_rsoc_graph<kDegId, false>(g, k1_blocks, mm, w, &graph, &ex);
   else
-    rc = lower ? build_rsoc_graph<kOrdered, true>(g, k1_blocks, mm, &graph, &ex)
-               : build_rsoc_graph<kOrdered, false>(g, k1_blocks, mm, &graph, &ex);
+    rc = lower ? build_rsoc_graph<kOrdered, true>(g, k1_blocks, mm, w, &graph, &ex)
+               : build_rsoc_graph<kOrdered, false>(g, k1_blocks, mm, w, &graph, &ex);
   if (rc != GCOL_OK) return rc;
   g->execs[key] = {graph, ex};
   *exec = ex;
@@ -675,8 +706,9 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   const char* eager_env = std::getenv("GCOL_EAGER");
   const bool eager = eager_env && eager_env[0] == '1';
   const int mm = split_min_of(opt);
+  const bool wide = use_wide(g, opt.k1_wide);
   if (!eager)
-    if (int rc = get_exec(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, &exec))
+    if (int rc = get_exec(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide, &exec))
       return rc;
   // Untimed prologue, like Coloring(n) before the reference's timer
   // (parallel.hpp:258 vs :267): colours := -1, marks := 0, control reset.
@@ -686,7 +718,8 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   if (int rc = reset_ctrl(g, static_cast<int>(opt.round_cap), g->d_listA, g->d_listB, nullptr, 0))
     return rc;
   if (eager) {
-    if (int rc = launch_eager(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm)) return rc;
+    if (int rc = launch_eager(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide))
+      return rc;
   } else {
     auto sp = g->splits.find(mm);
     if (sp != g->splits.end())
@@ -834,16 +867,14 @@ int gcol_cuda_tentative_snapshot(gcol_cuda_graph* g, const int32_t* colors_in,
     int rc = lower_only ? plan_k1<true, true, false>(g, 0, kSplitDefault, &K)
                         : plan_k1<true, false, false>(g, 0, kSplitDefault, &K);
     if (rc) return rc;
-    if (int r2 = reset_split(g, K.plan, K.grid1 * kCW)) return r2;
+    if (int r2 = reset_split(g, K.plan, K.grid1 * K.cw)) return r2;
     K.L = PairLogArgs{};
     if (lower_only)
-      k1_pipe<true, true, false><<<K.grid1, kK1Threads, K.smem, g->stream>>>(
-          g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, K.L, K.S,
-          0, 0);
+      launch_k1<true, true, false>(K, g->stream, g->d_off, g->d_cols, static_cast<int>(n), nitems,
+                                   d_wl, d_in, d_out, g->d_ctrl, 0, 0);
     else
-      k1_pipe<true, false, false><<<K.grid1, kK1Threads, K.smem, g->stream>>>(
-          g->d_off, g->d_cols, static_cast<int>(n), nitems, d_wl, d_in, d_out, g->d_ctrl, K.L, K.S,
-          0, 0);
+      launch_k1<true, false, false>(K, g->stream, g->d_off, g->d_cols, static_cast<int>(n),
+                                    nitems, d_wl, d_in, d_out, g->d_ctrl, 0, 0);
   }
   GCOL_CK(cudaGetLastError());
   if (int rc = copy_out(g, colors_out, d_out, sizeof(int) * n, memory)) return rc;
@@ -995,15 +1026,16 @@ int gcol_cuda_k1_range(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, int3
   GCOL_CK(cudaSetDevice(g->device));
   if (int rc = ensure_run_buffers(g)) return rc;
   K1Launch K;
-  if (int rc = plan_k1<false, true, true>(g, opt.k1_blocks_per_sm, split_min_of(opt), &K))
+  if (int rc = plan_k1<false, true, true>(g, opt.k1_blocks_per_sm, split_min_of(opt), &K,
+                                          use_wide(g, opt.k1_wide), hi - lo))
     return rc;
   if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, nullptr, 0)) return rc;
-  if (int rc = reset_split(g, K.plan, K.grid1 * kCW)) return rc;
+  if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
   GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
   if (hi > lo)
-    k1_pipe<false, true, true><<<K.grid1, kK1Threads, K.smem, g->stream>>>(
-        g->d_off, g->d_cols, static_cast<int>(g->n), static_cast<int>(hi - lo), nullptr,
-        colors_dev, colors_dev, g->d_ctrl, K.L, K.S, drift_rounds(g), static_cast<int>(lo));
+    launch_k1<false, true, true>(K, g->stream, g->d_off, g->d_cols, static_cast<int>(g->n),
+                                 static_cast<int>(hi - lo), nullptr, colors_dev, colors_dev,
+                                 g->d_ctrl, drift_rounds(g), static_cast<int>(lo));
   GCOL_CK(cudaGetLastError());
   GCOL_CK(cudaEventRecord(g->ev_end, g->stream));
   GCOL_CK(cudaStreamSynchronize(g->stream));

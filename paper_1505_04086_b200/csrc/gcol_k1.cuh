@@ -27,10 +27,11 @@
 namespace gcol {
 namespace dev {
 
-constexpr int kCW = 8;                    // consumer warps per CTA
+constexpr int kCW = 8;                    // consumer warps per CTA (narrow variant)
+constexpr int kCWWide = 16;               // consumer warps per CTA (wide variant)
 constexpr int kPW = 1;                    // producer warp (TMA bulk copies)
 constexpr int kK1Threads = (kCW + kPW) * 32;
-constexpr int kChunk = kCW * 32;          // vertices per chunk (one sub-tile per consumer)
+constexpr int kChunk = kCW * 32;          // vertices per chunk (narrow); ranges align to it
 constexpr int kSlots = 4;                 // staged chunks in flight per CTA (multiple of kPW)
 constexpr int kSlotStage = 6144;          // adjacency entries staged per chunk (24 KB)
 constexpr int kBmWords = 512;             // per-warp medium-row bitmap pool
@@ -58,10 +59,11 @@ struct K1Warp {
 };
 
 // One staged chunk: its rows and (a window of) their adjacency.
+template <int CW>
 struct alignas(16) K1Slot {
-  alignas(16) long long offs[kChunk + 2];          // contiguous mode: off[c0 .. c0 + rows]; worklist: b[]
-  int wv[kChunk];                      // worklist mode: vertex ids
-  int wdeg[kChunk];                    // worklist mode: degrees
+  alignas(16) long long offs[CW * 32 + 2];  // contiguous mode: off[c0 .. c0 + rows]; worklist: b[]
+  int wv[CW * 32];                     // worklist mode: vertex ids
+  int wdeg[CW * 32];                   // worklist mode: degrees
   alignas(16) int stage[kSlotStage];   // cols[base .. base + len)
   long long base;
   int len;
@@ -71,9 +73,10 @@ struct alignas(16) K1Slot {
   unsigned long long offb;             // mbarrier: offsets staged (producer only)
 };
 
+template <int CW>
 struct alignas(16) K1Smem {
-  K1Slot slot[kSlots];
-  K1Warp cw[kCW];
+  K1Slot<CW> slot[kSlots];
+  K1Warp cw[CW];
 };
 
 // Adjacency window in shared memory: rows lying inside read it, the rest
@@ -607,15 +610,17 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // reads and hence the colour count.  A CTA may not run more than `drift`
 // rounds ahead of the slowest one.
 // ---------------------------------------------------------------------------
-template <bool kSnap, bool kLower, bool kLog>
-__global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __restrict__ off,
+template <bool kSnap, bool kLower, bool kLog, int CW>
+__global__ void __launch_bounds__((CW + 1) * 32, 1) k1_pipe(const long long* __restrict__ off,
                                                       const int* __restrict__ cols, int n,
                                                       int nitems, const int* worklist,
                                                       const int* csrc, int* cdst, Ctrl* ctrl,
                                                       PairLogArgs LA, SplitArgs S, int drift,
                                                       int item0) {
   extern __shared__ __align__(16) unsigned char k1_raw[];
-  K1Smem& sm = *reinterpret_cast<K1Smem*>(k1_raw);
+  constexpr int kCW = CW;
+  constexpr int kChunk = CW * 32;
+  K1Smem<CW>& sm = *reinterpret_cast<K1Smem<CW>*>(k1_raw);
   __shared__ int s_ready[kSlots];
   __shared__ int s_consumed[kSlots];
   __shared__ int s_npairs, s_mbhead;
@@ -656,7 +661,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __rest
     auto request_offsets = [&](int k) {  // lane 0 only, contiguous mode
       const int c = blockIdx.x + k * G;
       if (c >= nchunks) return;
-      K1Slot& sl = sm.slot[k % kSlots];
+      K1Slot<CW>& sl = sm.slot[k % kSlots];
       const int c0 = c * kChunk;
       const int rows = min(kChunk, nitems - c0);
       const int cnt = rows + 1;           // off[item0 + c0 .. + rows]
@@ -669,7 +674,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __rest
     for (int k = 0;; ++k) {
       const int c = blockIdx.x + k * G;
       const int si = k % kSlots;
-      K1Slot& sl = sm.slot[si];
+      K1Slot<CW>& sl = sm.slot[si];
       const unsigned par = (unsigned)((k / kSlots) & 1);
       long long t0 = clock64();
       if (c >= nchunks) {
@@ -792,7 +797,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __rest
     }
     long long ta = clock64();
     ct_wait += ta - tw;
-    const K1Slot& sl = sm.slot[si];
+    const K1Slot<CW>& sl = sm.slot[si];
     const int i = warp * 32 + lane;
     const bool valid = !finished && i < sl.rows;
     int v = -1, deg = 0;
@@ -871,7 +876,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_pipe(const long long* __rest
   const unsigned g = __reduce_add_sync(kFull, gathers);
   if (lane == 0 && g) atomicAdd(&s_gathers, g);
   // the producer warps have returned: count only consumer warps from here on
-  asm volatile("bar.sync 1, %0;" ::"n"(kCW * 32));
+  asm volatile("bar.sync 1, %0;" ::"n"(CW * 32));
   if (threadIdx.x == 0) {
     if (s_gathers) atomicAdd(&ctrl->k1_gathers, (unsigned long long)s_gathers);
     if (kLog) {

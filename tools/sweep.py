@@ -52,7 +52,8 @@ def main():
         print(json.dumps(rec), flush=True)
         for rule, bps, mega in [(r, b, mg) for r in args.rules for b in args.bps for mg in args.mega]:
                 opt = gcol.ParallelOptions(priority=gcol.Priority[rule], k1_blocks_per_sm=bps,
-                                           k1_read_all=args.read_all, k1_split_min_degree=mega)
+                                           k1_read_all=args.read_all, k1_split_min_degree=mega,
+                                           k1_wide=bps)
                 out = torch.empty(n, dtype=torch.int32, device="cuda")
                 gcol.color_rsoc(g, 1, opt, colors_out=out)  # warm
                 res = []
