@@ -95,7 +95,7 @@ typedef struct {
   int32_t k1_split_min_degree; /* rows at least this long are split into 1024-entry
                                   pieces that every warp helps colour; 0 = default
                                   (1024) */
-  int32_t k1_wide;           /* 0 auto (wide when max degree <= 16), 1 narrow (8 consumer
+  int32_t k1_wide;           /* 0 auto (wide when max degree <= 32), 1 narrow (8 consumer
                                 warps per SM), 2 wide (16: twice the vertices in flight) */
   int32_t reserved[3];
 } gcol_cuda_options;

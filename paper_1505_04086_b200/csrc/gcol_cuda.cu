@@ -8,6 +8,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdint>
 #include <cstdio>
 #include <climits>
 #include <cstdlib>
@@ -245,11 +246,11 @@ int drift_rounds(const gcol_cuda_graph* g) {
 
 // Wide K1 (16 consumer warps per CTA, twice the vertices in flight) where
 // the palette is bounded by a small maximum degree and the colour count
-// cannot drift (option k1_wide: 0 auto, 1 narrow, 2 wide).
+// cannot drift (option k1_wide: 0 auto = max degree <= 32, 1 narrow, 2 wide).
 bool use_wide(const gcol_cuda_graph* g, int k1_wide) {
   if (k1_wide == 1) return false;
   if (k1_wide == 2) return true;
-  return g->max_degree <= 16;
+  return g->max_degree <= 32;
 }
 
 template <bool kSnap, bool kLower, bool kLog, int CW>
@@ -631,7 +632,11 @@ int gcol_cuda_graph_create(const int64_t* offsets, const int32_t* cols, int64_t 
     gcol_cuda_graph_destroy(g);
     return code;
   };
-  if (memory == GCOL_MEM_DEVICE) {
+  // K1 stages the CSR with TMA bulk copies, which need 16-byte aligned
+  // bases: a caller's device arrays that are not aligned are copied once.
+  const bool aligned = (reinterpret_cast<uintptr_t>(offsets) & 15u) == 0 &&
+                       (reinterpret_cast<uintptr_t>(cols) & 15u) == 0;
+  if (memory == GCOL_MEM_DEVICE && aligned) {
     g->d_off = const_cast<long long*>(reinterpret_cast<const long long*>(offsets));
     g->d_cols = const_cast<int*>(cols);
     g->owns_csr = false;
@@ -737,10 +742,12 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
     std::fprintf(stderr,
                  "[k1 profile] consumer cycles/chunk: wait %.0f piece %.0f small %.0f medium %.0f "
                  "drain %.0f (chunks %llu) | producer cycles/chunk: slot %.0f drift %.0f load %.0f "
-                 "(chunks %llu)\n",
+                 "(chunks %llu) | medium: redo cycles/chunk %.0f rows %llu redone %llu\n",
                  hdr.prof[0] / ch, hdr.prof[1] / ch, hdr.prof[2] / ch, hdr.prof[3] / ch,
                  hdr.prof[4] / ch, static_cast<unsigned long long>(hdr.prof[5]), hdr.prof[8] / pc,
-                 hdr.prof[9] / pc, hdr.prof[10] / pc, static_cast<unsigned long long>(hdr.prof[11]));
+                 hdr.prof[9] / pc, hdr.prof[10] / pc, static_cast<unsigned long long>(hdr.prof[11]),
+                 hdr.prof[6] / ch, static_cast<unsigned long long>(hdr.prof[7]),
+                 static_cast<unsigned long long>(hdr.prof[12]));
   }
   std::vector<unsigned long long> cpr(std::min(rounds, kMaxRoundsRecorded));
   if (!cpr.empty())

@@ -58,15 +58,24 @@ struct K1Warp {
   int nredo[2];
 };
 
-// One staged chunk: its rows and (a window of) their adjacency.
+// Staged adjacency entries per slot: 32 KB (narrow) / 24 KB (wide, whose
+// per-warp scratch takes the rest of the 227 KB).
+template <int CW>
+constexpr int stage_cap() {
+  return CW <= kCW ? 8192 : kSlotStage;
+}
+
+// One staged chunk: its rows and their adjacency, packed.  The adjacency of
+// the chunk's rows is contiguous in `cols` except where a long row (served
+// by pieces from global memory) sits in between, so the producer stages the
+// runs between long rows back to back (each run 16-byte aligned for TMA)
+// and records per row where its entries landed.
 template <int CW>
 struct alignas(16) K1Slot {
   alignas(16) long long offs[CW * 32 + 2];  // contiguous mode: off[c0 .. c0 + rows]; worklist: b[]
   int wv[CW * 32];                     // worklist mode: vertex ids
-  int wdeg[CW * 32];                   // worklist mode: degrees
-  alignas(16) int stage[kSlotStage];   // cols[base .. base + len)
-  long long base;
-  int len;
+  int aux[CW * 32];                    // worklist: degrees; contiguous: stage offset (-1: global)
+  alignas(16) int stage[stage_cap<CW>()];
   int chunk;                           // chunk index, -1: no more chunks
   int rows;
   unsigned long long full;             // mbarrier: slot staged (TMA tx + producer arrive)
@@ -77,17 +86,6 @@ template <int CW>
 struct alignas(16) K1Smem {
   K1Slot<CW> slot[kSlots];
   K1Warp cw[CW];
-};
-
-// Adjacency window in shared memory: rows lying inside read it, the rest
-// read global memory.
-struct StageWin {
-  const int* stage;
-  long long base;
-  int len;
-  __device__ __forceinline__ bool has(long long b, int deg) const {
-    return b >= base && b + deg <= base + len;
-  }
 };
 
 // Long-row pieces.  Piece p (global allocation order) is delivered to the
@@ -155,10 +153,10 @@ template <bool kSnap, bool kLower, bool kLog>
 __device__ __forceinline__ void k1_small(const int* __restrict__ cols, const int* csrc,
                                          int* cdst, int v, long long b, int deg, bool small,
                                          K1Warp& W, int table, uint64_t pol, const PairLog& L,
-                                         unsigned& gathers, const StageWin& sw) {
+                                         unsigned& gathers, const int* rs) {
+  // rs: the row's entries in shared memory, nullptr when not staged
   const int lane = lane_id();
-  const bool inwin = sw.has(b, deg);
-  const int* rs = sw.stage + (b - sw.base);  // valid when inwin
+  const bool inwin = rs != nullptr;
   const int maxk = __reduce_max_sync(kFull, (unsigned)(small ? deg : 0));
   bool active = small;
   int ns = 0;
@@ -281,10 +279,10 @@ __device__ __forceinline__ void k1_medium(const int* __restrict__ cols, const in
                                           int* cdst, int v, long long b, int deg, bool med,
                                           K1Warp& W, uint64_t pol, const PairLog& L,
                                           unsigned& gathers, int* redo, int* nredo,
-                                          const StageWin& sw) {
+                                          const int* stage, int so) {
+  // so: offset of the row's entries in `stage`, -1 when not staged
   const int lane = lane_id();
   const bool park_mode = kLog && redo != nullptr;
-  const bool inwin = sw.has(b, deg);
   unsigned medmask = __ballot_sync(kFull, med);
   while (medmask) {
     // rows of this batch: medium rows in lane order while their words fit
@@ -326,11 +324,10 @@ __device__ __forceinline__ void k1_medium(const int* __restrict__ cols, const in
         r[u] = lo;
         const long long br = __shfl_sync(kFull, b, lo);
         const int er = __shfl_sync(kFull, eoff, lo);
-        const bool iw = __shfl_sync(kFull, inwin, lo);
+        const int sr = __shfl_sync(kFull, so, lo);
         vr[u] = __shfl_sync(kFull, v, lo);
         dr[u] = __shfl_sync(kFull, deg, lo);
-        w[u] = !in ? 0 : (iw ? sw.stage[br - sw.base + (idx - er)]
-                             : ld_col(cols + br + (idx - er), pol));
+        w[u] = !in ? 0 : (sr >= 0 ? stage[sr + (idx - er)] : ld_col(cols + br + (idx - er), pol));
         take[u] = in && (!kLower || w[u] < vr[u]);
       }
       int c[4];
@@ -572,6 +569,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
   }
 }
 
+// Raise the barrier's expected transaction bytes without arriving.
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // 1-D TMA bulk copy global -> shared, completion counted on `bar`.
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
                                             unsigned long long* bar) {
@@ -580,6 +588,123 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
           "r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Request the offsets of chunk c (contiguous mode, one thread) into `sl`.
+template <int CW>
+__device__ __forceinline__ void k1_request_offsets(K1Slot<CW>& sl, const long long* off, int c,
+                                                   int nitems, int item0, int n, uint64_t pol) {
+  constexpr int kChunk = CW * 32;
+  const int c0 = c * kChunk;
+  if (c0 >= nitems) return;
+  const int rows = min(kChunk, nitems - c0);
+  const int cnt = rows + 1;           // off[item0 + c0 .. + rows]
+  // whole 16-byte pairs (item0 is even); an odd count reads one offset more
+  // unless that would pass off[n], where the last one is loaded here
+  const bool pad = (cnt & 1) && item0 + c0 + cnt + 1 <= n + 1;
+  const int bulk = pad ? cnt + 1 : (cnt & ~1);
+  if (bulk < cnt) sl.offs[cnt - 1] = ld_off(off + item0 + c0 + cnt - 1, pol);
+  mbar_arrive_expect_tx(&sl.offb, (unsigned)(bulk * 8));
+  tma_load_1d(sl.offs, off + item0 + c0, (unsigned)(bulk * 8), &sl.offb);
+}
+
+// Stage the adjacency of one contiguous chunk (producer warp, all lanes;
+// sl.offs must hold off[c0 .. c0 + rows]).  Run j (lane j) is the span of
+// rows between the (j-1)-th and j-th long row; runs are packed back to back
+// from stage[0], each starting at a 16-byte aligned source so one TMA bulk
+// copy moves it (+ <= 3 scalar tail entries), as far as the capacity goes.
+// Every row gets aux[i] = its first entry's stage offset, or -1.  Each
+// copying lane registers its bytes on `full` (expect_tx) before issuing, so
+// the copies overlap the aux[] computation; the caller's single arrive
+// (after a __syncwarp) then publishes aux[] and the tails.
+template <int CW>
+__device__ __forceinline__ void stage_chunk(K1Slot<CW>& sl, int rows, int min_deg,
+                                            const int* __restrict__ cols, long long m,
+                                            uint64_t pol) {
+  constexpr int R = CW;                  // rows per lane (kChunk / 32)
+  constexpr int CAP = stage_cap<CW>();
+  const int lane = lane_id();
+  unsigned lm[R];                        // long-row bitmap of the chunk, word t = rows t*32..
+  int nl = 0;
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    const int i = t * 32 + lane;
+    const bool lg = min_deg != INT_MAX && i < rows && sl.offs[i + 1] - sl.offs[i] >= min_deg;
+    lm[t] = __ballot_sync(kFull, lg);
+    nl += __popc(lm[t]);
+  }
+  // run j = rows [s_j, e_j): after the (j-1)-th long row, up to the j-th
+  // (the last run, j == min(nl, 31), extends to `rows`)
+  const int nr = min(nl, 31) + 1;
+  auto nth_long = [&](int q) {           // row index of the q-th long row
+    int r = rows;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const int p = __popc(lm[t]);
+      if (r == rows && q < p) r = t * 32 + (int)__fns(lm[t], 0, q + 1);
+      q -= p;
+    }
+    return r;
+  };
+  int s = 0, e = 0;
+  if (lane < nr) {
+    s = lane == 0 ? 0 : nth_long(lane - 1) + 1;
+    e = lane == nr - 1 ? rows : nth_long(lane);
+  }
+  long long A = 0, span = 0;
+  int sz = 0;
+  if (lane < nr && s < e) {
+    const long long bs = sl.offs[s], be = sl.offs[e];
+    A = bs & ~3LL;
+    span = be - A;
+    sz = (int)min((span + 3) & ~3LL, (long long)CAP + 4);
+  }
+  int incl = sz;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += y;            // <= 32 * (CAP + 4): no overflow
+  }
+  const int dst = incl - sz;
+  const int room = max(0, min(CAP - dst, sz));     // multiple of 4
+  const int avail = (int)min((long long)room, span);
+  // the copy rounds up to whole 16-byte units (entries past the run are
+  // harmless) except at the very end of `cols`, where <= 3 are loaded here
+  const int bulk = A + room <= m ? room : (avail & ~3);
+  if (bulk) {
+    mbar_expect_tx(&sl.full, (unsigned)bulk * 4u);
+    tma_load_1d(sl.stage + dst, cols + A, (unsigned)bulk * 4u, &sl.full);
+  }
+  for (int j = bulk; j < avail; ++j) sl.stage[dst + j] = ld_col(cols + A + j, pol);
+  // per-row stage offsets
+  if (nl == 0) {                         // one run: the common case
+    const long long A0 = __shfl_sync(kFull, A, 0);
+    const int r0 = __shfl_sync(kFull, avail, 0);
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const int i = t * 32 + lane;
+      if (i < rows) {
+        const long long b = sl.offs[i], bend = sl.offs[i + 1];
+        sl.aux[i] = bend - A0 <= r0 ? (int)(b - A0) : -1;
+      }
+    }
+    return;
+  }
+  int before = 0;                        // long rows before word t
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    const int i = t * 32 + lane;
+    const int run = min(before + __popc(lm[t] & ((1u << lane) - 1u)), 31);
+    const long long Ar = __shfl_sync(kFull, A, run);
+    const int dr = __shfl_sync(kFull, dst, run);
+    const int rr = __shfl_sync(kFull, avail, run);
+    if (i < rows) {
+      const long long b = sl.offs[i], bend = sl.offs[i + 1];
+      const bool staged = !((lm[t] >> lane) & 1u) && bend - Ar <= rr;
+      sl.aux[i] = staged ? dr + (int)(b - Ar) : -1;
+    }
+    before += __popc(lm[t]);
+  }
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -658,19 +783,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) k1_pipe(const long long* __r
     // the adjacency of chunk k is published, so both stay in flight.
     long long pt_slot = 0, pt_drift = 0, pt_load = 0, pchunks = 0;
     const bool contig = worklist == nullptr;
-    auto request_offsets = [&](int k) {  // lane 0 only, contiguous mode
-      const int c = blockIdx.x + k * G;
-      if (c >= nchunks) return;
-      K1Slot<CW>& sl = sm.slot[k % kSlots];
-      const int c0 = c * kChunk;
-      const int rows = min(kChunk, nitems - c0);
-      const int cnt = rows + 1;           // off[item0 + c0 .. + rows]
-      const int bulk = cnt & ~1;          // whole 16-byte pairs (item0 is even)
-      if (cnt & 1) sl.offs[cnt - 1] = ld_off(off + item0 + c0 + cnt - 1, pol);
-      mbar_arrive_expect_tx(&sl.offb, (unsigned)(bulk * 8));
-      tma_load_1d(sl.offs, off + item0 + c0, (unsigned)(bulk * 8), &sl.offb);
-    };
-    if (lane == 0 && contig) request_offsets(0);
+    const long long m = ld_off(off + n, pol);  // adjacency length
+    // the first kSlots chunks' offsets; later ones are requested by the
+    // consumer warp that frees the slot
+    if (lane == 0 && contig)
+      for (int j = 0; j < kSlots; ++j)
+        k1_request_offsets<CW>(sm.slot[j], off, blockIdx.x + j * G, nitems, item0, n, pol);
     for (int k = 0;; ++k) {
       const int c = blockIdx.x + k * G;
       const int si = k % kSlots;
@@ -694,27 +812,15 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) k1_pipe(const long long* __r
       const int c0 = c * kChunk;
       const int rows = min(kChunk, nitems - c0);
       if (contig) {
+        mbar_wait(&sl.offb, par);              // offsets of chunk k (every lane; the
+                                               // slot was freed before they were requested)
+        stage_chunk<CW>(sl, rows, S.min_deg, cols, m, pol);
         if (lane == 0) {
-          mbar_wait(&sl.offb, par);            // offsets of chunk k
-          // next chunk's offsets go out now (its slot must be free)
-          const int kn = k + 1;
-          if (kn >= kSlots)
-            while (*reinterpret_cast<volatile int*>(&s_consumed[kn % kSlots]) <
-                   kCW * (kn / kSlots))
-              __nanosleep(64);
-          request_offsets(kn);
-          const long long blo = sl.offs[0], bhi = sl.offs[rows];
-          const long long A = blo & ~3LL;
-          const int len = (int)min(bhi - A, (long long)kSlotStage);
-          const int bulk = len & ~3;
-          for (int j = bulk; j < len; ++j) sl.stage[j] = ld_col(cols + A + j, pol);
-          sl.base = A;
-          sl.len = len;
           sl.rows = rows;
           sl.chunk = c;
-          mbar_arrive_expect_tx(&sl.full, (unsigned)(bulk * 4));
-          if (bulk) tma_load_1d(sl.stage, cols + A, (unsigned)(bulk * 4), &sl.full);
         }
+        __syncwarp();  // every lane's expect_tx, tails and aux[] before the arrive
+        if (lane == 0) mbar_arrive(&sl.full);
       } else {  // worklist mode: per-row loads, nothing staged
         if (k >= kSlots)
           while (*reinterpret_cast<volatile int*>(&s_consumed[si]) < kCW * (k / kSlots))
@@ -725,12 +831,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) k1_pipe(const long long* __r
           const long long bb = valid ? ld_off(off + v, pol) : 0;
           sl.wv[i] = v;
           sl.offs[i] = bb;
-          sl.wdeg[i] = valid ? (int)(ld_off(off + v + 1, pol) - bb) : 0;
+          sl.aux[i] = valid ? (int)(ld_off(off + v + 1, pol) - bb) : 0;
         }
         __syncwarp();
         if (lane == 0) {
-          sl.base = 0;
-          sl.len = 0;
           sl.rows = rows;
           sl.chunk = c;
           mbar_arrive_expect_tx(&sl.full, 0u);
@@ -756,6 +860,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) k1_pipe(const long long* __r
   bool finished = false;  // no more chunks for this warp
   bool retired = false;   // decremented S.alive
   long long ct_wait = 0, ct_piece = 0, ct_small = 0, ct_med = 0, ct_drain = 0, cchunks = 0;
+  long long ct_redo = 0, n_med = 0, n_redo = 0;
   long long tw = clock64();
   for (int k = 0;;) {
     // long-row pieces first (one call site)
@@ -806,44 +911,49 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) k1_pipe(const long long* __r
       if (worklist) {
         v = sl.wv[i];
         b = sl.offs[i];
-        deg = sl.wdeg[i];
+        deg = sl.aux[i];
       } else {
         v = item0 + sl.chunk * kChunk + i;
         b = sl.offs[i];
         deg = (int)(sl.offs[i + 1] - b);
       }
     }
-    const StageWin sw{sl.stage, finished ? 0 : sl.base, finished ? 0 : sl.len};
+    const int so = (valid && !worklist) ? sl.aux[i] : -1;  // stage offset of the row
     const int table = k & 1;
     if (valid && deg == 0) st_color(cdst + v, 0);  // limit 0: only colour 0
     k1_push_long(S, v, deg, valid && deg >= S.min_deg);
     k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg,
                                   valid && deg >= 1 && deg <= kSmallMax, W, table, pol, L,
-                                  gathers, sw);
+                                  gathers, so >= 0 ? sl.stage + so : nullptr);
     long long tb = clock64();
     ct_small += tb - ta;
     // medium rows of this chunk (park mode), then the rows parked one chunk ago
     const bool any_med = __any_sync(kFull, valid && deg > kSmallMax && deg < S.min_deg) ||
                          (kLog && W.nredo[table ^ 1] > 0);
     for (int pass = 0; any_med && pass < (kLog ? 2 : 1); ++pass) {
+      const long long tpass = clock64();
       int pv = v, pdeg = deg;
       long long pb = b;
       bool pm = valid && deg > kSmallMax && deg < S.min_deg;
-      StageWin psw = sw;
+      int pso = so;
       if (pass == 1) {
         const int nr = W.nredo[table ^ 1];
         pm = lane < nr;
         pv = pm ? W.redo[table ^ 1][lane] : 0;
         pb = pm ? ld_off(off + pv, pol) : 0;
         pdeg = pm ? (int)(ld_off(off + pv + 1, pol) - pb) : 0;
-        psw = StageWin{sl.stage, 0, 0};
+        pso = -1;
         if (__ballot_sync(kFull, pm) == 0u) break;
+        n_redo += nr;
+      } else {
+        n_med += __popc(__ballot_sync(kFull, pm));
       }
       k1_medium<kSnap, kLower, kLog>(cols, csrc, cdst, pv, pb, pdeg, pm, W, pol, L, gathers,
                                      (kLog && pass == 0) ? W.redo[table] : nullptr,
-                                     &W.nredo[table], psw);
+                                     &W.nredo[table], sl.stage, pso);
       if (pass == 1 && lane == 0) W.nredo[table ^ 1] = 0;
       __syncwarp();
+      if (pass == 1) ct_redo += clock64() - tpass;
     }
     long long tc = clock64();
     ct_med += tc - tb;
@@ -857,7 +967,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) k1_pipe(const long long* __r
       __syncwarp();
       if (lane == 0) {
         const int old = atomicAdd(&s_consumed[si], 1);
-        if (old % kCW == kCW - 1 && S.done_chunks) atomicAdd(S.done_chunks, 1u);
+        if (old % kCW == kCW - 1) {  // last warp out: the slot is free
+          if (S.done_chunks) atomicAdd(S.done_chunks, 1u);
+          if (!worklist)
+            k1_request_offsets<CW>(sm.slot[si], off, blockIdx.x + (k + kSlots) * G, nitems,
+                                   item0, n, pol);
+        }
       }
       ++k;
     } else {
@@ -872,6 +987,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) k1_pipe(const long long* __r
     atomicAdd(&ctrl->prof[3], (unsigned long long)ct_med);
     atomicAdd(&ctrl->prof[4], (unsigned long long)ct_drain);
     atomicAdd(&ctrl->prof[5], (unsigned long long)cchunks);
+    atomicAdd(&ctrl->prof[6], (unsigned long long)ct_redo);
+    atomicAdd(&ctrl->prof[7], (unsigned long long)n_med);
+    atomicAdd(&ctrl->prof[12], (unsigned long long)n_redo);
   }
   const unsigned g = __reduce_add_sync(kFull, gathers);
   if (lane == 0 && g) atomicAdd(&s_gathers, g);

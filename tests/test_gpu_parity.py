@@ -244,13 +244,16 @@ def test_rsoc_configs_scaled(oracle_mod, name):
     band of the oracle's multi-threaded RSOC on the same graph."""
     off, cols = graphs.make_config(name, "cuda", scale_down=2 if name != "rmat24" else 6)
     g = gcol.Graph.from_device(off, cols)
-    run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_blocks_per_sm=1))
     hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
-    check_run(hg, run, 1)
+    ours = []
+    for _ in range(3):  # colour counts of both sides vary run to run: compare medians
+        run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_blocks_per_sm=1))
+        check_run(hg, run, 1)
+        ours.append(run.stats.num_colors)
     o = oracle_mod.CSR(hg.offsets(), hg.adjacency())
     counts = sorted(oracle_mod.color_parallel(o, 8, "rsoc")[1]["num_colors"] for _ in range(3))
     ref = counts[1]
-    assert run.stats.num_colors <= int(1.05 * ref) + 2, (run.stats.num_colors, ref)
+    assert sorted(ours)[1] <= int(1.05 * ref) + 2, (ours, ref)
 
 
 def test_k1_read_all_variant_and_residency_knob():

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--ref-runs", type=int, default=3)
     ap.add_argument("--read-all", action="store_true")
     ap.add_argument("--mega", nargs="+", type=int, default=[0])
+    ap.add_argument("--scale-down", type=int, default=0)
     args = ap.parse_args()
     import torch
     from paper_1505_04086_b200 import gcol, graphs
@@ -31,7 +32,7 @@ def main():
     threads = os.cpu_count()
     for cfg in args.configs:
         t0 = time.time()
-        off, cols = graphs.make_config(cfg, "cuda")
+        off, cols = graphs.make_config(cfg, "cuda", scale_down=args.scale_down)
         torch.cuda.synchronize()
         gen_s = time.time() - t0
         g = gcol.Graph.from_device(off, cols)
