@@ -95,7 +95,7 @@ typedef struct {
   int32_t k1_split_min_degree; /* rows at least this long are split into 1024-entry
                                   pieces that every warp helps colour; 0 = default
                                   (1024) */
-  int32_t k1_wide;           /* 0 auto (wide when max degree <= 32), 1 narrow (8 consumer
+  int32_t k1_wide;           /* 0 auto (wide when max degree <= 16), 1 narrow (8 consumer
                                 warps per SM), 2 wide (16: twice the vertices in flight) */
   int32_t reserved[3];
 } gcol_cuda_options;
@@ -158,6 +158,17 @@ int gcol_cuda_graph_info(const gcol_cuda_graph* g, int64_t* n, int64_t* m, int32
  * GCOL_ERR_VERIFY. */
 int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt, int32_t* colors_out,
                          int32_t colors_memory, gcol_cuda_stats* stats);
+
+/* color_rsoc on a HOST CSR in one call (gcol::color_rsoc(g, T, opt) with a
+ * host gcol::Graph, parallel.hpp:253): graph_create + color_rsoc +
+ * graph_destroy, except that the adjacency is uploaded in pieces on a second
+ * stream while the initial pass colours the rows already resident, so the
+ * PCIe transfer and the coloring overlap.  Same checks and errors as
+ * graph_create and color_rsoc; stats->wall_time_ns runs from the start of
+ * the initial pass and so includes its waits for the upload. */
+int gcol_cuda_color_rsoc_csr(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t m,
+                             int32_t device, const gcol_cuda_options* opt, int32_t* colors_out,
+                             gcol_cuda_stats* stats);
 
 /* run_coloring (bench.hpp:35-60) dispatch: GCOL_ALG_SEQ -> the exact
  * sequential First-Fit on the device, GCOL_ALG_RSOC -> color_rsoc,

@@ -94,6 +94,20 @@ inline gcol_cuda_options to_c(unsigned thread_count, const ParallelOptions& opt,
   return o;
 }
 
+inline void fill_stats(ColoringRun& run, const gcol_cuda_stats& st,
+                       const std::vector<uint64_t>& cpr) {
+  run.stats.algorithm = static_cast<Algorithm>(st.algorithm);
+  run.stats.thread_count = st.thread_count;
+  run.stats.rounds = st.rounds;
+  run.stats.conflicts_total = st.conflicts_total;
+  run.stats.conflicts_per_round.assign(cpr.begin(),
+                                       cpr.begin() + static_cast<std::ptrdiff_t>(st.cpr_len));
+  run.stats.barrier_events = st.barrier_events;
+  run.stats.num_colors = st.num_colors;
+  run.stats.wall_time_ns = st.wall_time_ns;
+  run.stats.fallback_triggered = st.fallback_triggered != 0;
+}
+
 inline ColoringRun run_coloring(const DeviceGraph& dg, std::size_t n, Algorithm algorithm,
                                 unsigned thread_count, const ParallelOptions& opt = {},
                                 const CudaOptions& co = {}) {
@@ -106,29 +120,43 @@ inline ColoringRun run_coloring(const DeviceGraph& dg, std::size_t n, Algorithm 
   const gcol_cuda_options o = to_c(thread_count, opt, co);
   throw_status(gcol_cuda_run_coloring(dg.get(), static_cast<int32_t>(algorithm), &o,
                                       run.coloring.colors.data(), GCOL_MEM_HOST, &st));
-  run.stats.algorithm = static_cast<Algorithm>(st.algorithm);
-  run.stats.thread_count = st.thread_count;
-  run.stats.rounds = st.rounds;
-  run.stats.conflicts_total = st.conflicts_total;
-  run.stats.conflicts_per_round.assign(cpr.begin(),
-                                       cpr.begin() + static_cast<std::ptrdiff_t>(st.cpr_len));
-  run.stats.barrier_events = st.barrier_events;
-  run.stats.num_colors = st.num_colors;
-  run.stats.wall_time_ns = st.wall_time_ns;
-  run.stats.fallback_triggered = st.fallback_triggered != 0;
+  fill_stats(run, st, cpr);
+  return run;
+}
+
+// RSOC on a host gcol::Graph in one call: the upload of the adjacency
+// overlaps the initial pass (gcol_cuda_color_rsoc_csr).
+inline ColoringRun color_rsoc_host(const gcol::Graph& g, unsigned thread_count,
+                                   const ParallelOptions& opt = {}, const CudaOptions& co = {}) {
+  if (thread_count < 1) throw gcol::input_error("thread_count must be at least 1");
+  if (g.num_vertices() >= 0x7fffffffu)
+    throw gcol::capacity_error("vertex ids do not fit the int32 column type");
+  ColoringRun run{Coloring(g.num_vertices()), {}};
+  std::vector<uint64_t> cpr(static_cast<std::size_t>(opt.round_cap) + 1);
+  gcol_cuda_stats st{};
+  st.conflicts_per_round = cpr.data();
+  st.cpr_cap = cpr.size();
+  const gcol_cuda_options o = to_c(thread_count, opt, co);
+  throw_status(gcol_cuda_color_rsoc_csr(
+      reinterpret_cast<const int64_t*>(g.offsets().data()),
+      reinterpret_cast<const int32_t*>(g.adjacency().data()),
+      static_cast<int64_t>(g.num_vertices()), static_cast<int64_t>(g.adjacency().size()), -1, &o,
+      run.coloring.colors.data(), &st));
+  fill_stats(run, st, cpr);
   return run;
 }
 
 inline ColoringRun run_coloring(const gcol::Graph& g, Algorithm algorithm,
                                 unsigned thread_count, const ParallelOptions& opt = {},
                                 const CudaOptions& co = {}) {
+  if (algorithm == Algorithm::rsoc) return color_rsoc_host(g, thread_count, opt, co);
   DeviceGraph dg(g);
   return run_coloring(dg, g.num_vertices(), algorithm, thread_count, opt, co);
 }
 
 inline ColoringRun color_rsoc(const gcol::Graph& g, unsigned thread_count,
                               const ParallelOptions& opt = {}, const CudaOptions& co = {}) {
-  return run_coloring(g, Algorithm::rsoc, thread_count, opt, co);
+  return color_rsoc_host(g, thread_count, opt, co);
 }
 
 inline Coloring first_fit_sequential(const gcol::Graph& g) {

@@ -21,7 +21,7 @@ SOURCES = ["gcol_cuda.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-Xcompiler", "-pthread",
     "--expt-relaxed-constexpr",
     "-Xptxas", "-v",
     "-cudart", "static",

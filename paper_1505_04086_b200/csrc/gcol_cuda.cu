@@ -4,10 +4,13 @@
 //
 // No CPU fallback exists anywhere in this file: every algorithmic step runs
 // on the device, and a missing device is an error (GCOL_ERR_NO_DEVICE).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <climits>
@@ -15,6 +18,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -90,6 +94,7 @@ struct gcol_cuda_graph {
   cudaStream_t stream = nullptr;
   int64_t n = 0, m = 0;
   int max_degree = 0;
+  GraphStats gs{};
   long long* d_off = nullptr;
   int* d_cols = nullptr;
   bool owns_csr = false;
@@ -108,6 +113,25 @@ struct gcol_cuda_graph {
   std::map<ExecKey, std::pair<cudaGraph_t, cudaGraphExec_t>> execs;
   std::map<int, SplitPlan> splits;
   std::map<cudaGraphExec_t, int> k1_warps;  // K1 warps of each instantiated graph
+  // streamed upload (gcol_cuda_color_rsoc_csr): the adjacency arrives in
+  // pieces on copy_stream while K1 runs; d_progress = entries resident
+  cudaStream_t copy_stream = nullptr;
+  unsigned long long* d_progress = nullptr;
+  cudaEvent_t ev_copied = nullptr;
+  cudaEvent_t ev_copy0 = nullptr;  // GCOL_TRACE: start of the upload
+  // heavy rows of the rounds, split into pieces (Ctrl::hq ...)
+  int hslots = 0, hq_cap = 0;
+  int2* d_hq = nullptr;
+  int* d_hslot = nullptr;          // [4][hslots]: v, i, left, flag
+  unsigned* d_hslot_bm = nullptr;  // [hslots][kBWinWords]
+  // verification of rows with deg >= kHPiece, in pieces (k_verify_big)
+  bool vplan_done = false;
+  int nvrows = 0;
+  int* d_vrows = nullptr;
+  int* d_vpre = nullptr;  // [nvrows + 1] piece prefix
+  // colour copy-out to pinned host memory, overlapped with verification
+  cudaStream_t out_stream = nullptr;
+  cudaEvent_t ev_final = nullptr;
 };
 
 namespace {
@@ -131,6 +155,23 @@ cudaError_t dalloc(T** p, size_t count, cudaStream_t s) {
   return cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T), s);
 }
 
+__global__ void k_count_long(const long long* __restrict__ off, int n, int min_deg,
+                             int piece, unsigned long long* out) {
+  unsigned long long rows = 0, pieces = 0;
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x) {
+    const long long d = off[v + 1] - off[v];
+    if (d >= min_deg) {
+      rows++;
+      pieces += (unsigned long long)((d + piece - 1) / piece);
+    }
+  }
+  if (rows) {
+    atomicAdd(out, rows);
+    atomicAdd(out + 1, pieces);
+  }
+}
+
 int ensure_run_buffers(gcol_cuda_graph* g) {
   if (g->d_colors) return GCOL_OK;
   const size_t n = static_cast<size_t>(g->n);
@@ -149,24 +190,59 @@ int ensure_run_buffers(gcol_cuda_graph* g) {
   GCOL_CK(cudaEventCreate(&g->ev_start));
   GCOL_CK(cudaEventCreate(&g->ev_k1));
   GCOL_CK(cudaEventCreate(&g->ev_end));
+  GCOL_CK(cudaStreamCreateWithFlags(&g->out_stream, cudaStreamNonBlocking));
+  GCOL_CK(cudaEventCreateWithFlags(&g->ev_final, cudaEventDisableTiming));
+  if (g->gs.rows[1] > 0) {  // rows the rounds split into pieces
+    g->hslots = static_cast<int>(std::min<unsigned long long>(g->gs.rows[1], 65536));
+    g->hq_cap = static_cast<int>(g->gs.pieces[1]);
+    GCOL_CK(dalloc(&g->d_hq, static_cast<size_t>(g->hq_cap), g->stream));
+    GCOL_CK(dalloc(&g->d_hslot, static_cast<size_t>(g->hslots) * 4, g->stream));
+    GCOL_CK(dalloc(&g->d_hslot_bm, static_cast<size_t>(g->hslots) * kBWinWords, g->stream));
+    GCOL_CK(cudaMemsetAsync(g->d_hslot, 0, sizeof(int) * 4 * static_cast<size_t>(g->hslots),
+                            g->stream));
+    GCOL_CK(cudaMemsetAsync(g->d_hslot_bm, 0,
+                            sizeof(unsigned) * kBWinWords * static_cast<size_t>(g->hslots),
+                            g->stream));
+  }
   return GCOL_OK;
 }
 
-__global__ void k_count_long(const long long* __restrict__ off, int n, int min_deg,
-                             int piece, unsigned long long* out) {
-  unsigned long long rows = 0, pieces = 0;
-  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (long long)gridDim.x * blockDim.x) {
-    const long long d = off[v + 1] - off[v];
-    if (d >= min_deg) {
-      rows++;
-      pieces += (unsigned long long)((d + piece - 1) / piece);
-    }
+// Host memory the DMA engines can read/write directly (page-locked): a
+// copy into it is asynchronous and can overlap other device work.
+// GCOL_TRACE=1: host timestamps of the phases of a call, printed at its end
+// (tooling for the end-to-end breakdown; off by default).
+struct Trace {
+  bool on = false;
+  std::vector<std::pair<const char*, std::chrono::steady_clock::time_point>> pts;
+  Trace() {
+    const char* e = std::getenv("GCOL_TRACE");
+    on = e && e[0] == '1';
   }
-  if (rows) {
-    atomicAdd(out, rows);
-    atomicAdd(out + 1, pieces);
+  void mark(const char* tag) {
+    if (on) pts.emplace_back(tag, std::chrono::steady_clock::now());
   }
+  void print(const char* what) const {
+    if (!on || pts.empty()) return;
+    std::fprintf(stderr, "[gcol trace] %s:", what);
+    for (size_t i = 1; i < pts.size(); ++i)
+      std::fprintf(stderr, " %s %.3f", pts[i].first,
+                   std::chrono::duration<double, std::milli>(pts[i].second - pts[i - 1].second)
+                       .count());
+    std::fprintf(stderr, " ms\n");
+  }
+};
+Trace* g_trace = nullptr;  // set for the duration of a traced call
+void tmark(const char* tag) {
+  if (g_trace) g_trace->mark(tag);
+}
+
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
 }
 
 int get_split(gcol_cuda_graph* g, int min_deg, SplitPlan** out) {
@@ -177,7 +253,18 @@ int get_split(gcol_cuda_graph* g, int min_deg, SplitPlan** out) {
   }
   SplitPlan P;
   P.min_deg = min_deg;
-  if (g->max_degree >= min_deg && g->n > 0) {
+  if (min_deg == kSplitDefault && g->n > 0) {  // counted with the graph
+    P.nslots = static_cast<int>(g->gs.rows[0]);
+    P.npieces = static_cast<int>(g->gs.pieces[0]);
+    if (P.nslots > 0) {
+      GCOL_CK(dalloc(&P.d_slot_v, P.nslots, g->stream));
+      GCOL_CK(dalloc(&P.d_slot_deg, P.nslots, g->stream));
+      GCOL_CK(dalloc(&P.d_slot_left, P.nslots, g->stream));
+      GCOL_CK(dalloc(&P.d_slot_bm, static_cast<size_t>(P.nslots) * 32, g->stream));
+      GCOL_CK(dalloc(&P.d_q, P.npieces, g->stream));
+      GCOL_CK(dalloc(&P.d_q_seq, P.npieces, g->stream));
+    }
+  } else if (g->max_degree >= min_deg && g->n > 0) {
     unsigned long long* d_cnt = nullptr;
     GCOL_CK(dalloc(&d_cnt, 2, g->stream));
     GCOL_CK(cudaMemsetAsync(d_cnt, 0, 16, g->stream));
@@ -246,11 +333,11 @@ int drift_rounds(const gcol_cuda_graph* g) {
 
 // Wide K1 (16 consumer warps per CTA, twice the vertices in flight) where
 // the palette is bounded by a small maximum degree and the colour count
-// cannot drift (option k1_wide: 0 auto = max degree <= 32, 1 narrow, 2 wide).
+// cannot drift (option k1_wide: 0 auto = max degree <= 16, 1 narrow, 2 wide).
 bool use_wide(const gcol_cuda_graph* g, int k1_wide) {
   if (k1_wide == 1) return false;
   if (k1_wide == 2) return true;
-  return g->max_degree <= 32;
+  return g->max_degree <= 16;
 }
 
 template <bool kSnap, bool kLower, bool kLog, int CW>
@@ -275,7 +362,8 @@ int plan_k1_cw(gcol_cuda_graph* g, int k1_blocks, int split_min, long long nitem
   K->plan = P;
   K->S = SplitArgs{P->nslots > 0 ? split_min : INT_MAX, P->d_slot_v, P->d_slot_deg,
                    P->d_slot_left, P->d_slot_bm, P->d_q, P->d_q_seq, P->d_ctr, P->d_ctr + 1,
-                   reinterpret_cast<int*>(P->d_ctr + 2), K->grid1, P->d_ctr + 3};
+                   reinterpret_cast<int*>(P->d_ctr + 2), K->grid1, P->d_ctr + 3,
+                   g->d_progress};
   const unsigned long long per = g->pair_cap / static_cast<unsigned long long>(K->grid1);
   K->L = PairLogArgs{g->d_pairs, static_cast<int>(std::min<unsigned long long>(per, 1u << 30)),
                      g->d_pair_counts, &g->d_ctrl->pair_overflow};
@@ -443,6 +531,16 @@ int reset_ctrl(gcol_cuda_graph* g, int round_cap, int* in_list, int* out_list, i
   c->flags = flags;
   c->in_len = in_len;
   c->round_cap = round_cap;
+  c->hslots = g->hslots;
+  c->hq_cap = g->hq_cap;
+  c->hq = g->d_hq;
+  if (g->hslots > 0) {
+    c->hslot_v = g->d_hslot;
+    c->hslot_i = g->d_hslot + g->hslots;
+    c->hslot_left = g->d_hslot + 2 * g->hslots;
+    c->hslot_flag = g->d_hslot + 3 * g->hslots;
+  }
+  c->hslot_bm = g->d_hslot_bm;
   GCOL_CK(cudaMemcpyAsync(g->d_ctrl, buf.data(), hdr, cudaMemcpyHostToDevice, g->stream));
   return GCOL_OK;
 }
@@ -466,9 +564,41 @@ int copy_out(gcol_cuda_graph* g, void* dst, const void* src, size_t bytes, int m
 }
 
 // Device verification + census of a device colour buffer.
+// Rows verified piecewise: built once per graph.
+int ensure_verify_plan(gcol_cuda_graph* g) {
+  if (g->vplan_done) return GCOL_OK;
+  g->vplan_done = true;
+  const int rows = static_cast<int>(g->gs.rows[2]);
+  if (rows == 0 || g->n == 0) return GCOL_OK;
+  int* d_pieces = nullptr;
+  int* d_len = nullptr;
+  GCOL_CK(dalloc(&d_len, 1, g->stream));
+  GCOL_CK(dalloc(&g->d_vrows, static_cast<size_t>(rows), g->stream));
+  GCOL_CK(dalloc(&g->d_vpre, static_cast<size_t>(rows) + 1, g->stream));
+  GCOL_CK(dalloc(&d_pieces, static_cast<size_t>(rows) + 1, g->stream));
+  GCOL_CK(cudaMemsetAsync(d_pieces, 0, sizeof(int) * (static_cast<size_t>(rows) + 1), g->stream));
+  GCOL_CK(cudaMemsetAsync(d_len, 0, sizeof(int), g->stream));
+  k_collect_big<<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, static_cast<int>(g->n), kHPiece,
+                                                       g->d_vrows, d_pieces, d_len);
+  GCOL_CK(cudaGetLastError());
+  size_t tmp_bytes = 0;
+  void* d_tmp = nullptr;
+  GCOL_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_pieces, g->d_vpre, rows + 1,
+                                        g->stream));
+  GCOL_CK(cudaMallocAsync(&d_tmp, std::max<size_t>(tmp_bytes, 1), g->stream));
+  GCOL_CK(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_pieces, g->d_vpre, rows + 1,
+                                        g->stream));
+  GCOL_CK(cudaFreeAsync(d_tmp, g->stream));
+  GCOL_CK(cudaFreeAsync(d_pieces, g->stream));
+  GCOL_CK(cudaFreeAsync(d_len, g->stream));
+  g->nvrows = rows;
+  return GCOL_OK;
+}
+
 int verify_device(gcol_cuda_graph* g, const int* d_col, gcol_cuda_verify_report* rep,
                   uint32_t* out_u, uint32_t* out_v, int32_t* out_c, int64_t cap) {
   const int n = static_cast<int>(g->n);
+  if (int rc = ensure_verify_plan(g)) return rc;
   VerifyAcc* d_acc = nullptr;
   int* d_vcount = nullptr;
   GCOL_CK(dalloc(&d_acc, 1, g->stream));
@@ -477,7 +607,11 @@ int verify_device(gcol_cuda_graph* g, const int* d_col, gcol_cuda_verify_report*
   if (cap > 0) GCOL_CK(dalloc(&d_vcount, static_cast<size_t>(n), g->stream));
   const int grid = g->sms * 8;
   if (n > 0)
-    k_verify_count<<<grid, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, d_col, d_acc, d_vcount);
+    k_verify_count<<<grid, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, d_col, d_acc, d_vcount,
+                                                   g->nvrows > 0 ? kHPiece : INT_MAX);
+  if (n > 0 && g->nvrows > 0)
+    k_verify_big<<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, d_col, g->d_vrows,
+                                                       g->d_vpre, g->nvrows, d_acc, d_vcount);
   GCOL_CK(cudaGetLastError());
   VerifyAcc acc;
   GCOL_CK(cudaMemcpyAsync(&acc, d_acc, sizeof acc, cudaMemcpyDeviceToHost, g->stream));
@@ -591,8 +725,87 @@ int gcol_cuda_device_count(int32_t* count) {
   return GCOL_OK;
 }
 
-int gcol_cuda_graph_create(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t m,
-                           int32_t memory, int32_t device, gcol_cuda_graph** out) {
+}  // extern "C"
+
+namespace {
+
+// Structural checks of a host CSR (graph.hpp:50-56: offsets cover the
+// adjacency and never decrease), split over host threads; called while the
+// upload DMA runs.
+int validate_offsets_host(const int64_t* off, int64_t n, GraphStats* gs) {
+  const int64_t kPer = 1 << 18;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int T = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>({static_cast<int64_t>(hw), 16, (n + kPer - 1) / kPer})));
+  std::atomic<bool> bad{false};
+  std::vector<GraphStats> part(static_cast<size_t>(T));
+  auto work = [&](int t) {
+    const int64_t lo = n * t / T, hi = n * (t + 1) / T;
+    GraphStats s{};
+    for (int64_t v = lo; v < hi; ++v) {
+      const int64_t d = off[v + 1] - off[v];
+      if (d < 0) {
+        bad.store(true, std::memory_order_relaxed);
+        return;
+      }
+      gs_add(s, d);
+    }
+    part[static_cast<size_t>(t)] = s;
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  if (bad.load()) return fail(GCOL_ERR_INVALID_ARGUMENT, "graph: offsets are not monotone");
+  GraphStats tot{};
+  for (const GraphStats& s : part) {
+    tot.max_degree = std::max(tot.max_degree, s.max_degree);
+    for (int k = 0; k < 3; ++k) {
+      tot.rows[k] += s.rows[k];
+      tot.pieces[k] += s.pieces[k];
+    }
+  }
+  *gs = tot;
+  return GCOL_OK;
+}
+
+__global__ void k_publish(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+constexpr int64_t kUploadPiece = 1 << 21;  // smallest streamed piece x 2 (entries)
+
+// Publishing the upload progress: a stream memory operation executed by the
+// copy stream itself (no kernel has to be scheduled next to the running K1);
+// a one-thread release-store kernel where the driver lacks it.
+using WriteValue64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+WriteValue64Fn write_value64() {
+  static WriteValue64Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+    return reinterpret_cast<WriteValue64Fn>(p);
+  }();
+  return fn;
+}
+
+void publish_progress(cudaStream_t s, unsigned long long* p, unsigned long long v) {
+  if (WriteValue64Fn fn = write_value64())
+    if (fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(p), v, 0) == CUDA_SUCCESS)
+      return;
+  k_publish<<<1, 1, 0, s>>>(p, v);
+}
+
+// Shared by graph_create and color_rsoc_csr.  `streamed`: the adjacency is
+// uploaded in pieces on a second stream, each followed by a release of the
+// entries now resident, and the call returns once the offsets are resident
+// (K1 follows the pieces; everything after K1 is ordered behind them).
+int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t m,
+                int32_t memory, int32_t device, bool streamed, gcol_cuda_graph** out) {
   if (!out) return fail(GCOL_ERR_INVALID_ARGUMENT, "out is null");
   *out = nullptr;
   if (n < 0 || m < 0) return fail(GCOL_ERR_INVALID_ARGUMENT, "negative size");
@@ -602,13 +815,8 @@ int gcol_cuda_graph_create(const int64_t* offsets, const int32_t* cols, int64_t 
   if (m > 0 && !cols) return fail(GCOL_ERR_INVALID_ARGUMENT, "cols is null");
   if (memory != GCOL_MEM_HOST && memory != GCOL_MEM_DEVICE)
     return fail(GCOL_ERR_INVALID_ARGUMENT, "bad memory kind");
-  if (memory == GCOL_MEM_HOST) {  // cheap structural checks (graph.hpp:50-56)
-    if (offsets[0] != 0 || offsets[n] != m)
-      return fail(GCOL_ERR_INVALID_ARGUMENT, "graph: offsets do not cover the adjacency array");
-    for (int64_t v = 0; v < n; ++v)
-      if (offsets[v] > offsets[v + 1])
-        return fail(GCOL_ERR_INVALID_ARGUMENT, "graph: offsets are not monotone");
-  }
+  if (memory == GCOL_MEM_HOST && (offsets[0] != 0 || offsets[n] != m))
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "graph: offsets do not cover the adjacency array");
   int dev = 0;
   int rc = ensure_device(device, &dev);
   if (rc != GCOL_OK) return rc;
@@ -645,26 +853,90 @@ int gcol_cuda_graph_create(const int64_t* offsets, const int32_t* cols, int64_t 
     if (dalloc(&g->d_off, static_cast<size_t>(n) + 1, g->stream) != cudaSuccess ||
         dalloc(&g->d_cols, static_cast<size_t>(m), g->stream) != cudaSuccess)
       return bail(fail(GCOL_ERR_CUDA, "device allocation of the CSR failed"));
-    if (copy_in(g, g->d_off, offsets, sizeof(long long) * (static_cast<size_t>(n) + 1), memory) ||
-        copy_in(g, g->d_cols, cols, sizeof(int) * static_cast<size_t>(m), memory))
-      return bail(GCOL_ERR_CUDA);
+    const size_t off_bytes = sizeof(long long) * (static_cast<size_t>(n) + 1);
+    if (!streamed) {
+      if (copy_in(g, g->d_off, offsets, off_bytes, memory) ||
+          copy_in(g, g->d_cols, cols, sizeof(int) * static_cast<size_t>(m), memory))
+        return bail(GCOL_ERR_CUDA);
+    } else {
+      cudaEvent_t ev_alloc = nullptr, ev_off = nullptr;
+      if (dalloc(&g->d_progress, 1, g->stream) != cudaSuccess ||
+          cudaMemsetAsync(g->d_progress, 0, sizeof(unsigned long long), g->stream) != cudaSuccess ||
+          cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_off, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreate(&g->ev_copied) != cudaSuccess || cudaEventCreate(&g->ev_copy0) != cudaSuccess)
+        return bail(fail(GCOL_ERR_CUDA, "streamed upload setup failed"));
+      const auto mt = memory == GCOL_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+      cudaEventRecord(ev_alloc, g->stream);
+      cudaStreamWaitEvent(g->copy_stream, ev_alloc, 0);
+      cudaEventRecord(g->ev_copy0, g->copy_stream);
+      cudaMemcpyAsync(g->d_off, offsets, off_bytes, mt, g->copy_stream);
+      cudaEventRecord(ev_off, g->copy_stream);
+      // pieces of m/32 entries (4M..16M: each costs ~25 us of DMA restart), the
+      // last 2 pieces' worth in halving steps down to 1M, so the rows that K1
+      // can only colour after the transfer ends are few
+      int64_t piece = std::min<int64_t>(std::max<int64_t>(m / 32, 4 << 20), 16 << 20);
+      if (const char* pe = std::getenv("GCOL_UPLOAD_PIECE")) piece = std::max<int64_t>(1024, std::atoll(pe));
+      for (int64_t p = 0, len = 0; p < m; p += len) {
+        const int64_t r = m - p;
+        len = r > 2 * piece ? piece : std::min(r, std::max<int64_t>(r / 2, kUploadPiece / 2));
+        cudaMemcpyAsync(g->d_cols + p, cols + p, sizeof(int) * static_cast<size_t>(len), mt,
+                        g->copy_stream);
+        publish_progress(g->copy_stream, g->d_progress, static_cast<unsigned long long>(p + len));
+      }
+      cudaEventRecord(g->ev_copied, g->copy_stream);
+      cudaStreamWaitEvent(g->stream, ev_off, 0);  // offsets first; the adjacency follows
+      cudaEventDestroy(ev_alloc);
+      cudaEventDestroy(ev_off);
+      if ((e = cudaGetLastError()) != cudaSuccess)
+        return bail(fail(GCOL_ERR_CUDA, std::string("streamed upload: ") + cudaGetErrorString(e)));
+    }
   }
-  int* d_max = nullptr;
-  if (dalloc(&d_max, 1, g->stream) != cudaSuccess) return bail(fail(GCOL_ERR_CUDA, "alloc"));
-  cudaMemsetAsync(d_max, 0, sizeof(int), g->stream);
-  if (n > 0) k_max_degree<<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, static_cast<int>(n), d_max);
-  cudaMemcpyAsync(&g->max_degree, d_max, sizeof(int), cudaMemcpyDeviceToHost, g->stream);
-  cudaFreeAsync(d_max, g->stream);
-  e = cudaStreamSynchronize(g->stream);
+  tmark("enqueue");
+  if (memory == GCOL_MEM_HOST) {  // validation + degree statistics overlap the upload
+    if (int vr = validate_offsets_host(offsets, n, &g->gs)) return bail(vr);
+  } else {
+    GraphStats* d_gs = nullptr;
+    if (dalloc(&d_gs, 1, g->stream) != cudaSuccess) return bail(fail(GCOL_ERR_CUDA, "alloc"));
+    cudaMemsetAsync(d_gs, 0, sizeof(GraphStats), g->stream);
+    if (n > 0)
+      k_graph_stats<<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, static_cast<int>(n), d_gs);
+    cudaMemcpyAsync(&g->gs, d_gs, sizeof(GraphStats), cudaMemcpyDeviceToHost, g->stream);
+    cudaFreeAsync(d_gs, g->stream);
+  }
+  tmark("validate");
+  // a host CSR must be fully read before the call returns (the streamed
+  // upload keeps its own stream, synchronised by the run and destroy)
+  e = streamed ? cudaGetLastError() : cudaStreamSynchronize(g->stream);
+  g->max_degree = g->gs.max_degree;
+  tmark("sync");
   if (e != cudaSuccess)
     return bail(fail(GCOL_ERR_CUDA, std::string("graph upload: ") + cudaGetErrorString(e)));
   *out = g;
   return GCOL_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int gcol_cuda_graph_create(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t m,
+                           int32_t memory, int32_t device, gcol_cuda_graph** out) {
+  return create_impl(offsets, cols, n, m, memory, device, false, out);
+}
+
 int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
   if (!g) return GCOL_OK;
   cudaSetDevice(g->device);
+  if (g->copy_stream) {  // a streamed upload still in flight reads the caller's memory
+    cudaStreamSynchronize(g->copy_stream);
+    cudaStreamDestroy(g->copy_stream);
+    g->copy_stream = nullptr;
+  }
+  if (g->ev_copied) cudaEventDestroy(g->ev_copied);
+  if (g->ev_copy0) cudaEventDestroy(g->ev_copy0);
+  if (g->d_progress && g->stream) cudaFreeAsync(g->d_progress, g->stream);
   for (auto& kv : g->execs) {
     cudaGraphExecDestroy(kv.second.second);
     cudaGraphDestroy(kv.second.first);
@@ -675,6 +947,10 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
       cudaFreeAsync(g->d_off, g->stream);
       cudaFreeAsync(g->d_cols, g->stream);
     }
+    for (void* p : {static_cast<void*>(g->d_hq), static_cast<void*>(g->d_hslot),
+                    static_cast<void*>(g->d_hslot_bm), static_cast<void*>(g->d_vrows),
+                    static_cast<void*>(g->d_vpre)})
+      if (p) cudaFreeAsync(p, g->stream);
     for (void* p : {static_cast<void*>(g->d_colors), static_cast<void*>(g->d_listA),
                     static_cast<void*>(g->d_listB), static_cast<void*>(g->d_heavy),
                     static_cast<void*>(g->d_marks), static_cast<void*>(g->d_pairs),
@@ -684,7 +960,11 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
     cudaStreamSynchronize(g->stream);
     cudaStreamDestroy(g->stream);
   }
-  for (cudaEvent_t ev : {g->ev_start, g->ev_k1, g->ev_end})
+  if (g->out_stream) {
+    cudaStreamSynchronize(g->out_stream);
+    cudaStreamDestroy(g->out_stream);
+  }
+  for (cudaEvent_t ev : {g->ev_start, g->ev_k1, g->ev_end, g->ev_final})
     if (ev) cudaEventDestroy(ev);
   delete g;
   return GCOL_OK;
@@ -715,6 +995,7 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   if (!eager)
     if (int rc = get_exec(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide, &exec))
       return rc;
+  tmark("exec");
   // Untimed prologue, like Coloring(n) before the reference's timer
   // (parallel.hpp:258 vs :267): colours := -1, marks := 0, control reset.
   const size_t n = static_cast<size_t>(g->n);
@@ -731,10 +1012,23 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
       if (int rc = reset_split(g, &sp->second, g->k1_warps[exec])) return rc;
     GCOL_CK(cudaGraphLaunch(exec, g->stream));
   }
+  // streamed upload: K1 followed the pieces; what comes next reads anything
+  if (g->ev_copied) GCOL_CK(cudaStreamWaitEvent(g->stream, g->ev_copied, 0));
+  // the colours are final here: a copy into pinned host memory overlaps the
+  // verification pass below (both only read them)
+  const bool early_out = colors_memory == GCOL_MEM_HOST && n > 0 && is_pinned_host(colors_out);
+  if (early_out) {
+    GCOL_CK(cudaEventRecord(g->ev_final, g->stream));
+    GCOL_CK(cudaStreamWaitEvent(g->out_stream, g->ev_final, 0));
+    GCOL_CK(cudaMemcpyAsync(colors_out, g->d_colors, sizeof(int) * n, cudaMemcpyDeviceToHost,
+                            g->out_stream));
+  }
   // Header + conflicts_per_round back in two copies.
+  tmark("launch");
   Ctrl hdr;
   GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
   GCOL_CK(cudaStreamSynchronize(g->stream));
+  tmark("run");
   const int rounds = hdr.round;
   if (std::getenv("GCOL_K1_PROFILE")) {
     const double ch = hdr.prof[5] ? static_cast<double>(hdr.prof[5]) : 1.0;
@@ -756,11 +1050,25 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   float ms_total = 0.f, ms_k1 = 0.f;
   GCOL_CK(cudaEventElapsedTime(&ms_total, g->ev_start, g->ev_end));
   GCOL_CK(cudaEventElapsedTime(&ms_k1, g->ev_start, g->ev_k1));
+  if (g_trace && g->ev_copy0) {
+    float a = 0.f, b = 0.f, c = 0.f;
+    cudaEventSynchronize(g->ev_copied);
+    cudaEventElapsedTime(&a, g->ev_copy0, g->ev_copied);
+    cudaEventElapsedTime(&b, g->ev_copy0, g->ev_start);
+    cudaEventElapsedTime(&c, g->ev_copy0, g->ev_end);
+    std::fprintf(stderr, "[gcol trace] upload %.3f ms; K1 starts at %.3f, K1 ends %.3f, rounds end %.3f\n",
+                 a, b, b + ms_k1, c);
+  }
   // finalize_run (parallel.hpp:164-177): verify after the timed region.
   gcol_cuda_verify_report rep{};
   if (int rc = verify_device(g, g->d_colors, &rep, nullptr, nullptr, nullptr, 0)) return rc;
-  if (int rc = copy_out(g, colors_out, g->d_colors, sizeof(int) * n, colors_memory)) return rc;
+  tmark("verify");
+  if (early_out)
+    GCOL_CK(cudaStreamSynchronize(g->out_stream));
+  else if (int rc = copy_out(g, colors_out, g->d_colors, sizeof(int) * n, colors_memory))
+    return rc;
   GCOL_CK(cudaStreamSynchronize(g->stream));
+  tmark("out");
   if (stats) {
     stats->algorithm = GCOL_ALG_RSOC;
     stats->thread_count = opt.thread_count;
@@ -789,6 +1097,29 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   if (rep.violations != 0 || rep.out_of_bound != 0)
     return fail(GCOL_ERR_VERIFY, "parallel coloring finished improper");
   return GCOL_OK;
+}
+
+int gcol_cuda_color_rsoc_csr(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t m,
+                             int32_t device, const gcol_cuda_options* opt_in, int32_t* colors_out,
+                             gcol_cuda_stats* stats) {
+  gcol_cuda_options opt;
+  if (int rc = read_options(opt_in, &opt)) return rc;
+  if (n > 0 && !colors_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "colors_out is null");
+  gcol_cuda_graph* g = nullptr;
+  Trace tr;
+  g_trace = tr.on ? &tr : nullptr;
+  tmark("start");
+  if (int rc = create_impl(offsets, cols, n, m, GCOL_MEM_HOST, device, true, &g)) {
+    g_trace = nullptr;
+    return rc;
+  }
+  tmark("create");
+  const int rc = gcol_cuda_color_rsoc(g, opt_in, colors_out, GCOL_MEM_HOST, stats);
+  gcol_cuda_graph_destroy(g);
+  tmark("destroy");
+  tr.print("color_rsoc_csr");
+  g_trace = nullptr;
+  return rc;
 }
 
 int gcol_cuda_first_fit_sequential(gcol_cuda_graph* g, int32_t* colors_out, int32_t colors_memory) {

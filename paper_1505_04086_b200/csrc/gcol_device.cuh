@@ -22,6 +22,7 @@ constexpr int kWarpMax = 1023;          // 64..1023: warp per row, 1024-colour s
 constexpr int kStage = 1024;            // staged adjacency entries per warp (4 KB)
 constexpr int kStageStep = kStage - 64; // rows starting in a batch always fit the stage
 constexpr int kBWinWords = 512;         // block window: 16384 colours (2 KB)
+constexpr int kHPiece = 4096;           // entries per piece of a heavy row in the rounds
 constexpr int kMaxRoundsRecorded = 1 << 16;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -57,6 +58,18 @@ struct Ctrl {
   int capped;
   int cand_total;                   // round-1 candidates
   int done;                         // loop exit flag (eager mode reads it)
+  // heavy rows (deg > kWarpMax) of a round, split into kHPiece-entry pieces
+  // spread over the whole grid (k_heavy); slots are per heavy row
+  int heavy_slots;                  // slots used this round
+  int heavy_pieces;                 // pieces queued this round
+  int hslots;                       // slot capacity (0: split path off)
+  int hq_cap;                       // piece capacity
+  int2* hq;                         // (slot, first entry) per piece
+  int* hslot_v;                     // row of a slot
+  int* hslot_i;                     // its worklist position
+  int* hslot_left;                  // pieces not finished yet
+  int* hslot_flag;                  // 1: the row is defective
+  unsigned* hslot_bm;               // [hslots][kBWinWords] colours seen, 0..16383
   unsigned long long prof[16];      // K1 phase cycle counters (GCOL_K1_PROFILE)
   unsigned long long cpr[kMaxRoundsRecorded];  // conflicts_per_round
 };

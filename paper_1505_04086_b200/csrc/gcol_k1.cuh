@@ -105,6 +105,7 @@ struct SplitArgs {
   int* alive;           // consumer warps that may still publish pieces
   int G;                // mailboxes (= K1 grid)
   unsigned* done_chunks;  // chunks fully consumed (drift bound)
+  const unsigned long long* progress;  // streamed upload: adjacency entries resident (or null)
 };
 
 // First-Fit restricted to the colour window [wb, wb + 1024) (warp-wide);
@@ -393,6 +394,12 @@ __device__ __forceinline__ void k1_medium(const int* __restrict__ cols, const in
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned r;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  return r;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long r;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
   return r;
 }
 
@@ -814,6 +821,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) k1_pipe(const long long* __r
       if (contig) {
         mbar_wait(&sl.offb, par);              // offsets of chunk k (every lane; the
                                                // slot was freed before they were requested)
+        if (S.progress) {  // streamed upload: the chunk's adjacency must be resident
+          const unsigned long long need = (unsigned long long)sl.offs[rows];
+          if (lane == 0)
+            while (ld_acquire_u64(S.progress) < need) __nanosleep(256);
+          __syncwarp();
+        }
         stage_chunk<CW>(sl, rows, S.min_deg, cols, m, pol);
         if (lane == 0) {
           sl.rows = rows;

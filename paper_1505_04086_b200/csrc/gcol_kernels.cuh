@@ -92,7 +92,28 @@ __global__ void __launch_bounds__(kBlock) k_list(const long long* __restrict__ o
     const long long b = ld_off(off + v, pol);
     const int deg = (int)(ld_off(off + v + 1, pol) - b);
     if (deg > kWarpMax) {
-      if (lane == 0) heavy[atomicAdd(&ctrl->heavy_len, 1)] = i;
+      int slot = -1;
+      if (!kDetectOnly && R != kOrdered && ctrl->hslots > 0) {
+        if (lane == 0) {
+          slot = atomicAdd(&ctrl->heavy_slots, 1);
+          if (slot >= ctrl->hslots) slot = -1;  // out of slots: one block per row below
+        }
+        slot = __shfl_sync(kFull, slot, 0);
+      }
+      if (slot >= 0) {  // split over the grid: kHPiece-entry pieces for k_heavy
+        const int np = (deg + kHPiece - 1) / kHPiece;
+        int p0 = 0;
+        if (lane == 0) {
+          p0 = atomicAdd(&ctrl->heavy_pieces, np);
+          ctrl->hslot_v[slot] = v;
+          ctrl->hslot_i[slot] = i;
+          ctrl->hslot_left[slot] = np;
+        }
+        p0 = __shfl_sync(kFull, p0, 0);
+        for (int j = lane; j < np; j += 32) ctrl->hq[p0 + j] = make_int2(slot, j * kHPiece);
+      } else if (lane == 0) {
+        heavy[atomicAdd(&ctrl->heavy_len, 1)] = i;
+      }
       continue;
     }
     const bool d = warp_defective<R>(off, cols, colors, v, b, deg, pol);
@@ -125,6 +146,99 @@ __global__ void __launch_bounds__(kBlock) k_list(const long long* __restrict__ o
   }
 }
 
+// One piece of a split heavy row (block-wide): detect its conflicts and
+// OR the colours it sees into the row's slot bitmap; the block finishing the
+// row's last piece recolours it when defective (First-Fit over the bitmap).
+template <int R>
+__device__ __forceinline__ void heavy_piece(const long long* __restrict__ off,
+                                            const int* __restrict__ cols, int* colors, Ctrl* ctrl,
+                                            int slot, int start, unsigned* s_bwin, int* s_red,
+                                            uint64_t pol) {
+  constexpr int U = 4;
+  const int tid = threadIdx.x;
+  const int v = ctrl->hslot_v[slot];
+  const long long b = ld_off(off + v, pol);
+  const int deg = (int)(ld_off(off + v + 1, pol) - b);
+  const int cv = ld_color(colors + v);
+  const int end = min(deg, start + kHPiece);
+  for (int k = tid; k < kBWinWords; k += kBlock) s_bwin[k] = 0u;
+  __syncthreads();
+  bool hit = false;
+  unsigned long long reg = 0ull;
+  for (int base = start; base < end; base += kBlock * U) {
+    int w[U], c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * kBlock + tid;
+      w[u] = i < end ? ld_col(cols + b + i, pol) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = w[u] >= 0 ? ld_color(colors + w[u]) : -2;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (c[u] >= 0 && c[u] <= deg && c[u] < kBWinWords * 32) {
+        if (c[u] < 64) reg |= 1ull << c[u];
+        else atomicOr(&s_bwin[c[u] >> 5], 1u << (c[u] & 31));
+      }
+      if (cv >= 0 && c[u] == cv && considers<R>(v, w[u])) {
+        if (R == kDegId) {
+          const int dw = (int)(ld_off(off + w[u] + 1, pol) - ld_off(off + w[u], pol));
+          hit |= yields_to<R>(v, deg, w[u], dw);
+        } else {
+          hit = true;
+        }
+      }
+    }
+  }
+  const unsigned lo = __reduce_or_sync(kFull, (unsigned)reg);
+  const unsigned hi = __reduce_or_sync(kFull, (unsigned)(reg >> 32));
+  if (lane_id() == 0) {
+    if (lo) atomicOr(&s_bwin[0], lo);
+    if (hi) atomicOr(&s_bwin[1], hi);
+  }
+  const int any = __syncthreads_or(hit);
+  unsigned* gbm = ctrl->hslot_bm + (size_t)slot * kBWinWords;
+  for (int k = tid; k < kBWinWords; k += kBlock)
+    if (s_bwin[k]) atomicOr(gbm + k, s_bwin[k]);
+  if (tid == 0 && any) atomicOr(ctrl->hslot_flag + slot, 1);
+  __syncthreads();
+  if (tid == 0) *s_red = atom_add_acq_rel(ctrl->hslot_left + slot, -1) == 1 ? 1 : 0;
+  __syncthreads();
+  if (!*s_red) return;
+  // last piece of the row
+  const bool defective = ld_acquire_u32(reinterpret_cast<const unsigned*>(ctrl->hslot_flag + slot)) != 0u;
+  __syncthreads();
+  if (tid == 0) *s_red = INT_MAX;
+  __syncthreads();
+  if (defective) {
+    const int lim = min(deg, kBWinWords * 32 - 1);  // candidates 0..lim
+    for (int k = tid; k * 32 <= lim; k += kBlock) {
+      unsigned fr = ~ld_acquire_u32(gbm + k);
+      const int top = lim - k * 32;  // valid bits 0..top of this word
+      if (top < 31) fr &= (2u << top) - 1u;
+      if (fr) atomicMin(s_red, k * 32 + __ffs(fr) - 1);
+    }
+  }
+  __syncthreads();
+  int c = *s_red;
+  __syncthreads();
+  if (defective && c == INT_MAX) {  // 16384 colours all seen: the next windows, the slow way
+    PairLog L{};
+    unsigned dummy = 0;
+    c = block_first_fit<false, false, false>(cols, colors, v, b, deg, s_bwin, s_red, pol, L,
+                                              dummy);
+  }
+  if (tid == 0) {
+    if (defective) {
+      st_color(colors + v, c);
+      atomicAdd(&ctrl->recolored, 1);
+      ctrl->out_list[atomicAdd(&ctrl->out_len, 1)] = v;
+    }
+    ctrl->hslot_flag[slot] = 0;
+  }
+  for (int k = tid; k < kBWinWords; k += kBlock) gbm[k] = 0u;  // clean for the next round
+}
+
 template <int R, bool kDetectOnly>
 __global__ void __launch_bounds__(kBlock) k_heavy(const long long* __restrict__ off,
                                                   const int* __restrict__ cols, int* colors,
@@ -132,6 +246,14 @@ __global__ void __launch_bounds__(kBlock) k_heavy(const long long* __restrict__ 
   __shared__ unsigned s_bwin[kBWinWords];
   __shared__ int s_red;
   const uint64_t pol = policy_evict_first();
+  if (!kDetectOnly && R != kOrdered) {
+    const int npc = ctrl->heavy_pieces;
+    for (int p = blockIdx.x; p < npc; p += gridDim.x) {
+      const int2 e = ctrl->hq[p];
+      heavy_piece<R>(off, cols, colors, ctrl, e.x, e.y, s_bwin, &s_red, pol);
+      __syncthreads();
+    }
+  }
   const int nh = ctrl->heavy_len;
   const int* in = ctrl->in_list;
   PairLog L{};
@@ -187,6 +309,8 @@ __global__ void k_control(Ctrl* ctrl, cudaGraphConditionalHandle handle, int in_
   ctrl->in_len = found;
   ctrl->out_len = 0;
   ctrl->heavy_len = 0;
+  ctrl->heavy_slots = 0;
+  ctrl->heavy_pieces = 0;
   unsigned cont = 0;
   if (found > 0) {
     if (r >= ctrl->round_cap) ctrl->capped = 1;
@@ -212,10 +336,11 @@ struct VerifyAcc {
 __global__ void __launch_bounds__(kBlock) k_verify_count(const long long* __restrict__ off,
                                                          const int* __restrict__ cols, int n,
                                                          const int* colors, VerifyAcc* acc,
-                                                         int* vcount) {
+                                                         int* vcount, int big_min) {
+  // rows with deg >= big_min (a piece plan exists) are left to k_verify_big
+  constexpr int U = 4;
   __shared__ unsigned long long s_acc[4];
   __shared__ int s_max;
-  const uint64_t pol = policy_evict_first();
   const int lane = lane_id();
   if (threadIdx.x < 4) s_acc[threadIdx.x] = 0ull;
   if (threadIdx.x == 0) s_max = -1;
@@ -234,8 +359,8 @@ __global__ void __launch_bounds__(kBlock) k_verify_count(const long long* __rest
     bool big = false;
     if (valid) {
       c = colors[v];
-      b = ld_off(off + v, pol);
-      deg = (int)(ld_off(off + v + 1, pol) - b);
+      b = __ldg(off + v);
+      deg = (int)(__ldg(off + v + 1) - b);
       if (c == -1) {
         unc++;
         cnt = 1;
@@ -243,17 +368,23 @@ __global__ void __launch_bounds__(kBlock) k_verify_count(const long long* __rest
         if (c < -1 || c > deg) oob++;
         if (c < -1) neg++;
         if (c > mx) mx = c;
-        if (deg <= 32) {
-          for (int k = 0; k < deg; ++k) {
-            const int w = ld_col(cols + b + k, pol);
-            if (w > v && colors[w] == c) cnt++;
-          }
-        } else {
-          big = true;
-        }
+        big = deg > 32;
       }
     }
-    unsigned bigm = __ballot_sync(kFull, big);
+    // thread per row: independent loads, U entries at a time
+    const int lim = valid && c != -1 && !big ? deg : 0;
+    const int maxk = (int)__reduce_max_sync(kFull, (unsigned)lim);
+    for (int k = 0; k < maxk; k += U) {
+      int w[U], cw[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] = k + u < lim ? __ldg(cols + b + k + u) : -1;
+#pragma unroll
+      for (int u = 0; u < U; ++u) cw[u] = w[u] > v ? colors[w[u]] : -3;
+#pragma unroll
+      for (int u = 0; u < U; ++u) cnt += cw[u] == c;
+    }
+    // warp per row
+    unsigned bigm = __ballot_sync(kFull, big && deg < big_min);
     while (bigm) {
       const int r = __ffs(bigm) - 1;
       bigm &= bigm - 1;
@@ -262,11 +393,19 @@ __global__ void __launch_bounds__(kBlock) k_verify_count(const long long* __rest
       const long long br = __shfl_sync(kFull, b, r);
       const int dr = __shfl_sync(kFull, deg, r);
       int hits = 0;
-      for (int k = lane; k < dr; k += 32) {
-        const int w = ld_col(cols + br + k, pol);
-        if (w > vr && colors[w] == cr) hits++;
+      for (int k0 = 0; k0 < dr; k0 += 32 * U) {
+        int w[U], cw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = k0 + u * 32 + lane;
+          w[u] = k < dr ? __ldg(cols + br + k) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) cw[u] = w[u] > vr ? colors[w[u]] : -3;
+#pragma unroll
+        for (int u = 0; u < U; ++u) hits += cw[u] == cr;
       }
-      hits = __reduce_add_sync(kFull, (unsigned)hits);
+      hits = (int)__reduce_add_sync(kFull, (unsigned)hits);
       if (lane == r) cnt += hits;
     }
     if (valid) {
@@ -287,6 +426,71 @@ __global__ void __launch_bounds__(kBlock) k_verify_count(const long long* __rest
     atomicAdd(&acc->negative, s_acc[3]);
     atomicAdd(&acc->violations, s_acc[0] + s_acc[1]);
     atomicMax(&acc->max_color, s_max);
+  }
+}
+
+// The rows k_verify_count left out (deg >= big_min), as kHPiece-entry pieces
+// spread over the grid: piece p belongs to rows[j] with pre[j] <= p < pre[j+1].
+__global__ void __launch_bounds__(kBlock) k_verify_big(const long long* __restrict__ off,
+                                                       const int* __restrict__ cols,
+                                                       const int* colors, const int* rows,
+                                                       const int* pre, int nrows, VerifyAcc* acc,
+                                                       int* vcount) {
+  constexpr int U = 4;
+  __shared__ int s_hits;
+  const int npieces = pre[nrows];
+  for (int p = blockIdx.x; p < npieces; p += gridDim.x) {
+    int lo = 0, hi = nrows - 1;  // last j with pre[j] <= p
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(pre + mid) <= p) lo = mid;
+      else hi = mid - 1;
+    }
+    const int v = rows[lo];
+    const int c = colors[v];
+    if (c == -1) continue;  // counted once by k_verify_count
+    const long long b = __ldg(off + v);
+    const int deg = (int)(__ldg(off + v + 1) - b);
+    const int start = (p - pre[lo]) * kHPiece;
+    const int end = min(deg, start + kHPiece);
+    if (threadIdx.x == 0) s_hits = 0;
+    __syncthreads();
+    int hits = 0;
+    for (int k0 = start; k0 < end; k0 += kBlock * U) {
+      int w[U], cw[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u * kBlock + threadIdx.x;
+        w[u] = k < end ? __ldg(cols + b + k) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) cw[u] = w[u] > v ? colors[w[u]] : -3;
+#pragma unroll
+      for (int u = 0; u < U; ++u) hits += cw[u] == c;
+    }
+    hits = (int)__reduce_add_sync(kFull, (unsigned)hits);
+    if (lane_id() == 0 && hits) atomicAdd(&s_hits, hits);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_hits) {
+      atomicAdd(&acc->conflict_edges, (unsigned long long)s_hits);
+      atomicAdd(&acc->violations, (unsigned long long)s_hits);
+      if (vcount) atomicAdd(vcount + v, s_hits);
+    }
+    __syncthreads();
+  }
+}
+
+// Rows with deg >= min_deg, appended in any order, and their piece counts.
+__global__ void k_collect_big(const long long* __restrict__ off, int n, int min_deg, int* rows,
+                              int* pieces, int* len) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x) {
+    const long long d = off[v + 1] - off[v];
+    if (d >= min_deg) {
+      const int j = atomicAdd(len, 1);
+      rows[j] = (int)v;
+      pieces[j] = (int)((d + kHPiece - 1) / kHPiece);
+    }
   }
 }
 
@@ -367,13 +571,50 @@ __global__ void __launch_bounds__(kBlock) k_first_fit_seq(const long long* __res
   }
 }
 
-__global__ void k_max_degree(const long long* __restrict__ off, int n, int* out) {
-  int mx = 0;
+// Degree statistics every run plan needs, in one pass over the offsets
+// (on the host while validating a host CSR, or by k_graph_stats):
+//   [0] rows K1 splits into kPiece pieces (deg >= kSplitDefault)
+//   [1] rows the rounds split into kHPiece pieces (deg > kWarpMax)
+//   [2] rows verified in kHPiece pieces (deg >= kHPiece)
+struct GraphStats {
+  unsigned long long rows[3];
+  unsigned long long pieces[3];
+  int max_degree;
+  int pad;
+};
+
+__host__ __device__ inline void gs_add(GraphStats& s, long long d) {
+  if (d > s.max_degree) s.max_degree = (int)d;
+  if (d >= kSplitDefault) {
+    s.rows[0]++;
+    s.pieces[0] += (unsigned long long)((d + kPiece - 1) / kPiece);
+  }
+  if (d > kWarpMax) {
+    s.rows[1]++;
+    s.pieces[1] += (unsigned long long)((d + kHPiece - 1) / kHPiece);
+  }
+  if (d >= kHPiece) {
+    s.rows[2]++;
+    s.pieces[2] += (unsigned long long)((d + kHPiece - 1) / kHPiece);
+  }
+}
+
+__global__ void k_graph_stats(const long long* __restrict__ off, int n, GraphStats* out) {
+  GraphStats s{};
   for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (long long)gridDim.x * blockDim.x)
-    mx = max(mx, (int)(off[v + 1] - off[v]));
-  mx = (int)__reduce_max_sync(kFull, (unsigned)mx);
-  if (lane_id() == 0) atomicMax(out, mx);
+    gs_add(s, off[v + 1] - off[v]);
+  const int mx = (int)__reduce_max_sync(kFull, (unsigned)s.max_degree);
+  if (lane_id() == 0) atomicMax(&out->max_degree, mx);
+  for (int k = 0; k < 3; ++k) {
+    if (__any_sync(kFull, s.rows[k] != 0)) {
+      // few rows qualify: plain atomics from the lanes that saw some
+      if (s.rows[k]) {
+        atomicAdd(&out->rows[k], s.rows[k]);
+        atomicAdd(&out->pieces[k], s.pieces[k]);
+      }
+    }
+  }
 }
 
 __global__ void k_fill(int* p, long long n, int value) {

@@ -375,6 +375,52 @@ def color_rsoc(g: Graph, thread_count: int, opt: Optional[ParallelOptions] = Non
     return run_coloring(g, Algorithm.rsoc, thread_count, opt, **kw)
 
 
+def color_rsoc_csr(offsets, adjacency, thread_count: int,
+                   opt: Optional[ParallelOptions] = None, *, colors_out=None,
+                   device: int = -1) -> ColoringRun:
+    """color_rsoc on a host CSR in one call (parallel.hpp:253 with a host
+    Graph): the adjacency upload is overlapped with the initial pass
+    (gcol_cuda_color_rsoc_csr).  offsets/adjacency: int64 / int32 host arrays
+    (numpy, or CPU torch tensors -- pinned ones upload asynchronously);
+    colors_out: optional int32 host array of n entries."""
+    if thread_count < 1:
+        raise input_error("thread_count must be at least 1")
+    opt = opt or ParallelOptions()
+
+    def host_ptr(a, dtype):
+        if isinstance(a, np.ndarray):
+            a = np.ascontiguousarray(a, dtype=dtype)
+            return a, _ptr(a), a.size
+        if a.is_cuda:
+            raise input_error("color_rsoc_csr takes host arrays")
+        return a, C.c_void_p(a.data_ptr()), a.numel()
+
+    off_keep, off_p, n1 = host_ptr(offsets, np.int64)
+    cols_keep, cols_p, m = host_ptr(adjacency, np.int32)
+    n = n1 - 1
+    if n < 0:
+        raise input_error("offsets must hold n + 1 entries")
+    cap = max(int(opt.round_cap), 1) + 1
+    cpr = np.zeros(min(cap, 1 << 16), dtype=np.uint64)
+    st = _lib.Stats()
+    st.conflicts_per_round = cpr.ctypes.data_as(C.POINTER(C.c_uint64))
+    st.cpr_cap = cpr.size
+    copt = opt.to_c(thread_count)
+    if colors_out is None:
+        out = np.empty(n, dtype=np.int32)
+        optr = _ptr(out)
+    elif isinstance(colors_out, np.ndarray):
+        out = colors_out
+        optr = _ptr(out)
+    else:  # CPU torch tensor (e.g. pinned)
+        out = colors_out
+        optr = C.c_void_p(out.data_ptr())
+    _check(LIB.gcol_cuda_color_rsoc_csr(off_p, cols_p, n, m, int(device), C.byref(copt), optr,
+                                        C.byref(st)))
+    del off_keep, cols_keep
+    return ColoringRun(out, _stats_from_c(st, cpr))
+
+
 def first_fit_sequential(g: Graph) -> np.ndarray:
     """coloring.hpp:110-116 on the device; bit-identical to the reference."""
     out = np.empty(g.num_vertices(), dtype=np.int32)

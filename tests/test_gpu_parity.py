@@ -273,3 +273,53 @@ def test_device_resident_graph_and_output():
     hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
     assert gcol.verify_coloring(hg, host).ok()
     assert run.stats.num_colors == gcol.count_colors(host)
+
+
+def test_streamed_host_csr_one_call():
+    """gcol_cuda_color_rsoc_csr: upload overlapped with the initial pass.
+    Same invariants as color_rsoc on a resident graph, on graphs spanning
+    many upload pieces (2M entries each) and on the edge shapes."""
+    rng = np.random.default_rng(4242)
+    for n, avg in ((1, 0.0), (2, 0.0), (5000, 6.0), (300_000, 30.0)):
+        g = random_graph(rng, n, avg)
+        run = gcol.color_rsoc_csr(g.offsets(), g.adjacency(), 16)
+        check_run(g, run, 16)
+    off, cols = graphs.make_config("rmat24", "cuda", scale_down=4)  # ~16.6M entries: 8 pieces
+    h_off, h_cols = off.cpu().pin_memory(), cols.cpu().pin_memory()
+    hg = gcol.Graph(h_off.numpy(), h_cols.numpy())
+    out = torch.empty(off.numel() - 1, dtype=torch.int32).pin_memory()
+    for prio in (gcol.Priority.degree_id, gcol.Priority.id_low):
+        run = gcol.color_rsoc_csr(h_off, h_cols, 1, gcol.ParallelOptions(priority=prio),
+                                  colors_out=out)
+        assert run.coloring is out
+        check_run(hg, gcol.ColoringRun(out.numpy(), run.stats), 1)
+
+
+def test_streamed_host_csr_rejects_bad_graphs():
+    off = np.array([0, 2, 1, 3], dtype=np.int64)  # not monotone
+    cols = np.array([1, 2, 0], dtype=np.int32)
+    with pytest.raises(gcol.input_error):
+        gcol.color_rsoc_csr(off, cols, 1)
+    with pytest.raises(gcol.input_error):  # offsets do not cover the adjacency
+        gcol.color_rsoc_csr(np.array([0, 1, 2], dtype=np.int64), np.array([1], dtype=np.int32), 1)
+    with pytest.raises(gcol.input_error):
+        gcol.color_rsoc_csr(np.array([0, 0], dtype=np.int64), np.zeros(0, dtype=np.int32), 0)
+
+
+def test_verify_rows_split_into_pieces(oracle_mod):
+    """Rows of degree >= 4096 are verified in pieces spread over the grid
+    (k_verify_big); counts and the ordered report must not change."""
+    rng = np.random.default_rng(123)
+    n = 30_000
+    hubs = [5, 17_000, 29_999]
+    edges = [(h, int(w)) for h in hubs for w in rng.choice(n, size=9000, replace=False) if w != h]
+    edges += [tuple(e) for e in rng.integers(0, n, size=(40_000, 2))]
+    g = gcol.build_graph(edges, n)
+    assert g.max_degree() >= 4096
+    for trial in range(3):
+        pal = rng.integers(-1 if trial == 2 else 0, 3, size=n).astype(np.int32)
+        want = oracle_mod.verify_coloring(oracle_csr(oracle_mod, g), pal)
+        got = gcol.verify_coloring(g, pal)
+        assert [(v.u, v.v, v.color) for v in got.violations] == want
+    run = gcol.color_rsoc(g, 4)
+    check_run(g, run, 4)
