@@ -375,7 +375,10 @@ def run_ours(args):
                    "m_directed": m, "max_degree": maxdeg, "priority": args.priority,
                    "parallelism": "replicas" if world > 1 else "single-gpu",
                    "l2": "flushed between timed iterations (512 MB write, untimed)"},
-        "colors": {"gpu": colors[-1], "gpu_all": sorted(set(colors)), "rounds": rounds[-1],
+        # RSOC is nondeterministic on both sides: the median of the timed runs is
+        # compared with the median of the reference's runs
+        "colors": {"gpu": sorted(colors)[(len(colors) - 1) // 2], "gpu_runs": colors,
+                   "rounds": rounds[-1],
                    "conflicts_total": last.conflicts_total,
                    "conflicts_per_round": last.conflicts_per_round,
                    "pairs_logged": last.pairs_logged,
@@ -401,7 +404,7 @@ def run_ours(args):
                       f"{threads} threads ({tmean * 1e3:.1f} ms each)"}
         line["colors"].update({"ref_rsoc_median": med, "ref_rsoc_all": ref_colors,
                                "serial_ff": serial_ff, "gate_1p05": math.floor(1.05 * med),
-                               "within_gate": colors[-1] <= math.floor(1.05 * med)})
+                               "within_gate": line["colors"]["gpu"] <= math.floor(1.05 * med)})
     if rank == 0:
         s = json.dumps(line)
         print(s, flush=True)

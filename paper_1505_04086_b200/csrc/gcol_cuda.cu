@@ -353,7 +353,9 @@ int plan_k1_cw(gcol_cuda_graph* g, int k1_blocks, int split_min, long long nitem
   const int bps = k1_blocks > 0 ? std::min(k1_blocks, occ) : 1;
   // small graphs: fewer CTAs, so the ~(32 CW) x CTAs vertices in flight stay
   // a small share of the graph (colour quality)
-  const long long want = std::max(1LL, nitems / (CW * 32 * 24LL));
+  long long per_cta = 24;  // chunks per CTA at least
+  if (const char* e = std::getenv("GCOL_K1_PER")) per_cta = std::max(1, std::atoi(e));
+  const long long want = std::max(1LL, nitems / (CW * 32 * per_cta));
   K->grid1 = static_cast<int>(std::min<long long>(g->sms * bps, want));
   K->cw = CW;
   K->smem = smem;

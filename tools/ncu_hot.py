@@ -15,7 +15,7 @@ h = rows[hi]
 data = [r for r in rows[hi + 1:] if len(r) == len(h)]
 ni = h.index("Warp Stall Sampling (All Samples)")
 si = h.index("Source")
-tot = sum(int(r[ni] or 0) for r in data) or 1
+tot = sum((int(r[ni]) if r[ni].strip().isdigit() else 0) for r in data) or 1
 print(len(data), "rows, samples", tot)
-for r in sorted(data, key=lambda r: -int(r[ni] or 0))[:N]:
-    print(f"{int(r[ni]):7d} {100 * int(r[ni]) / tot:5.1f}%  {r[si][:110]}")
+for r in sorted(data, key=lambda r: -(int(r[ni]) if r[ni].strip().isdigit() else 0))[:N]:
+    print(f"{(int(r[ni]) if r[ni].strip().isdigit() else 0):7d} {100 * (int(r[ni]) if r[ni].strip().isdigit() else 0) / tot:5.1f}%  {r[si][:110]}")

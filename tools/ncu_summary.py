@@ -19,6 +19,8 @@ def launches(path):
         if len(r) <= vi:
             continue
         name = r[ki].split("(")[0].replace("void ", "")
+        if not (name.startswith("gcol::") or "::k_" in name or name.startswith("k_")):
+            continue  # not ours (e.g. torch kernels of the graph generator)
         agg[name][0] += 1
         agg[name][1] += float(r[vi].replace(",", ""))
     tot = sum(t for _, t in agg.values())
