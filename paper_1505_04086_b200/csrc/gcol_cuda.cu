@@ -348,7 +348,7 @@ int plan_k1_cw(gcol_cuda_graph* g, int k1_blocks, int split_min, long long nitem
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   int occ = 1;
-  GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1, (CW + 1) * 32, smem));
+  GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1, (CW + k1_producers<CW>()) * 32, smem));
   if (occ < 1) occ = 1;
   const int bps = k1_blocks > 0 ? std::min(k1_blocks, occ) : 1;
   // small graphs: fewer CTAs, so the ~(32 CW) x CTAs vertices in flight stay
@@ -386,10 +386,10 @@ void launch_k1(const K1Launch& K, cudaStream_t stream, const long long* off, con
                int n, int nitems, const int* wl, const int* csrc, int* cdst, Ctrl* ctrl,
                int drift, int item0) {
   if (K.cw == kCWWide)
-    k1_pipe<kSnap, kLower, kLog, kCWWide><<<K.grid1, (kCWWide + 1) * 32, K.smem, stream>>>(
+    k1_pipe<kSnap, kLower, kLog, kCWWide><<<K.grid1, (kCWWide + k1_producers<kCWWide>()) * 32, K.smem, stream>>>(
         off, cols, n, nitems, wl, csrc, cdst, ctrl, K.L, K.S, drift, item0);
   else
-    k1_pipe<kSnap, kLower, kLog, kCW><<<K.grid1, (kCW + 1) * 32, K.smem, stream>>>(
+    k1_pipe<kSnap, kLower, kLog, kCW><<<K.grid1, (kCW + k1_producers<kCW>()) * 32, K.smem, stream>>>(
         off, cols, n, nitems, wl, csrc, cdst, ctrl, K.L, K.S, drift, item0);
 }
 
@@ -419,7 +419,7 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, bool wide
     p.func = K.cw == kCWWide ? reinterpret_cast<void*>(k1_pipe<false, kLower, true, kCWWide>)
                              : reinterpret_cast<void*>(k1_pipe<false, kLower, true, kCW>);
     p.gridDim = dim3(K.grid1);
-    p.blockDim = dim3((K.cw + 1) * 32);
+    p.blockDim = dim3((K.cw + (K.cw == kCWWide ? k1_producers<kCWWide>() : k1_producers<kCW>())) * 32);
     p.sharedMemBytes = static_cast<unsigned>(K.smem);
     p.kernelParams = args;
     GCOL_CK(cudaGraphAddKernelNode(&n_k1, graph, &n_ev0, 1, &p));

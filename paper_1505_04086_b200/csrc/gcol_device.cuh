@@ -135,19 +135,25 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // Warp-aggregated append of (u, v) observations: one atomicAdd per warp.
 // Must be called by all 32 lanes.
-__device__ __forceinline__ void log_pairs(const PairLog& L, bool pred, int u, int v) {
-  const unsigned m = __ballot_sync(kFull, pred);
-  if (!m) return;
+// The append itself is out of line: it is rare, and inlined at every call
+// site it would swell the K1 kernel past the instruction cache.
+__device__ __noinline__ void log_pairs_append(int2* region, int cap, int* s_count, int* overflow,
+                                              unsigned m, bool pred, int u, int v) {
   const int lane = lane_id();
   const int leader = __ffs(m) - 1;
   int base = 0;
-  if (lane == leader) base = atomicAdd(L.s_count, __popc(m));
+  if (lane == leader) base = atomicAdd(s_count, __popc(m));
   base = __shfl_sync(kFull, base, leader);
   if (pred) {
     const int idx = base + __popc(m & ((1u << lane) - 1u));
-    if (idx < L.cap) L.region[idx] = make_int2(u, v);
-    else *L.overflow = 1;
+    if (idx < cap) region[idx] = make_int2(u, v);
+    else *overflow = 1;
   }
+}
+
+__device__ __forceinline__ void log_pairs(const PairLog& L, bool pred, int u, int v) {
+  const unsigned m = __ballot_sync(kFull, pred);
+  if (m) log_pairs_append(L.region, L.cap, L.s_count, L.overflow, m, pred, u, v);
 }
 
 // Warp-aggregated append of ids to a list: one atomicAdd per warp.

@@ -29,10 +29,14 @@ namespace dev {
 
 constexpr int kCW = 8;                    // consumer warps per CTA (narrow variant)
 constexpr int kCWWide = 16;               // consumer warps per CTA (wide variant)
-constexpr int kPW = 1;                    // producer warp (TMA bulk copies)
-constexpr int kK1Threads = (kCW + kPW) * 32;
+// producer warps (TMA bulk copies, alternate chunks): the wide variant's
+// consumers outrun one producer
+template <int CW>
+constexpr int k1_producers() {
+  return CW > 8 ? 2 : 1;
+}
 constexpr int kChunk = kCW * 32;          // vertices per chunk (narrow); ranges align to it
-constexpr int kSlots = 4;                 // staged chunks in flight per CTA (multiple of kPW)
+constexpr int kSlots = 4;                 // staged chunks in flight per CTA (multiple of producers)
 constexpr int kSlotStage = 6144;          // adjacency entries staged per chunk (24 KB)
 constexpr int kBmWords = 512;             // per-warp medium-row bitmap pool
 constexpr int kStaleMax = 4;              // stale neighbours remembered per parked row
@@ -75,6 +79,7 @@ struct alignas(16) K1Slot {
   alignas(16) long long offs[CW * 32 + 2];  // contiguous mode: off[c0 .. c0 + rows]; worklist: b[]
   int wv[CW * 32];                     // worklist mode: vertex ids
   int aux[CW * 32];                    // worklist: degrees; contiguous: stage offset (-1: global)
+  unsigned lm[CW];                     // producer scratch: long-row bitmap
   alignas(16) int stage[stage_cap<CW>()];
   int chunk;                           // chunk index, -1: no more chunks
   int rows;
@@ -628,30 +633,33 @@ template <int CW>
 __device__ __forceinline__ void stage_chunk(K1Slot<CW>& sl, int rows, int min_deg,
                                             const int* __restrict__ cols, long long m,
                                             uint64_t pol) {
+  // Loops are kept rolled (long-row bitmap in shared memory): this runs once
+  // per chunk on one warp, and unrolled it would crowd the instruction cache.
   constexpr int R = CW;                  // rows per lane (kChunk / 32)
   constexpr int CAP = stage_cap<CW>();
   const int lane = lane_id();
-  unsigned lm[R];                        // long-row bitmap of the chunk, word t = rows t*32..
   int nl = 0;
-#pragma unroll
-  for (int t = 0; t < R; ++t) {
+#pragma unroll 1
+  for (int t = 0; t < R; ++t) {          // lm[t]: long rows among rows t*32 ..
     const int i = t * 32 + lane;
     const bool lg = min_deg != INT_MAX && i < rows && sl.offs[i + 1] - sl.offs[i] >= min_deg;
-    lm[t] = __ballot_sync(kFull, lg);
-    nl += __popc(lm[t]);
+    const unsigned w = __ballot_sync(kFull, lg);
+    if (lane == 0) sl.lm[t] = w;
+    nl += __popc(w);
   }
+  __syncwarp();
   // run j = rows [s_j, e_j): after the (j-1)-th long row, up to the j-th
   // (the last run, j == min(nl, 31), extends to `rows`)
   const int nr = min(nl, 31) + 1;
   auto nth_long = [&](int q) {           // row index of the q-th long row
-    int r = rows;
-#pragma unroll
+#pragma unroll 1
     for (int t = 0; t < R; ++t) {
-      const int p = __popc(lm[t]);
-      if (r == rows && q < p) r = t * 32 + (int)__fns(lm[t], 0, q + 1);
+      const unsigned w = sl.lm[t];
+      const int p = __popc(w);
+      if (q < p) return t * 32 + (int)__fns(w, 0, q + 1);
       q -= p;
     }
-    return r;
+    return rows;
   };
   int s = 0, e = 0;
   if (lane < nr) {
@@ -683,34 +691,22 @@ __device__ __forceinline__ void stage_chunk(K1Slot<CW>& sl, int rows, int min_de
     tma_load_1d(sl.stage + dst, cols + A, (unsigned)bulk * 4u, &sl.full);
   }
   for (int j = bulk; j < avail; ++j) sl.stage[dst + j] = ld_col(cols + A + j, pol);
-  // per-row stage offsets
-  if (nl == 0) {                         // one run: the common case
-    const long long A0 = __shfl_sync(kFull, A, 0);
-    const int r0 = __shfl_sync(kFull, avail, 0);
-#pragma unroll
-    for (int t = 0; t < R; ++t) {
-      const int i = t * 32 + lane;
-      if (i < rows) {
-        const long long b = sl.offs[i], bend = sl.offs[i + 1];
-        sl.aux[i] = bend - A0 <= r0 ? (int)(b - A0) : -1;
-      }
-    }
-    return;
-  }
+  // per-row stage offsets: row i lies in run (long rows before i), capped at 31
   int before = 0;                        // long rows before word t
-#pragma unroll
+#pragma unroll 1
   for (int t = 0; t < R; ++t) {
+    const unsigned w = sl.lm[t];
     const int i = t * 32 + lane;
-    const int run = min(before + __popc(lm[t] & ((1u << lane) - 1u)), 31);
+    const int run = min(before + __popc(w & ((1u << lane) - 1u)), 31);
     const long long Ar = __shfl_sync(kFull, A, run);
     const int dr = __shfl_sync(kFull, dst, run);
     const int rr = __shfl_sync(kFull, avail, run);
     if (i < rows) {
       const long long b = sl.offs[i], bend = sl.offs[i + 1];
-      const bool staged = !((lm[t] >> lane) & 1u) && bend - Ar <= rr;
+      const bool staged = !((w >> lane) & 1u) && bend - Ar <= rr;
       sl.aux[i] = staged ? dr + (int)(b - Ar) : -1;
     }
-    before += __popc(lm[t]);
+    before += __popc(w);
   }
 }
 
@@ -743,7 +739,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // rounds ahead of the slowest one.
 // ---------------------------------------------------------------------------
 template <bool kSnap, bool kLower, bool kLog, int CW>
-__global__ void __launch_bounds__((CW + 1) * 32, 1) k1_pipe(const long long* __restrict__ off,
+__global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(const long long* __restrict__ off,
                                                       const int* __restrict__ cols, int n,
                                                       int nitems, const int* worklist,
                                                       const int* csrc, int* cdst, Ctrl* ctrl,
@@ -793,10 +789,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) k1_pipe(const long long* __r
     const long long m = ld_off(off + n, pol);  // adjacency length
     // the first kSlots chunks' offsets; later ones are requested by the
     // consumer warp that frees the slot
+    constexpr int kPW = k1_producers<CW>();
+    const int pw = warp - kCW;  // this producer stages chunks k = pw (mod kPW)
     if (lane == 0 && contig)
-      for (int j = 0; j < kSlots; ++j)
+      for (int j = pw; j < kSlots; j += kPW)
         k1_request_offsets<CW>(sm.slot[j], off, blockIdx.x + j * G, nitems, item0, n, pol);
-    for (int k = 0;; ++k) {
+    for (int k = pw;; k += kPW) {
       const int c = blockIdx.x + k * G;
       const int si = k % kSlots;
       K1Slot<CW>& sl = sm.slot[si];
@@ -878,28 +876,27 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) k1_pipe(const long long* __r
   for (int k = 0;;) {
     // long-row pieces first (one call site)
     {
-      int pslot, pstart;
+      int pslot = 0, pstart = 0;
       bool ex;
-      if (k1_pop(S, &s_mbhead, pslot, pstart, &ex)) {
+      bool got = k1_pop(S, &s_mbhead, pslot, pstart, &ex);
+      if (!got && retired) {
+        int stop = 1;
+        if (S.min_deg != INT_MAX && lane == 0)
+          stop = ex && ld_acquire_u32(reinterpret_cast<const unsigned*>(S.alive)) == 0u;
+        if (!__shfl_sync(kFull, stop, 0)) {
+          __nanosleep(200);
+          continue;
+        }
+        if (S.min_deg == INT_MAX) break;
+        // alive hit 0 after the mailbox looked empty: one last look
+        got = k1_pop(S, &s_mbhead, pslot, pstart, &ex);
+        if (!got) break;
+      }
+      if (got) {
         const long long tp = clock64();
         k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L,
                                       gathers);
         ct_piece += clock64() - tp;
-        continue;
-      }
-      if (retired) {
-        int stop = 1;
-        if (S.min_deg != INT_MAX && lane == 0)
-          stop = ex && ld_acquire_u32(reinterpret_cast<const unsigned*>(S.alive)) == 0u;
-        if (__shfl_sync(kFull, stop, 0)) {
-          if (S.min_deg == INT_MAX) break;
-          // alive hit 0 after the mailbox looked empty: one last look
-          if (!k1_pop(S, &s_mbhead, pslot, pstart, &ex)) break;
-          k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L,
-                                        gathers);
-          continue;
-        }
-        __nanosleep(200);
         continue;
       }
     }
