@@ -365,7 +365,7 @@ int plan_k1_cw(gcol_cuda_graph* g, int k1_blocks, int split_min, long long nitem
   K->S = SplitArgs{P->nslots > 0 ? split_min : INT_MAX, P->d_slot_v, P->d_slot_deg,
                    P->d_slot_left, P->d_slot_bm, P->d_q, P->d_q_seq, P->d_ctr, P->d_ctr + 1,
                    reinterpret_cast<int*>(P->d_ctr + 2), K->grid1, P->d_ctr + 3,
-                   g->d_progress};
+                   g->d_progress, g->max_degree > 64 ? 1 : 0};
   const unsigned long long per = g->pair_cap / static_cast<unsigned long long>(K->grid1);
   K->L = PairLogArgs{g->d_pairs, static_cast<int>(std::min<unsigned long long>(per, 1u << 30)),
                      g->d_pair_counts, &g->d_ctrl->pair_overflow};

@@ -156,6 +156,25 @@ __device__ __forceinline__ void log_pairs(const PairLog& L, bool pred, int u, in
   if (m) log_pairs_append(L.region, L.cap, L.s_count, L.overflow, m, pred, u, v);
 }
 
+// The same log with the append inlined: for kernels whose register budget
+// cannot afford an out-of-line call (the wide K1, 96 registers per thread).
+struct PairLogInl : PairLog {};
+
+__device__ __forceinline__ void log_pairs(const PairLogInl& L, bool pred, int u, int v) {
+  const unsigned m = __ballot_sync(kFull, pred);
+  if (!m) return;
+  const int lane = lane_id();
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(L.s_count, __popc(m));
+  base = __shfl_sync(kFull, base, leader);
+  if (pred) {
+    const int idx = base + __popc(m & ((1u << lane) - 1u));
+    if (idx < L.cap) L.region[idx] = make_int2(u, v);
+    else *L.overflow = 1;
+  }
+}
+
 // Warp-aggregated append of ids to a list: one atomicAdd per warp.
 __device__ __forceinline__ void append_warp(int* list, int* len, bool pred, int v) {
   const unsigned m = __ballot_sync(kFull, pred);

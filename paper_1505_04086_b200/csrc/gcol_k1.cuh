@@ -22,6 +22,8 @@
 // rows are sorted, every edge is examined by its higher endpoint, and each
 // stale read that survives the re-check is logged for round 1.
 #pragma once
+#include <type_traits>
+
 #include "gcol_device.cuh"
 
 namespace gcol {
@@ -80,6 +82,8 @@ struct alignas(16) K1Slot {
   int wv[CW * 32];                     // worklist mode: vertex ids
   int aux[CW * 32];                    // worklist: degrees; contiguous: stage offset (-1: global)
   unsigned lm[CW];                     // producer scratch: long-row bitmap
+  long long wbase;                     // window mode (wlen >= 0): stage = cols[wbase, +wlen)
+  int wlen;
   alignas(16) int stage[stage_cap<CW>()];
   int chunk;                           // chunk index, -1: no more chunks
   int rows;
@@ -111,6 +115,7 @@ struct SplitArgs {
   int G;                // mailboxes (= K1 grid)
   unsigned* done_chunks;  // chunks fully consumed (drift bound)
   const unsigned long long* progress;  // streamed upload: adjacency entries resident (or null)
+  int dyn_tiles;        // 1: consumer warps take sub-tiles from a CTA counter
 };
 
 // First-Fit restricted to the colour window [wb, wb + 1024) (warp-wide);
@@ -155,10 +160,10 @@ __device__ __forceinline__ int row_of(int excl, int j) {
 // ---------------------------------------------------------------------------
 // small rows: thread per row over the staged adjacency, 64-bit register mask
 // ---------------------------------------------------------------------------
-template <bool kSnap, bool kLower, bool kLog>
+template <bool kSnap, bool kLower, bool kLog, class PL>
 __device__ __forceinline__ void k1_small(const int* __restrict__ cols, const int* csrc,
                                          int* cdst, int v, long long b, int deg, bool small,
-                                         K1Warp& W, int table, uint64_t pol, const PairLog& L,
+                                         K1Warp& W, int table, uint64_t pol, const PL& L,
                                          unsigned& gathers, const int* rs) {
   // rs: the row's entries in shared memory, nullptr when not staged
   const int lane = lane_id();
@@ -212,7 +217,8 @@ __device__ __forceinline__ void k1_small(const int* __restrict__ cols, const int
 // in-flight neighbours have all committed is committed now; otherwise it
 // gets one more sub-tile in the lane's carry slot, and whatever is still
 // uncoloured at that second check is logged for round 1.
-__device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const PairLog& L) {
+template <class PL>
+__device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const PL& L) {
   const int lane = lane_id();
   // (1) carry slot: final check
   {
@@ -280,10 +286,10 @@ __device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const 
 // an in-flight lower neighbour is not committed: its id goes to `redo`, and
 // one sub-tile later the whole row is recomputed in log mode.
 // ---------------------------------------------------------------------------
-template <bool kSnap, bool kLower, bool kLog>
+template <bool kSnap, bool kLower, bool kLog, class PL>
 __device__ __forceinline__ void k1_medium(const int* __restrict__ cols, const int* csrc,
                                           int* cdst, int v, long long b, int deg, bool med,
-                                          K1Warp& W, uint64_t pol, const PairLog& L,
+                                          K1Warp& W, uint64_t pol, const PL& L,
                                           unsigned& gathers, int* redo, int* nredo,
                                           const int* stage, int so) {
   // so: offset of the row's entries in `stage`, -1 when not staged
@@ -480,10 +486,10 @@ __device__ bool k1_pop(const SplitArgs& S, int* s_mbhead, int& slot, int& start,
   return ok != 0;
 }
 
-template <bool kSnap, bool kLower, bool kLog>
+template <bool kSnap, bool kLower, bool kLog, class PL>
 __device__ __forceinline__ void k1_piece(const long long* __restrict__ off, const int* __restrict__ cols,
                          const int* csrc, int* cdst, const SplitArgs& S, int slot, int start,
-                         K1Warp& W, uint64_t pol, const PairLog& L, unsigned& gathers) {
+                         K1Warp& W, uint64_t pol, const PL& L, unsigned& gathers) {
   constexpr int U = 8;
   const int lane = lane_id();
   const int v = S.slot_v[slot];
@@ -751,7 +757,7 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
   K1Smem<CW>& sm = *reinterpret_cast<K1Smem<CW>*>(k1_raw);
   __shared__ int s_ready[kSlots];
   __shared__ int s_consumed[kSlots];
-  __shared__ int s_npairs, s_mbhead;
+  __shared__ int s_npairs, s_mbhead, s_next;
   __shared__ unsigned s_gathers;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const uint64_t pol = policy_evict_first();
@@ -768,6 +774,7 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
     s_npairs = 0;
     s_gathers = 0;
     s_mbhead = 0;
+    s_next = 0;
   }
   if (warp < kCW) {
     K1Warp& W = sm.cw[warp];
@@ -825,13 +832,32 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
             while (ld_acquire_u64(S.progress) < need) __nanosleep(256);
           __syncwarp();
         }
-        stage_chunk<CW>(sl, rows, S.min_deg, cols, m, pol);
-        if (lane == 0) {
-          sl.rows = rows;
-          sl.chunk = c;
+        if (S.min_deg == INT_MAX) {
+          // no long rows in the graph: the chunk's adjacency is one run, staged
+          // as one window [wbase, wbase + wlen); rows inside it read shared memory
+          if (lane == 0) {
+            constexpr int CAP = stage_cap<CW>();
+            const long long A = sl.offs[0] & ~3LL;
+            const int len = (int)min(sl.offs[rows] - A, (long long)CAP);
+            const int bulk = A + ((len + 3) & ~3) <= m ? ((len + 3) & ~3) : (len & ~3);
+            for (int x = bulk; x < len; ++x) sl.stage[x] = ld_col(cols + A + x, pol);
+            sl.wbase = A;
+            sl.wlen = len;
+            sl.rows = rows;
+            sl.chunk = c;
+            mbar_arrive_expect_tx(&sl.full, (unsigned)bulk * 4u);
+            if (bulk) tma_load_1d(sl.stage, cols + A, (unsigned)bulk * 4u, &sl.full);
+          }
+        } else {
+          stage_chunk<CW>(sl, rows, S.min_deg, cols, m, pol);
+          if (lane == 0) {
+            sl.wlen = -1;  // per-row offsets in aux[]
+            sl.rows = rows;
+            sl.chunk = c;
+          }
+          __syncwarp();  // every lane's expect_tx, tails and aux[] before the arrive
+          if (lane == 0) mbar_arrive(&sl.full);
         }
-        __syncwarp();  // every lane's expect_tx, tails and aux[] before the arrive
-        if (lane == 0) mbar_arrive(&sl.full);
       } else {  // worklist mode: per-row loads, nothing staged
         if (k >= kSlots)
           while (*reinterpret_cast<volatile int*>(&s_consumed[si]) < kCW * (k / kSlots))
@@ -866,14 +892,29 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
 
   // ------------------------------- consumers ---------------------------------
   K1Warp& W = sm.cw[warp];
-  PairLog L{LA.pairs + (size_t)blockIdx.x * LA.region_cap, LA.region_cap, &s_npairs, LA.overflow};
+  // the wide variant inlines the rare log append (register budget), the
+  // narrow one keeps it out of line (instruction-cache footprint)
+  using PL = typename std::conditional<(CW > dev::kCW), PairLogInl, PairLog>::type;
+  PL L;
+  L.region = LA.pairs + (size_t)blockIdx.x * LA.region_cap;
+  L.cap = LA.region_cap;
+  L.s_count = &s_npairs;
+  L.overflow = LA.overflow;
   unsigned gathers = 0;
   bool finished = false;  // no more chunks for this warp
   bool retired = false;   // decremented S.alive
   long long ct_wait = 0, ct_piece = 0, ct_small = 0, ct_med = 0, ct_drain = 0, cchunks = 0;
   long long ct_redo = 0, n_med = 0, n_redo = 0;
   long long tw = clock64();
-  for (int k = 0;;) {
+  // Sub-tile t is rows [32 (t mod CW), +32) of chunk k = t / CW.  Statically,
+  // warp w takes t = w, w + CW, ...; with dyn_tiles (skewed degrees, where
+  // sub-tile costs vary widely) warps take them in ascending order from a CTA
+  // counter, so a slow sub-tile holds up only itself and the warps' current
+  // rows always lie within two consecutive chunks.
+  int t = -1;    // sub-tile taken and not finished (-1: none)
+  int cnt = 0;   // sub-tiles finished by this warp: parity picks the park tables
+  int k = 0, si = 0;
+  for (;;) {
     // long-row pieces first (one call site)
     {
       int pslot = 0, pstart = 0;
@@ -900,8 +941,19 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
         continue;
       }
     }
-    const int si = k % kSlots;
+    int j = 0;
     if (!finished) {
+      if (t < 0) {
+        if (S.dyn_tiles) {
+          if (lane == 0) t = atomicAdd(&s_next, 1);
+          t = __shfl_sync(kFull, t, 0);
+        } else {
+          t = cnt * kCW + warp;
+        }
+      }
+      k = t / kCW;
+      j = t - k * kCW;
+      si = k % kSlots;
       int ok = 0;
       if (lane == 0) ok = mbar_try_wait(&sm.slot[si].full, (unsigned)((k / kSlots) & 1));
       if (!__shfl_sync(kFull, ok, 0)) {
@@ -913,7 +965,7 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
     long long ta = clock64();
     ct_wait += ta - tw;
     const K1Slot<CW>& sl = sm.slot[si];
-    const int i = warp * 32 + lane;
+    const int i = j * 32 + lane;
     const bool valid = !finished && i < sl.rows;
     int v = -1, deg = 0;
     long long b = 0;
@@ -928,8 +980,12 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
         deg = (int)(sl.offs[i + 1] - b);
       }
     }
-    const int so = (valid && !worklist) ? sl.aux[i] : -1;  // stage offset of the row
-    const int table = k & 1;
+    int so = -1;  // stage offset of the row's entries, -1: global memory
+    if (valid && !worklist) {
+      if (sl.wlen >= 0) so = b >= sl.wbase && b + deg <= sl.wbase + sl.wlen ? (int)(b - sl.wbase) : -1;
+      else so = sl.aux[i];
+    }
+    const int table = cnt & 1;
     if (valid && deg == 0) st_color(cdst + v, 0);  // limit 0: only colour 0
     k1_push_long(S, v, deg, valid && deg >= S.min_deg);
     k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg,
@@ -984,7 +1040,8 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
                                    item0, n, pol);
         }
       }
-      ++k;
+      t = -1;
+      ++cnt;
     } else {
       retired = true;
       if (lane == 0 && S.min_deg != INT_MAX) atomicSub(S.alive, 1);
