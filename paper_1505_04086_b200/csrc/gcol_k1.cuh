@@ -31,11 +31,11 @@ namespace dev {
 
 constexpr int kCW = 8;                    // consumer warps per CTA (narrow variant)
 constexpr int kCWWide = 16;               // consumer warps per CTA (wide variant)
-// producer warps (TMA bulk copies, alternate chunks): the wide variant's
-// consumers outrun one producer
+// producer warps (TMA bulk copies, alternate chunks); one keeps up with
+// both variants since the single-window staging
 template <int CW>
 constexpr int k1_producers() {
-  return CW > 8 ? 2 : 1;
+  return 1;
 }
 constexpr int kChunk = kCW * 32;          // vertices per chunk (narrow); ranges align to it
 constexpr int kSlots = 4;                 // staged chunks in flight per CTA (multiple of producers)
