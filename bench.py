@@ -54,6 +54,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--report", default="", help="also write the JSON line to this path")
+    p.add_argument("--exchange", default="push", choices=["push", "nccl"],
+                   help="multi-GPU: peer pushes inside the kernels (product) or NCCL at round "
+                        "boundaries (baseline)")
     p.add_argument("--distributed", action="store_true",
                    help="use the partitioned multi-GPU path even at N=1 (testing)")
     return p.parse_args()
@@ -230,6 +233,13 @@ def run_distributed(args):
     import torch
     import torch.distributed as dist
     rank, world, local = dist_env()
+    if "RANK" not in os.environ:  # --distributed outside torchrun: a world of one
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ.update({"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0",
+                           "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(sk.getsockname()[1])})
+        sk.close()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1505_04086_b200 import dist as gdist, gcol
@@ -242,6 +252,9 @@ def run_distributed(args):
                                                    k1_blocks_per_sm=args.k1_blocks_per_sm))
     colors = torch.empty(n, dtype=torch.int32, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    push = args.exchange == "push"
+    if push:  # peers' replicas mapped into this process (CUDA IPC over NVLink)
+        peer_ptrs, unmap = gdist.map_peer_replicas(ops, colors, rank, world)
 
     def step():
         colors.fill_(-1)
@@ -250,7 +263,10 @@ def run_distributed(args):
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        st = gdist.color_rsoc_distributed(ops, colors, n, rank, world)
+        if push:
+            st = gdist.color_rsoc_partitioned(ops, colors, n, rank, world, peer_ptrs)
+        else:
+            st = gdist.color_rsoc_distributed(ops, colors, n, rank, world)
         e1.record()
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
@@ -276,8 +292,11 @@ def run_distributed(args):
             "dtype": "int32", "data": "synthetic",
             "config": {"workload": CONFIG_WORKLOAD[args.config], "config": args.config, "n": n,
                        "m_directed": m, "priority": args.priority,
-                       "parallelism": f"1-D vertex partition x{world}, replicated colours, "
-                                      "per-round NCCL delta exchange",
+                       "parallelism": (f"interleaved 256-id chunks x{world}, replicated colours, "
+                                       "commits pushed to peer replicas over NVLink (CUDA IPC), "
+                                       "round counts all-reduced") if push else
+                                      (f"1-D vertex partition x{world}, replicated colours, "
+                                       "per-round NCCL delta exchange"),
                        "l2": "flushed between timed iterations (512 MB write, untimed)"},
             "colors": {"gpu": ncol, "rounds": st.rounds,
                        "conflicts_per_round": st.conflicts_per_round,
@@ -289,6 +308,9 @@ def run_distributed(args):
         if args.report:
             with open(args.report, "w") as f:
                 f.write(json.dumps(line) + "\n")
+    if push:
+        dist.barrier()
+        unmap()
     dist.destroy_process_group()
     return 0
 

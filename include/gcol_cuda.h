@@ -217,11 +217,46 @@ int gcol_cuda_count_colors(gcol_cuda_graph* g, const int32_t* colors, int64_t nc
                            int32_t memory, uint32_t* num_colors);
 
 /* ---- Multi-GPU building blocks (one process and one handle per GPU) ----
- * A 1-D partition of vertex ids: each rank owns [lo, hi) and keeps a full
- * replica of the colour array on its device.  All pointers are device
- * pointers on the handle's device.  The host orchestration (exchange of
- * owned slices and per-round (id, colour) deltas over NCCL, global
- * termination) is paper_1505_04086_b200/dist.py. */
+ * Every rank keeps a full replica of the colour array on its device.  All
+ * pointers are device pointers on the handle's device.  The host
+ * orchestration is paper_1505_04086_b200/dist.py.
+ *
+ * Push mode (the product): ids are dealt out in 256-id
+ * chunks, chunk c to rank c mod world, so all GPUs sweep the ids in one
+ * ascending front; every colour a rank commits (initial pass and rounds)
+ * is stored into its own replica AND into every peer's replica through
+ * peer-mapped memory (NVLink), so other GPUs see it within the round. */
+
+/* Registers this GPU as `rank` of `world` (<= 8) with the peers' replicas
+ * (world device pointers, mapped into this process, e.g. by CUDA IPC;
+ * entry `rank` is ignored).  Used by k1_owned and round_list. */
+int gcol_cuda_partition_set(gcol_cuda_graph* g, int32_t rank, int32_t world,
+                            int32_t* const* peer_colors);
+
+/* Peer mapping of a replica between processes (CUDA IPC): export gives the
+ * 64-byte handle of the allocation holding dev_ptr and dev_ptr's offset in
+ * it; import maps a peer's handle into this process (peer access enabled)
+ * and returns base + offset; close unmaps it. */
+int gcol_cuda_ipc_export(const void* dev_ptr, uint8_t handle_out[64], uint64_t* offset_out);
+int gcol_cuda_ipc_import(const uint8_t handle[64], uint64_t offset, void** dev_ptr_out);
+int gcol_cuda_ipc_close(void* dev_ptr, uint64_t offset);
+
+/* Initial pass over the owned chunks, in place on colors_dev, pushing every
+ * committed colour to the peers.  Call after every replica is initialised
+ * to -1 (barrier). */
+int gcol_cuda_k1_owned(gcol_cuda_graph* g, const gcol_cuda_options* opt, int32_t* colors_dev,
+                       gcol_cuda_stats* stats);
+
+/* Round-1 candidates from the observation log of the last k1_owned: the
+ * losers (under `priority`) of logged pairs whose colours are now equal,
+ * owned or not -> cand_out (device, capacity n), count in *ncand.  Call
+ * after every rank's k1_owned has completed (barrier), so the remote
+ * endpoints' colours have arrived. */
+int gcol_cuda_candidates(gcol_cuda_graph* g, int32_t priority, const int32_t* colors_dev,
+                         int32_t* cand_out, int64_t* ncand);
+
+/* Baseline mode (contiguous ranges, NCCL exchange at round boundaries):
+ * each rank owns [lo, hi). */
 
 /* Initial pass (K1) over the owned rows [lo, hi) in place on colors_dev
  * (lo a multiple of 256).  Colours of rows outside the range are read as
@@ -235,7 +270,8 @@ int gcol_cuda_detect_range(gcol_cuda_graph* g, int32_t priority, const int32_t* 
                            int64_t lo, int64_t hi, int32_t* out_dev, int64_t* nout);
 
 /* One fused detect-and-recolor round over a device worklist, in place on
- * colors_dev; recoloured ids -> out_dev (capacity nin), count in *nout. */
+ * colors_dev; recoloured ids -> out_dev (capacity nin), count in *nout.
+ * After gcol_cuda_partition_set the recolours are pushed to the peers. */
 int gcol_cuda_round_list(gcol_cuda_graph* g, int32_t priority, int32_t* colors_dev,
                          const int32_t* in_dev, int64_t nin, int32_t* out_dev, int64_t* nout);
 

@@ -109,6 +109,12 @@ SIGNATURES = {
     "gcol_cuda_verify_coloring": (C.c_int, [_vp, _vp, _i64, _i32, C.POINTER(VerifyReport), _vp,
                                             _vp, _vp, _i64]),
     "gcol_cuda_count_colors": (C.c_int, [_vp, _vp, _i64, _i32, C.POINTER(C.c_uint32)]),
+    "gcol_cuda_ipc_export": (C.c_int, [_vp, _vp, C.POINTER(C.c_uint64)]),
+    "gcol_cuda_ipc_import": (C.c_int, [_vp, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "gcol_cuda_ipc_close": (C.c_int, [_vp, C.c_uint64]),
+    "gcol_cuda_partition_set": (C.c_int, [_vp, _i32, _i32, _vp]),
+    "gcol_cuda_k1_owned": (C.c_int, [_vp, C.POINTER(Options), _vp, C.POINTER(Stats)]),
+    "gcol_cuda_candidates": (C.c_int, [_vp, _i32, _vp, _vp, C.POINTER(C.c_int64)]),
     "gcol_cuda_k1_range": (C.c_int, [_vp, C.POINTER(Options), _vp, _i64, _i64, C.POINTER(Stats)]),
     "gcol_cuda_detect_range": (C.c_int, [_vp, _i32, _vp, _i64, _i64, _vp, C.POINTER(_i64)]),
     "gcol_cuda_round_list": (C.c_int, [_vp, _i32, _vp, _vp, _i64, _vp, C.POINTER(_i64)]),

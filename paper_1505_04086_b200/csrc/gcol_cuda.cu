@@ -129,6 +129,12 @@ struct gcol_cuda_graph {
   int nvrows = 0;
   int* d_vrows = nullptr;
   int* d_vpre = nullptr;  // [nvrows + 1] piece prefix
+  // multi-GPU partition (gcol_cuda_partition_set): interleaved 256-id chunks,
+  // chunk c owned by rank c mod world; peers = the other GPUs' replicas
+  int part_rank = 0, part_world = 1;
+  PeerSet peers{};
+  int owned_k1_grid = 0;        // last gcol_cuda_k1_owned launch: its log slices
+  PairLogArgs owned_k1_log{};
   // colour copy-out to pinned host memory, overlapped with verification
   cudaStream_t out_stream = nullptr;
   cudaEvent_t ev_final = nullptr;
@@ -365,7 +371,7 @@ int plan_k1_cw(gcol_cuda_graph* g, int k1_blocks, int split_min, long long nitem
   K->S = SplitArgs{P->nslots > 0 ? split_min : INT_MAX, P->d_slot_v, P->d_slot_deg,
                    P->d_slot_left, P->d_slot_bm, P->d_q, P->d_q_seq, P->d_ctr, P->d_ctr + 1,
                    reinterpret_cast<int*>(P->d_ctr + 2), K->grid1, P->d_ctr + 3,
-                   g->d_progress, g->max_degree > 64 ? 1 : 0};
+                   g->d_progress, g->max_degree > 64 ? 1 : 0, 1, 0};
   const unsigned long long per = g->pair_cap / static_cast<unsigned long long>(K->grid1);
   K->L = PairLogArgs{g->d_pairs, static_cast<int>(std::min<unsigned long long>(per, 1u << 30)),
                      g->d_pair_counts, &g->d_ctrl->pair_overflow};
@@ -724,6 +730,62 @@ int gcol_cuda_device_count(int32_t* count) {
   if (e != cudaSuccess) c = 0;
   if (count) *count = c;
   if (c == 0) return fail(GCOL_ERR_NO_DEVICE, "no CUDA device available");
+  return GCOL_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+using GetAddressRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+GetAddressRangeFn get_address_range() {
+  static GetAddressRangeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+    return reinterpret_cast<GetAddressRangeFn>(p);
+  }();
+  return fn;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gcol_cuda_ipc_export(const void* dev_ptr, uint8_t handle_out[64], uint64_t* offset_out) {
+  if (!dev_ptr || !handle_out || !offset_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "ipc_export: null");
+  GetAddressRangeFn range = get_address_range();
+  if (!range) return fail(GCOL_ERR_CUDA, "ipc_export: cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "ipc_export: not a device allocation");
+  cudaIpcMemHandle_t h;
+  GCOL_CK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  static_assert(sizeof h == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle_out, &h, sizeof h);
+  *offset_out = static_cast<uint64_t>(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return GCOL_OK;
+}
+
+int gcol_cuda_ipc_import(const uint8_t handle[64], uint64_t offset, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "ipc_import: null");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  void* base = nullptr;
+  GCOL_CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *dev_ptr_out = static_cast<char*>(base) + offset;
+  return GCOL_OK;
+}
+
+int gcol_cuda_ipc_close(void* dev_ptr, uint64_t offset) {
+  if (!dev_ptr) return GCOL_OK;
+  GCOL_CK(cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - offset));
   return GCOL_OK;
 }
 
@@ -1387,6 +1449,118 @@ int gcol_cuda_k1_range(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, int3
   return GCOL_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Peer pushes on (the handle's partition) or off, in stream order.
+int set_peers(gcol_cuda_graph* g, bool on) {
+  static const PeerSet none{};
+  GCOL_CK(cudaMemcpyToSymbolAsync(c_peers, on ? &g->peers : &none, sizeof(PeerSet), 0,
+                                  cudaMemcpyHostToDevice, g->stream));
+  return GCOL_OK;
+}
+
+template <int R>
+void launch_candidates(gcol_cuda_graph* g, const K1Launch& K, const int* colors) {
+  k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, static_cast<int>(g->n),
+                                                         colors, g->d_ctrl, K.L, K.grid1, g->d_marks);
+}
+
+}  // namespace
+
+extern "C" {
+
+int gcol_cuda_partition_set(gcol_cuda_graph* g, int32_t rank, int32_t world,
+                            int32_t* const* peer_colors) {
+  if (int rc = check_graph(g)) return rc;
+  if (world < 1 || world > kMaxPeers + 1 || rank < 0 || rank >= world)
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "partition: need 1 <= world <= 8, 0 <= rank < world");
+  if (world > 1 && !peer_colors) return fail(GCOL_ERR_INVALID_ARGUMENT, "partition: peer_colors is null");
+  PeerSet ps{};
+  for (int q = 0; q < world; ++q) {
+    if (q == rank) continue;
+    if (!peer_colors[q]) return fail(GCOL_ERR_INVALID_ARGUMENT, "partition: null peer replica");
+    ps.ptr[ps.n++] = peer_colors[q];
+  }
+  g->part_rank = rank;
+  g->part_world = world;
+  g->peers = ps;
+  return GCOL_OK;
+}
+
+int gcol_cuda_k1_owned(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, int32_t* colors_dev,
+                       gcol_cuda_stats* stats) {
+  if (int rc = check_graph(g)) return rc;
+  gcol_cuda_options opt;
+  if (int rc = read_options(opt_in, &opt)) return rc;
+  if (!colors_dev) return fail(GCOL_ERR_INVALID_ARGUMENT, "k1_owned: colors_dev is null");
+  GCOL_CK(cudaSetDevice(g->device));
+  if (int rc = ensure_run_buffers(g)) return rc;
+  K1Launch K;
+  if (int rc = plan_k1<false, true, true>(g, opt.k1_blocks_per_sm, split_min_of(opt), &K, false))
+    return rc;
+  K.S.cstride = g->part_world;
+  K.S.coffset = g->part_rank;
+  const int n = static_cast<int>(g->n);
+  if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, nullptr, 0)) return rc;
+  if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
+  if (int rc = set_peers(g, true)) return rc;
+  GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
+  if (n > 0)
+    launch_k1<false, true, true>(K, g->stream, g->d_off, g->d_cols, n, n, nullptr, colors_dev,
+                                 colors_dev, g->d_ctrl, drift_rounds(g), 0);
+  GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
+  GCOL_CK(cudaGetLastError());
+  if (int rc = set_peers(g, false)) return rc;
+  g->owned_k1_grid = K.grid1;  // the log's slices, for gcol_cuda_candidates
+  g->owned_k1_log = K.L;
+  Ctrl hdr;
+  GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  if (stats) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g->ev_start, g->ev_k1);
+    stats->initial_pass_ns = static_cast<uint64_t>(static_cast<double>(ms) * 1e6);
+    stats->pairs_logged = hdr.pair_len;
+    stats->pair_overflow = static_cast<uint32_t>(hdr.pair_overflow);
+    stats->k1_gathers = hdr.k1_gathers;
+  }
+  return GCOL_OK;
+}
+
+int gcol_cuda_candidates(gcol_cuda_graph* g, int32_t priority, const int32_t* colors_dev,
+                         int32_t* cand_out, int64_t* ncand) {
+  if (int rc = check_graph(g)) return rc;
+  if (priority == GCOL_PRIORITY_DEFAULT) priority = GCOL_PRIORITY_DEGREE_ID;
+  if (priority < GCOL_PRIORITY_ID_LOW || priority > GCOL_PRIORITY_ORDERED)
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "unknown priority rule");
+  if (!colors_dev || !cand_out || !ncand) return fail(GCOL_ERR_INVALID_ARGUMENT, "candidates: null buffer");
+  if (g->owned_k1_grid <= 0) return fail(GCOL_ERR_INVALID_ARGUMENT, "candidates: run k1_owned first");
+  GCOL_CK(cudaSetDevice(g->device));
+  // keep the log and its overflow flag; point the worklist at cand_out
+  int* list = cand_out;
+  const int zero = 0;
+  GCOL_CK(cudaMemcpyAsync(&g->d_ctrl->in_list, &list, sizeof list, cudaMemcpyHostToDevice, g->stream));
+  GCOL_CK(cudaMemcpyAsync(&g->d_ctrl->in_len, &zero, sizeof zero, cudaMemcpyHostToDevice, g->stream));
+  GCOL_CK(cudaMemsetAsync(g->d_marks, 0, sizeof(int) * static_cast<size_t>(g->n), g->stream));
+  K1Launch K;
+  K.grid1 = g->owned_k1_grid;
+  K.L = g->owned_k1_log;
+  if (g->n > 0) {
+    const int r = rule_of(priority);
+    if (r == kIdLow) launch_candidates<kIdLow>(g, K, colors_dev);
+    else if (r == kIdHigh || r == kOrdered) launch_candidates<kIdHigh>(g, K, colors_dev);
+    else launch_candidates<kDegId>(g, K, colors_dev);
+  }
+  GCOL_CK(cudaGetLastError());
+  int len = 0;
+  GCOL_CK(cudaMemcpyAsync(&len, &g->d_ctrl->in_len, sizeof len, cudaMemcpyDeviceToHost, g->stream));
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  *ncand = len;
+  return GCOL_OK;
+}
+
 int gcol_cuda_detect_range(gcol_cuda_graph* g, int32_t priority, const int32_t* colors_dev,
                            int64_t lo, int64_t hi, int32_t* out_dev, int64_t* nout) {
   if (int rc = check_graph(g)) return rc;
@@ -1425,6 +1599,7 @@ int gcol_cuda_round_list(gcol_cuda_graph* g, int32_t priority, int32_t* colors_d
   if (int rc = ensure_run_buffers(g)) return rc;
   if (int rc = reset_ctrl(g, 1, const_cast<int*>(in_dev), out_dev, nullptr, static_cast<int>(nin)))
     return rc;
+  if (int rc = set_peers(g, true)) return rc;  // recolours reach the peers' replicas
   if (nin > 0) {
     const int r = rule_of(priority);
     if (r == kIdLow) {
@@ -1439,6 +1614,7 @@ int gcol_cuda_round_list(gcol_cuda_graph* g, int32_t priority, int32_t* colors_d
     }
   }
   GCOL_CK(cudaGetLastError());
+  if (int rc = set_peers(g, false)) return rc;
   Ctrl hdr;
   GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
   GCOL_CK(cudaStreamSynchronize(g->stream));

@@ -124,6 +124,33 @@ __device__ __forceinline__ void st_color(int* p, int v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
+// Multi-GPU: every GPU keeps a full replica of the
+// colours; a partitioned run commits each colour to the local replica and
+// pushes it into every peer's replica (peer-mapped HBM over NVLink), so the
+// other GPUs see it within the round.  Empty (n = 0) outside partitioned
+// runs; set per launch by the host (stream-ordered symbol copy).
+constexpr int kMaxPeers = 7;  // 8 GPUs per node
+struct PeerSet {
+  int* ptr[kMaxPeers];        // peer replicas (this GPU's own excluded)
+  int n;
+};
+__constant__ PeerSet c_peers;
+
+__device__ __forceinline__ void st_color_sys(int* p, int v) {
+  asm volatile("st.relaxed.sys.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void commit_color(int* base, int v, int c) {
+  st_color(base + v, c);
+  const int np = c_peers.n;
+  for (int q = 0; q < np; ++q) st_color_sys(c_peers.ptr[q] + v, c);
+}
+
+// Before a pushing kernel's threads exit: their peer stores are performed.
+__device__ __forceinline__ void peers_fence() {
+  if (c_peers.n) __threadfence_system();
+}
+
 // kSnap: snapshot mode reads a frozen, never-written array with plain loads.
 template <bool kSnap>
 __device__ __forceinline__ int read_color(const int* c, int w) {

@@ -116,6 +116,8 @@ struct SplitArgs {
   unsigned* done_chunks;  // chunks fully consumed (drift bound)
   const unsigned long long* progress;  // streamed upload: adjacency entries resident (or null)
   int dyn_tiles;        // 1: consumer warps take sub-tiles from a CTA counter
+  int cstride, coffset; // this launch owns the chunks coffset + cstride * i (interleaved
+                        // multi-GPU partition; 1, 0: all)
 };
 
 // First-Fit restricted to the colour window [wb, wb + 1024) (warp-wide);
@@ -207,7 +209,7 @@ __device__ __forceinline__ void k1_small(const int* __restrict__ cols, const int
       W.ddeg[table][lane] = (unsigned char)deg;
       W.dns[table][lane] = (unsigned char)min(ns, kStaleMax);
     } else {
-      st_color(cdst + v, __ffsll((long long)~mask) - 1);
+      commit_color(cdst, v, __ffsll((long long)~mask) - 1);
     }
   }
   __syncwarp();
@@ -242,7 +244,7 @@ __device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const 
       log_pairs(L, k < ns && c[k] == -1, u[k], v);  // still in flight: round 1 checks it
     }
     if (v >= 0) {
-      st_color(cdst + v, __ffsll((long long)~mask) - 1);
+      commit_color(cdst, v, __ffsll((long long)~mask) - 1);
       W.cv[lane] = -1;
     }
   }
@@ -266,7 +268,7 @@ __device__ __forceinline__ void k1_drain(K1Warp& W, int table, int* cdst, const 
       if (k < ns && c[k] == -1) W.cst[lane][left++] = u[k];
     }
     if (left == 0) {
-      st_color(cdst + v, __ffsll((long long)~mask) - 1);
+      commit_color(cdst, v, __ffsll((long long)~mask) - 1);
     } else {  // second chance
       W.cv[lane] = v;
       W.cmask[lane][0] = (unsigned)mask;
@@ -394,7 +396,7 @@ __device__ __forceinline__ void k1_medium(const int* __restrict__ cols, const in
       __syncwarp();
       if (lane == 0) *nredo += __popc(pm);
     }
-    if (inb && !park) st_color(cdst + v, color);
+    if (inb && !park) commit_color(cdst, v, color);
     __syncwarp();
   }
 }
@@ -552,7 +554,7 @@ __device__ __forceinline__ void k1_piece(const long long* __restrict__ off, cons
       for (int wb = 1024; color < 0 && wb <= deg; wb += 1024)
         color = warp_ff_window<kSnap, kLower>(cols, csrc, v, b, deg, wb, W.win, pol);
     }
-    if (lane == 0) st_color(cdst + v, color);
+    if (lane == 0) commit_color(cdst, v, color);
   }
   __syncwarp();
 }
@@ -762,7 +764,9 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const uint64_t pol = policy_evict_first();
   const int G = gridDim.x;
-  const int nchunks = (nitems + kChunk - 1) / kChunk;
+  const int nchunks_all = (nitems + kChunk - 1) / kChunk;
+  // chunks of this launch: global chunk coffset + cstride * local index
+  const int nchunks = nchunks_all > S.coffset ? (nchunks_all - S.coffset + S.cstride - 1) / S.cstride : 0;
   if (threadIdx.x < kSlots) {
     s_ready[threadIdx.x] = -1;
     s_consumed[threadIdx.x] = 0;
@@ -800,14 +804,16 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
     const int pw = warp - kCW;  // this producer stages chunks k = pw (mod kPW)
     if (lane == 0 && contig)
       for (int j = pw; j < kSlots; j += kPW)
-        k1_request_offsets<CW>(sm.slot[j], off, blockIdx.x + j * G, nitems, item0, n, pol);
+        k1_request_offsets<CW>(sm.slot[j], off, (blockIdx.x + j * G) * S.cstride + S.coffset,
+                               nitems, item0, n, pol);
     for (int k = pw;; k += kPW) {
-      const int c = blockIdx.x + k * G;
+      const int cl = blockIdx.x + k * G;                // local chunk index
+      const int c = cl * S.cstride + S.coffset;         // global chunk index
       const int si = k % kSlots;
       K1Slot<CW>& sl = sm.slot[si];
       const unsigned par = (unsigned)((k / kSlots) & 1);
       long long t0 = clock64();
-      if (c >= nchunks) {
+      if (cl >= nchunks) {
         if (lane == 0) {
           if (k >= kSlots)
             while (*reinterpret_cast<volatile int*>(&s_consumed[si]) < kCW * (k / kSlots))
@@ -986,7 +992,7 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
       else so = sl.aux[i];
     }
     const int table = cnt & 1;
-    if (valid && deg == 0) st_color(cdst + v, 0);  // limit 0: only colour 0
+    if (valid && deg == 0) commit_color(cdst, v, 0);  // limit 0: only colour 0
     k1_push_long(S, v, deg, valid && deg >= S.min_deg);
     k1_small<kSnap, kLower, kLog>(cols, csrc, cdst, v, b, deg,
                                   valid && deg >= 1 && deg <= kSmallMax, W, table, pol, L,
@@ -1036,8 +1042,9 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
         if (old % kCW == kCW - 1) {  // last warp out: the slot is free
           if (S.done_chunks) atomicAdd(S.done_chunks, 1u);
           if (!worklist)
-            k1_request_offsets<CW>(sm.slot[si], off, blockIdx.x + (k + kSlots) * G, nitems,
-                                   item0, n, pol);
+            k1_request_offsets<CW>(sm.slot[si], off,
+                                   (blockIdx.x + (k + kSlots) * G) * S.cstride + S.coffset,
+                                   nitems, item0, n, pol);
         }
       }
       t = -1;
@@ -1058,6 +1065,7 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
     atomicAdd(&ctrl->prof[7], (unsigned long long)n_med);
     atomicAdd(&ctrl->prof[12], (unsigned long long)n_redo);
   }
+  peers_fence();
   const unsigned g = __reduce_add_sync(kFull, gathers);
   if (lane == 0 && g) atomicAdd(&s_gathers, g);
   // the producer warps have returned: count only consumer warps from here on

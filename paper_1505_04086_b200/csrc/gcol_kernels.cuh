@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kBlock) k_list(const long long* __restrict__ o
         const int c = warp_first_fit<false, true, false>(cols, colors, v, b, deg, s_win[warp],
                                                          pol, L, dummy);
         if (lane == 0) {
-          st_color(colors + v, c);
+          commit_color(colors, v, c);
           atomicAdd(&ctrl->recolored, 1);
           if (claim_slot(marks, v, stamp)) out[atomicAdd(&ctrl->out_len, 1)] = v;
         }
@@ -137,13 +137,14 @@ __global__ void __launch_bounds__(kBlock) k_list(const long long* __restrict__ o
         const int c = warp_first_fit<false, false, false>(cols, colors, v, b, deg, s_win[warp],
                                                           pol, L, dummy);
         if (lane == 0) {
-          st_color(colors + v, c);
+          commit_color(colors, v, c);
           atomicAdd(&ctrl->recolored, 1);
           out[atomicAdd(&ctrl->out_len, 1)] = v;
         }
       }
     }
   }
+  peers_fence();
 }
 
 // One piece of a split heavy row (block-wide): detect its conflicts and
@@ -230,7 +231,7 @@ __device__ __forceinline__ void heavy_piece(const long long* __restrict__ off,
   }
   if (tid == 0) {
     if (defective) {
-      st_color(colors + v, c);
+      commit_color(colors, v, c);
       atomicAdd(&ctrl->recolored, 1);
       ctrl->out_list[atomicAdd(&ctrl->out_len, 1)] = v;
     }
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(kBlock) k_heavy(const long long* __restrict__ 
         const int c = block_first_fit<false, true, false>(cols, colors, v, b, deg, s_bwin, &s_red,
                                                           pol, L, dummy);
         if (threadIdx.x == 0) {
-          st_color(colors + v, c);
+          commit_color(colors, v, c);
           atomicAdd(&ctrl->recolored, 1);
           if (claim_slot(marks, v, stamp)) ctrl->out_list[atomicAdd(&ctrl->out_len, 1)] = v;
         }
@@ -285,13 +286,14 @@ __global__ void __launch_bounds__(kBlock) k_heavy(const long long* __restrict__ 
         const int c = block_first_fit<false, false, false>(cols, colors, v, b, deg, s_bwin,
                                                            &s_red, pol, L, dummy);
         if (threadIdx.x == 0) {
-          st_color(colors + v, c);
+          commit_color(colors, v, c);
           atomicAdd(&ctrl->recolored, 1);
           ctrl->out_list[atomicAdd(&ctrl->out_len, 1)] = v;
         }
       }
     }
   }
+  peers_fence();
 }
 
 // K3: one thread closes the round (finish_round, parallel.hpp:140-154) and

@@ -64,6 +64,54 @@ class CheckerOps:
         colors[ids.long()] = vals
 
 
+class CheckerPushOps(CheckerOps):
+    """Push mode on CPU: every rank's replica is a shared-memory tensor and a
+    commit writes all of them (the CPU stand-in for the peer stores)."""
+
+    def __init__(self, off, cols, replicas, rank, world):
+        super().__init__(off, cols)
+        self.reps, self.rank, self.world = replicas, rank, world
+        self.pairs = []
+
+    def partition(self, rank, world, peer_ptrs):
+        assert (rank, world) == (self.rank, self.world)
+
+    def _commit(self, v, c):
+        for r in self.reps:
+            r[v] = c
+
+    def k1_owned(self, colors):
+        n = colors.numel()
+        self.pairs = []
+        for c0 in range(self.rank * gdist.CHUNK, n, self.world * gdist.CHUNK):
+            for v in range(c0, min(c0 + gdist.CHUNK, n)):
+                nb = self.cols[self.off[v]:self.off[v + 1]]
+                nb = nb[nb < v]
+                seen = colors[nb].tolist()
+                self.pairs += [(int(u), v) for u, cu in zip(nb, seen) if cu == -1]
+                used = set(c for c in seen if 0 <= c <= self.deg[v])
+                c = 0
+                while c in used:
+                    c += 1
+                self._commit(v, c)
+        return 0.0
+
+    def candidates(self, colors):
+        out = set()
+        for u, v in self.pairs:
+            if int(colors[u]) == int(colors[v]):
+                out.add(u if (self.deg[u], u) < (self.deg[v], v) else v)
+        return torch.tensor(sorted(out), dtype=torch.int32)
+
+    def round_list(self, colors, work):
+        out = []
+        for v in work.tolist():
+            if self._defective(colors, v):
+                self._commit(v, self._ff(colors, v, False))
+                out.append(v)
+        return torch.tensor(out, dtype=torch.int32)
+
+
 def _graph(seed, n, avg):
     from paper_1505_04086_b200 import gcol
     rng = np.random.default_rng(seed)
@@ -81,6 +129,20 @@ def _worker(rank, world, port, seed, n, avg, q):
         colors = torch.full((n,), -1, dtype=torch.int32)
         st = gdist.color_rsoc_distributed(ops, colors, n, rank, world)
         q.put((rank, colors.numpy().copy(), st.rounds, st.conflicts_per_round,
+               st.round1_candidates))
+    finally:
+        dist.destroy_process_group()
+
+
+def _push_worker(rank, world, port, seed, n, avg, reps, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = _graph(seed, n, avg)
+        ops = CheckerPushOps(g.offsets(), g.adjacency(), reps, rank, world)
+        st = gdist.color_rsoc_partitioned(ops, reps[rank], n, rank, world, peer_ptrs=[0] * world)
+        q.put((rank, reps[rank].numpy().copy(), st.rounds, st.conflicts_per_round,
                st.round1_candidates))
     finally:
         dist.destroy_process_group()
@@ -129,3 +191,38 @@ def test_partition_bounds():
             for (a, b), (c, d) in zip(parts, parts[1:]):
                 assert b == c and a <= b
             assert all(lo % 256 == 0 for lo, _ in parts)
+
+
+@pytest.mark.parametrize("seed,n,avg,world", [(4, 900, 6.0, 2), (5, 2000, 14.0, 2), (6, 1300, 5.0, 3)])
+def test_push_mode_world(seed, n, avg, world):
+    """Push mode: interleaved 256-id chunks, commits written into every
+    replica, candidates gathered once, count all-reduced per round."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    reps = [torch.full((n,), -1, dtype=torch.int32).share_memory_() for _ in range(world)]
+    procs = [ctx.Process(target=_push_worker, args=(r, world, port, seed, n, avg, reps, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    c0 = res[0][1]
+    for r in res[1:]:
+        assert np.array_equal(c0, r[1]), "replicas diverged"
+        assert (r[2], r[3], r[4]) == (res[0][2], res[0][3], res[0][4])
+    g = _graph(seed, n, avg)
+    off, cols = g.offsets(), g.adjacency()
+    deg = np.diff(off)
+    assert (c0 >= 0).all() and (c0 <= deg).all()
+    rows = np.repeat(np.arange(n), deg)
+    assert not (c0[rows] == c0[cols]).any(), "monochromatic edge"
+    assert res[0][3][-1] == 0 and res[0][2] == len(res[0][3])
+
+
+def test_owner_of_interleaves_chunks():
+    ids = torch.arange(0, 4096)
+    own = gdist.owner_of(ids, 4)
+    assert own[:256].eq(0).all() and own[256:512].eq(1).all() and own[1024:1280].eq(0).all()

@@ -68,3 +68,59 @@ def test_k1_range_matches_full_on_one_partition():
     assert (colors >= 0).all()
     with pytest.raises(gcol.input_error):
         ops.k1_range(colors, 3, n)  # ranges start on 256-id chunk boundaries
+
+
+def emulate_push(off, cols, n, P, priority=gcol.Priority.degree_id):
+    """Push mode with P logical ranks on one device, run one after another
+    (no rank waits on another): rank r's handle pushes every colour it
+    commits into the other ranks' replicas through their device pointers,
+    the same stores that go over NVLink between GPUs."""
+    ops = [gdist.DeviceOps(gcol.Graph.from_device(off, cols), priority=int(priority))
+           for _ in range(P)]
+    reps = [torch.full((n,), -1, dtype=torch.int32, device="cuda") for _ in range(P)]
+    ptrs = [t.data_ptr() for t in reps]
+    for r in range(P):
+        ops[r].partition(r, P, ptrs)
+    for r in range(P):
+        ops[r].k1_owned(reps[r])
+    torch.cuda.synchronize()
+    every = torch.cat([ops[r].candidates(reps[r]) for r in range(P)])
+    own = gdist.owner_of(every.long(), P)
+    work = [torch.unique(every[own == r]).to(torch.int32) for r in range(P)]
+    cand = sum(w.numel() for w in work)
+    rounds = 0
+    while True:
+        rec = [ops[r].round_list(reps[r], work[r]) for r in range(P)]
+        rounds += 1
+        if sum(x.numel() for x in rec) == 0:
+            break
+        work = rec
+        assert rounds < 1000
+    return reps, rounds, cand
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_push_mode_partitions(P):
+    off, cols = graphs.erdos_renyi(80_000, 16, 12, "cuda")
+    n = off.numel() - 1
+    reps, rounds, cand = emulate_push(off, cols, n, P)
+    for r in range(1, P):
+        assert torch.equal(reps[0], reps[r]), "replicas diverged"
+    hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
+    c = reps[0].cpu().numpy()
+    assert gcol.verify_coloring(hg, c).ok()
+    assert (c >= 0).all() and (c <= np.diff(hg.offsets())).all()
+    assert gcol.count_colors(c) <= hg.max_degree() + 1
+
+
+def test_push_mode_skewed_graph():
+    """Hubs split into pieces and dynamic sub-tiles under the partition."""
+    off, cols = graphs.make_config("rmat24", "cuda", scale_down=7)
+    n = off.numel() - 1
+    reps, rounds, cand = emulate_push(off, cols, n, 4)
+    for r in range(1, 4):
+        assert torch.equal(reps[0], reps[r])
+    hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
+    c = reps[0].cpu().numpy()
+    assert gcol.verify_coloring(hg, c).ok()
+    assert (c <= np.diff(hg.offsets())).all()
