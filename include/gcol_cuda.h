@@ -170,6 +170,17 @@ int gcol_cuda_color_rsoc_csr(const int64_t* offsets, const int32_t* cols, int64_
                              int32_t device, const gcol_cuda_options* opt, int32_t* colors_out,
                              gcol_cuda_stats* stats);
 
+/* color_catalyurek (parallel.hpp:180-246): rounds of a tentative First-Fit
+ * phase over the worklist (in place, stale reads allowed) and a detection
+ * phase whose defective vertices form the next worklist; W_1 = V.  Stats as
+ * the reference's: barrier_events = 2 * rounds, conflicts_per_round[r] =
+ * defective vertices found in round r (last entry 0).  `priority` picks the
+ * endpoint that retries (ID_LOW is the reference's
+ * has_conflicting_higher_neighbor). */
+int gcol_cuda_color_catalyurek(gcol_cuda_graph* g, const gcol_cuda_options* opt,
+                               int32_t* colors_out, int32_t colors_memory,
+                               gcol_cuda_stats* stats);
+
 /* run_coloring (bench.hpp:35-60) dispatch: GCOL_ALG_SEQ -> the exact
  * sequential First-Fit on the device, GCOL_ALG_RSOC -> color_rsoc,
  * GCOL_ALG_CATALYUREK -> color_catalyurek. */

@@ -5,6 +5,7 @@
 // gives reference users the same call shapes, types and exceptions:
 //
 //   gcol::color_rsoc(g, T, opt)         parallel.hpp:253  ->  gcol::cuda::color_rsoc(g, T, opt)
+//   gcol::color_catalyurek(g, T, opt)   parallel.hpp:183  ->  gcol::cuda::color_catalyurek(g, T, opt)
 //   gcol::run_coloring(g, alg, T, opt)  bench.hpp:35      ->  gcol::cuda::run_coloring(g, alg, T, opt)
 //   gcol::first_fit_sequential(g)       coloring.hpp:110  ->  gcol::cuda::first_fit_sequential(g)
 //   gcol::verify_coloring(g, c)         coloring.hpp:159  ->  gcol::cuda::verify_coloring(g, c)
@@ -157,6 +158,12 @@ inline ColoringRun run_coloring(const gcol::Graph& g, Algorithm algorithm,
 inline ColoringRun color_rsoc(const gcol::Graph& g, unsigned thread_count,
                               const ParallelOptions& opt = {}, const CudaOptions& co = {}) {
   return color_rsoc_host(g, thread_count, opt, co);
+}
+
+// gcol::color_catalyurek (parallel.hpp:183) on the device.
+inline ColoringRun color_catalyurek(const gcol::Graph& g, unsigned thread_count,
+                                    const ParallelOptions& opt = {}, const CudaOptions& co = {}) {
+  return run_coloring(g, Algorithm::catalyurek, thread_count, opt, co);
 }
 
 inline Coloring first_fit_sequential(const gcol::Graph& g) {

@@ -99,6 +99,8 @@ SIGNATURES = {
     "gcol_cuda_color_rsoc": (C.c_int, [_vp, C.POINTER(Options), _vp, _i32, C.POINTER(Stats)]),
     "gcol_cuda_color_rsoc_csr": (C.c_int, [_vp, _vp, _i64, _i64, _i32, C.POINTER(Options), _vp,
                                            C.POINTER(Stats)]),
+    "gcol_cuda_color_catalyurek": (C.c_int, [_vp, C.POINTER(Options), _vp, _i32,
+                                             C.POINTER(Stats)]),
     "gcol_cuda_run_coloring": (C.c_int, [_vp, _i32, C.POINTER(Options), _vp, _i32,
                                          C.POINTER(Stats)]),
     "gcol_cuda_first_fit_sequential": (C.c_int, [_vp, _vp, _i32]),

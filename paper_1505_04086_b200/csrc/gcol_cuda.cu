@@ -104,6 +104,7 @@ struct gcol_cuda_graph {
   int* d_listB = nullptr;
   int* d_heavy = nullptr;
   int* d_marks = nullptr;
+  int* d_iota = nullptr;  // 0..n-1: Çatalyürek's first worklist
   int2* d_pairs = nullptr;
   int* d_pair_counts = nullptr;
   unsigned long long pair_cap = 0;
@@ -1011,6 +1012,7 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
       cudaFreeAsync(g->d_off, g->stream);
       cudaFreeAsync(g->d_cols, g->stream);
     }
+    if (g->d_iota) cudaFreeAsync(g->d_iota, g->stream);
     for (void* p : {static_cast<void*>(g->d_hq), static_cast<void*>(g->d_hslot),
                     static_cast<void*>(g->d_hslot_bm), static_cast<void*>(g->d_vrows),
                     static_cast<void*>(g->d_vpre)})
@@ -1201,13 +1203,143 @@ int gcol_cuda_first_fit_sequential(gcol_cuda_graph* g, int32_t* colors_out, int3
   return GCOL_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Çatalyürek's two-phase rounds (parallel.hpp:180-246) on the device:
+// tentative First-Fit over the worklist in place (the K1 pipeline reading
+// every neighbour, no parking: stale reads are the algorithm's), then a
+// detection phase over the same worklist whose defective vertices form the
+// next one.  Host-driven: one synchronisation per round reads the count.
+template <int R>
+int run_catalyurek(gcol_cuda_graph* g, const gcol_cuda_options& opt,
+                   std::vector<unsigned long long>* cpr, bool* capped) {
+  const int n = static_cast<int>(g->n);
+  const int mm = split_min_of(opt);
+  const bool wide = use_wide(g, opt.k1_wide);
+  if (!g->d_iota) {
+    GCOL_CK(dalloc(&g->d_iota, static_cast<size_t>(n), g->stream));
+    if (n > 0) k_iota<<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_iota, n);
+  }
+  int* in = g->d_iota;
+  int nin = n;
+  int* lists[2] = {g->d_listA, g->d_listB};
+  int which = 0;
+  *capped = false;
+  for (int round = 1;; ++round) {
+    // tentative phase over the worklist (all of V in round 1)
+    if (nin > 0) {
+      K1Launch K;
+      if (int rc = plan_k1<false, false, false>(g, opt.k1_blocks_per_sm, mm, &K, wide, nin))
+        return rc;
+      if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, nullptr, 0)) return rc;
+      if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
+      launch_k1<false, false, false>(K, g->stream, g->d_off, g->d_cols, n, nin,
+                                     round == 1 ? nullptr : in, g->d_colors, g->d_colors,
+                                     g->d_ctrl, 0, 0);
+      if (round == 1) GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
+    } else if (round == 1) {
+      GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
+    }
+    // detection phase: flags of the worklist, then the flagged entries
+    int* out = lists[which];
+    which ^= 1;
+    if (int rc = reset_ctrl(g, 1, in, out, g->d_marks, nin)) return rc;
+    if (nin > 0) {
+      k_list<R, true><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
+                                                             g->d_ctrl, g->d_heavy, g->d_marks);
+      k_heavy<R, true><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
+                                                              g->d_ctrl, g->d_heavy, g->d_marks);
+      k_compact_flags<<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_ctrl, in, nin, g->d_marks);
+    }
+    GCOL_CK(cudaGetLastError());
+    int found = 0;
+    GCOL_CK(cudaMemcpyAsync(&found, &g->d_ctrl->out_len, sizeof found, cudaMemcpyDeviceToHost,
+                            g->stream));
+    GCOL_CK(cudaStreamSynchronize(g->stream));
+    cpr->push_back(static_cast<unsigned long long>(found));  // finish_round
+    if (found == 0) break;
+    if (static_cast<uint64_t>(round) >= opt.round_cap) {
+      *capped = true;
+      break;
+    }
+    in = out;
+    nin = found;
+  }
+  return GCOL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gcol_cuda_color_catalyurek(gcol_cuda_graph* g, const gcol_cuda_options* opt_in,
+                               int32_t* colors_out, int32_t colors_memory, gcol_cuda_stats* stats) {
+  if (int rc = check_graph(g)) return rc;
+  gcol_cuda_options opt;
+  if (int rc = read_options(opt_in, &opt)) return rc;
+  if (g->n > 0 && !colors_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "colors_out is null");
+  GCOL_CK(cudaSetDevice(g->device));
+  if (int rc = ensure_run_buffers(g)) return rc;
+  const size_t n = static_cast<size_t>(g->n);
+  GCOL_CK(cudaMemsetAsync(g->d_colors, 0xff, sizeof(int) * n, g->stream));  // Coloring(n), untimed
+  std::vector<unsigned long long> cpr;
+  bool capped = false;
+  GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
+  const int r = rule_of(opt.priority);
+  int rc;
+  if (r == kIdLow) rc = run_catalyurek<kIdLow>(g, opt, &cpr, &capped);
+  else if (r == kIdHigh || r == kOrdered) rc = run_catalyurek<kIdHigh>(g, opt, &cpr, &capped);
+  else rc = run_catalyurek<kDegId>(g, opt, &cpr, &capped);
+  if (rc) return rc;
+  GCOL_CK(cudaEventRecord(g->ev_end, g->stream));
+  gcol_cuda_verify_report rep{};
+  if (int r2 = verify_device(g, g->d_colors, &rep, nullptr, nullptr, nullptr, 0)) return r2;
+  if (int r2 = copy_out(g, colors_out, g->d_colors, sizeof(int) * n, colors_memory)) return r2;
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  float ms_total = 0.f, ms_k1 = 0.f;
+  GCOL_CK(cudaEventElapsedTime(&ms_total, g->ev_start, g->ev_end));
+  GCOL_CK(cudaEventElapsedTime(&ms_k1, g->ev_start, g->ev_k1));
+  if (stats) {
+    stats->algorithm = GCOL_ALG_CATALYUREK;
+    stats->thread_count = opt.thread_count;
+    stats->rounds = cpr.size();
+    uint64_t total = 0;
+    for (auto c : cpr) total += c;
+    stats->conflicts_total = total;
+    stats->barrier_events = 2 * cpr.size();  // two barriers per round (parallel.hpp:181-182)
+    stats->num_colors = rep.num_colors;
+    stats->fallback_triggered = 0;
+    stats->wall_time_ns = static_cast<uint64_t>(static_cast<double>(ms_total) * 1e6);
+    stats->initial_pass_ns = static_cast<uint64_t>(static_cast<double>(ms_k1) * 1e6);
+    stats->cpr_len = cpr.size();
+    if (stats->conflicts_per_round)
+      for (uint64_t i = 0; i < cpr.size() && i < stats->cpr_cap; ++i)
+        stats->conflicts_per_round[i] = cpr[i];
+    stats->pairs_logged = 0;
+    stats->round1_candidates = static_cast<uint64_t>(g->n);  // W_1 = V
+    stats->pair_overflow = 0;
+    stats->priority = opt.priority;
+    stats->k1_gathers = 0;
+  }
+  if (capped)
+    return fail(GCOL_ERR_ROUND_CAP,
+                "round_cap reached before convergence (no CPU repair fallback exists)");
+  if (rep.violations != 0 || rep.out_of_bound != 0)
+    return fail(GCOL_ERR_VERIFY, "parallel coloring finished improper");
+  return GCOL_OK;
+}
+
 int gcol_cuda_run_coloring(gcol_cuda_graph* g, int32_t algorithm, const gcol_cuda_options* opt_in,
                            int32_t* colors_out, int32_t colors_memory, gcol_cuda_stats* stats) {
   if (int rc = check_graph(g)) return rc;
   if (algorithm == GCOL_ALG_RSOC)
     return gcol_cuda_color_rsoc(g, opt_in, colors_out, colors_memory, stats);
+  if (algorithm == GCOL_ALG_CATALYUREK)
+    return gcol_cuda_color_catalyurek(g, opt_in, colors_out, colors_memory, stats);
   if (algorithm != GCOL_ALG_SEQ)
-    return fail(GCOL_ERR_INVALID_ARGUMENT, "algorithm not available on the device yet");
+    return fail(GCOL_ERR_INVALID_ARGUMENT, "unknown algorithm");
   gcol_cuda_options opt;
   if (int rc = read_options(opt_in, &opt)) return rc;
   cudaEvent_t a, b;

@@ -646,6 +646,24 @@ __global__ void __launch_bounds__(kBlock) k_detect_range(const long long* __rest
   }
 }
 
+// Çatalyürek's detection phase output: the flagged worklist entries,
+// appended to ctrl->out_list (warp-aggregated).
+__global__ void __launch_bounds__(kBlock) k_compact_flags(Ctrl* ctrl, const int* in, int nin,
+                                                          const int* flags) {
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < nin;
+       i0 += (long long)gridDim.x * blockDim.x) {
+    const long long i = i0 + lane_id();
+    const bool pred = i < nin && flags[i] != 0;
+    append_warp(ctrl->out_list, &ctrl->out_len, pred, pred ? in[i] : 0);
+  }
+}
+
+__global__ void k_iota(int* p, int n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = (int)i;
+}
+
 // Apply (id, colour) deltas received from other ranks.
 __global__ void k_scatter_colors(int* colors, const int* ids, const int* vals, long long count) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;

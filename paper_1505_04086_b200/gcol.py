@@ -375,6 +375,12 @@ def color_rsoc(g: Graph, thread_count: int, opt: Optional[ParallelOptions] = Non
     return run_coloring(g, Algorithm.rsoc, thread_count, opt, **kw)
 
 
+def color_catalyurek(g: Graph, thread_count: int, opt: Optional[ParallelOptions] = None,
+                     **kw) -> ColoringRun:
+    """parallel.hpp:180-246 on the device (tentative phase, then detection)."""
+    return run_coloring(g, Algorithm.catalyurek, thread_count, opt, **kw)
+
+
 def color_rsoc_csr(offsets, adjacency, thread_count: int,
                    opt: Optional[ParallelOptions] = None, *, colors_out=None,
                    device: int = -1) -> ColoringRun:

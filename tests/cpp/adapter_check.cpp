@@ -61,6 +61,12 @@ int main() {
     const auto n = static_cast<gcol::vertex_t>(1 + rng() % 5000);
     const gcol::Graph g = random_graph(rng, n, 2.0 + static_cast<double>(rng() % 80) / 10.0);
     for (unsigned t : {1u, 16u}) check_run(g, gcol::cuda::color_rsoc(g, t), t);
+    {
+      const gcol::ColoringRun c = gcol::cuda::color_catalyurek(g, 4);
+      check(c.coloring.complete() && gcol::verify_coloring(g, c.coloring).ok(), "catalyurek proper");
+      check(c.stats.barrier_events == 2 * c.stats.rounds, "catalyurek barrier_events");
+      check(c.stats.conflicts_per_round.back() == 0, "catalyurek last round clean");
+    }
     const gcol::Coloring seq = gcol::first_fit_sequential(g);
     check(gcol::cuda::first_fit_sequential(g) == seq, "first_fit_sequential bit-identical");
     const gcol::ColoringRun s = gcol::cuda::run_coloring(g, gcol::Algorithm::seq, 1);

@@ -323,3 +323,45 @@ def test_verify_rows_split_into_pieces(oracle_mod):
         assert [(v.u, v.v, v.color) for v in got.violations] == want
     run = gcol.color_rsoc(g, 4)
     check_run(g, run, 4)
+
+
+def test_catalyurek_device():
+    """color_catalyurek on the device: test_parallel.cpp:18-36 invariants with
+    barrier_events = 2 x rounds, K12 -> 12 colours, star(200) -> 2 colours,
+    the empty graph in one round, and the colour band of the oracle's run."""
+    def check_cat(g, run, threads):
+        check_run(g, run, threads, algorithm="catalyurek")
+        assert run.stats.barrier_events == 2 * run.stats.rounds
+        assert run.stats.algorithm == gcol.Algorithm.catalyurek
+    k12 = gcol.build_graph([(i, j) for i in range(12) for j in range(i + 1, 12)], 12)
+    r = gcol.color_catalyurek(k12, 4)
+    check_cat(k12, r, 4)
+    assert r.stats.num_colors == 12
+    star = gcol.build_graph([(0, i) for i in range(1, 201)], 201)
+    r = gcol.color_catalyurek(star, 4)
+    check_cat(star, r, 4)
+    assert r.stats.num_colors == 2
+    empty = gcol.build_graph([], 0)
+    r = gcol.color_catalyurek(empty, 2)
+    assert r.stats.rounds == 1 and r.stats.conflicts_per_round == [0]
+    rng = np.random.default_rng(808)
+    for n, avg in ((1, 0.0), (500, 3.0), (20_000, 12.0), (100_000, 30.0)):
+        g = random_graph(rng, n, avg)
+        for prio in (gcol.Priority.id_low, gcol.Priority.degree_id):
+            check_cat(g, gcol.color_catalyurek(g, 8, gcol.ParallelOptions(priority=prio)), 8)
+
+
+def test_catalyurek_scaled_configs(oracle_mod):
+    for name, sd in (("er", 2), ("rmat24", 6)):
+        off, cols = graphs.make_config(name, "cuda", scale_down=sd)
+        g = gcol.Graph.from_device(off, cols)
+        hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
+        ours = []
+        for _ in range(3):
+            run = gcol.color_catalyurek(g, 1)
+            check_run(hg, run, 1, algorithm="catalyurek")
+            ours.append(run.stats.num_colors)
+        o = oracle_mod.CSR(hg.offsets(), hg.adjacency())
+        ref = sorted(oracle_mod.color_parallel(o, 8, "catalyurek")[1]["num_colors"]
+                     for _ in range(3))[1]
+        assert sorted(ours)[1] <= int(1.10 * ref) + 2, (name, ours, ref)
