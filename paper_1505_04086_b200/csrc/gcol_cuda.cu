@@ -115,10 +115,12 @@ struct gcol_cuda_graph {
   std::map<int, SplitPlan> splits;
   std::map<cudaGraphExec_t, int> k1_warps;  // K1 warps of each instantiated graph
   // streamed upload (gcol_cuda_color_rsoc_csr): the adjacency arrives in
-  // pieces on copy_stream while K1 runs; d_progress = entries resident
-  cudaStream_t copy_stream = nullptr;
-  unsigned long long* d_progress = nullptr;
-  cudaEvent_t ev_copied = nullptr;
+  // 2^piece_shift-entry pieces alternating between two copy streams while K1
+  // runs; d_ready[p] = 1 once piece p is resident
+  cudaStream_t copy_stream = nullptr, copy_stream2 = nullptr;
+  unsigned* d_ready = nullptr;
+  int piece_shift = 0;
+  cudaEvent_t ev_copied = nullptr, ev_copied2 = nullptr;
   cudaEvent_t ev_copy0 = nullptr;  // GCOL_TRACE: start of the upload
   // heavy rows of the rounds, split into pieces (Ctrl::hq ...)
   int hslots = 0, hq_cap = 0;
@@ -372,7 +374,7 @@ int plan_k1_cw(gcol_cuda_graph* g, int k1_blocks, int split_min, long long nitem
   K->S = SplitArgs{P->nslots > 0 ? split_min : INT_MAX, P->d_slot_v, P->d_slot_deg,
                    P->d_slot_left, P->d_slot_bm, P->d_q, P->d_q_seq, P->d_ctr, P->d_ctr + 1,
                    reinterpret_cast<int*>(P->d_ctr + 2), K->grid1, P->d_ctr + 3,
-                   g->d_progress, g->max_degree > 64 ? 1 : 0, 1, 0};
+                   g->d_ready, g->piece_shift, g->max_degree > 64 ? 1 : 0, 1, 0};
   const unsigned long long per = g->pair_cap / static_cast<unsigned long long>(K->grid1);
   K->L = PairLogArgs{g->d_pairs, static_cast<int>(std::min<unsigned long long>(per, 1u << 30)),
                      g->d_pair_counts, &g->d_ctrl->pair_overflow};
@@ -834,35 +836,34 @@ int validate_offsets_host(const int64_t* off, int64_t n, GraphStats* gs) {
   return GCOL_OK;
 }
 
-__global__ void k_publish(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__global__ void k_publish(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-constexpr int64_t kUploadPiece = 1 << 21;  // smallest streamed piece x 2 (entries)
 
-// Publishing the upload progress: a stream memory operation executed by the
+// Publishing a resident piece: a stream memory operation executed by the
 // copy stream itself (no kernel has to be scheduled next to the running K1);
 // a one-thread release-store kernel where the driver lacks it.
-using WriteValue64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
-WriteValue64Fn write_value64() {
-  static WriteValue64Fn fn = [] {
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn write_value32() {
+  static WriteValue32Fn fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q{};
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) != cudaSuccess ||
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
         q != cudaDriverEntryPointSuccess) {
       cudaGetLastError();
       p = nullptr;
     }
-    return reinterpret_cast<WriteValue64Fn>(p);
+    return reinterpret_cast<WriteValue32Fn>(p);
   }();
   return fn;
 }
 
-void publish_progress(cudaStream_t s, unsigned long long* p, unsigned long long v) {
-  if (WriteValue64Fn fn = write_value64())
-    if (fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(p), v, 0) == CUDA_SUCCESS)
+void publish_piece(cudaStream_t s, unsigned* flag) {
+  if (WriteValue32Fn fn = write_value32())
+    if (fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), 1u, 0) == CUDA_SUCCESS)
       return;
-  k_publish<<<1, 1, 0, s>>>(p, v);
+  k_publish<<<1, 1, 0, s>>>(flag, 1u);
 }
 
 // Shared by graph_create and color_rsoc_csr.  `streamed`: the adjacency is
@@ -924,32 +925,40 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
           copy_in(g, g->d_cols, cols, sizeof(int) * static_cast<size_t>(m), memory))
         return bail(GCOL_ERR_CUDA);
     } else {
+      // pieces of 2^shift entries (1M..4M) alternate between two copy streams,
+      // so one stream's DMA runs while the other publishes its flag
+      int shift = 20;
+      while (shift < 22 && (int64_t{1} << (shift + 5)) < m) ++shift;
+      if (const char* pe = std::getenv("GCOL_UPLOAD_SHIFT")) shift = std::max(10, std::atoi(pe));
+      const int64_t piece = int64_t{1} << shift;
+      const int64_t npieces = (m + piece - 1) / piece;
+      g->piece_shift = shift;
       cudaEvent_t ev_alloc = nullptr, ev_off = nullptr;
-      if (dalloc(&g->d_progress, 1, g->stream) != cudaSuccess ||
-          cudaMemsetAsync(g->d_progress, 0, sizeof(unsigned long long), g->stream) != cudaSuccess ||
+      if (dalloc(&g->d_ready, static_cast<size_t>(std::max<int64_t>(npieces, 1)), g->stream) != cudaSuccess ||
+          cudaMemsetAsync(g->d_ready, 0, sizeof(unsigned) * static_cast<size_t>(std::max<int64_t>(npieces, 1)),
+                          g->stream) != cudaSuccess ||
           cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaStreamCreateWithFlags(&g->copy_stream2, cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&ev_off, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&g->ev_copied2, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreate(&g->ev_copied) != cudaSuccess || cudaEventCreate(&g->ev_copy0) != cudaSuccess)
         return bail(fail(GCOL_ERR_CUDA, "streamed upload setup failed"));
       const auto mt = memory == GCOL_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
       cudaEventRecord(ev_alloc, g->stream);
       cudaStreamWaitEvent(g->copy_stream, ev_alloc, 0);
+      cudaStreamWaitEvent(g->copy_stream2, ev_alloc, 0);
       cudaEventRecord(g->ev_copy0, g->copy_stream);
       cudaMemcpyAsync(g->d_off, offsets, off_bytes, mt, g->copy_stream);
       cudaEventRecord(ev_off, g->copy_stream);
-      // pieces of m/32 entries (4M..16M: each costs ~25 us of DMA restart), the
-      // last 2 pieces' worth in halving steps down to 1M, so the rows that K1
-      // can only colour after the transfer ends are few
-      int64_t piece = std::min<int64_t>(std::max<int64_t>(m / 32, 4 << 20), 16 << 20);
-      if (const char* pe = std::getenv("GCOL_UPLOAD_PIECE")) piece = std::max<int64_t>(1024, std::atoll(pe));
-      for (int64_t p = 0, len = 0; p < m; p += len) {
-        const int64_t r = m - p;
-        len = r > 2 * piece ? piece : std::min(r, std::max<int64_t>(r / 2, kUploadPiece / 2));
-        cudaMemcpyAsync(g->d_cols + p, cols + p, sizeof(int) * static_cast<size_t>(len), mt,
-                        g->copy_stream);
-        publish_progress(g->copy_stream, g->d_progress, static_cast<unsigned long long>(p + len));
+      for (int64_t p = 0; p < npieces; ++p) {
+        cudaStream_t cs = (p & 1) ? g->copy_stream : g->copy_stream2;
+        const int64_t b = p * piece, len = std::min(piece, m - b);
+        cudaMemcpyAsync(g->d_cols + b, cols + b, sizeof(int) * static_cast<size_t>(len), mt, cs);
+        publish_piece(cs, g->d_ready + p);
       }
+      cudaEventRecord(g->ev_copied2, g->copy_stream2);
+      cudaStreamWaitEvent(g->copy_stream, g->ev_copied2, 0);
       cudaEventRecord(g->ev_copied, g->copy_stream);
       cudaStreamWaitEvent(g->stream, ev_off, 0);  // offsets first; the adjacency follows
       cudaEventDestroy(ev_alloc);
@@ -994,14 +1003,15 @@ int gcol_cuda_graph_create(const int64_t* offsets, const int32_t* cols, int64_t 
 int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
   if (!g) return GCOL_OK;
   cudaSetDevice(g->device);
-  if (g->copy_stream) {  // a streamed upload still in flight reads the caller's memory
-    cudaStreamSynchronize(g->copy_stream);
-    cudaStreamDestroy(g->copy_stream);
-    g->copy_stream = nullptr;
-  }
-  if (g->ev_copied) cudaEventDestroy(g->ev_copied);
-  if (g->ev_copy0) cudaEventDestroy(g->ev_copy0);
-  if (g->d_progress && g->stream) cudaFreeAsync(g->d_progress, g->stream);
+  for (cudaStream_t* cs : {&g->copy_stream, &g->copy_stream2})
+    if (*cs) {  // a streamed upload still in flight reads the caller's memory
+      cudaStreamSynchronize(*cs);
+      cudaStreamDestroy(*cs);
+      *cs = nullptr;
+    }
+  for (cudaEvent_t ev : {g->ev_copied, g->ev_copied2, g->ev_copy0})
+    if (ev) cudaEventDestroy(ev);
+  if (g->d_ready && g->stream) cudaFreeAsync(g->d_ready, g->stream);
   for (auto& kv : g->execs) {
     cudaGraphExecDestroy(kv.second.second);
     cudaGraphDestroy(kv.second.first);

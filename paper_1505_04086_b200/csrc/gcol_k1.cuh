@@ -114,7 +114,8 @@ struct SplitArgs {
   int* alive;           // consumer warps that may still publish pieces
   int G;                // mailboxes (= K1 grid)
   unsigned* done_chunks;  // chunks fully consumed (drift bound)
-  const unsigned long long* progress;  // streamed upload: adjacency entries resident (or null)
+  const unsigned* piece_ready;  // streamed upload: flag per 2^piece_shift adjacency entries
+  int piece_shift;              //   resident (null: the whole CSR is resident)
   int dyn_tiles;        // 1: consumer warps take sub-tiles from a CTA counter
   int cstride, coffset; // this launch owns the chunks coffset + cstride * i (interleaved
                         // multi-GPU partition; 1, 0: all)
@@ -832,10 +833,11 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
       if (contig) {
         mbar_wait(&sl.offb, par);              // offsets of chunk k (every lane; the
                                                // slot was freed before they were requested)
-        if (S.progress) {  // streamed upload: the chunk's adjacency must be resident
-          const unsigned long long need = (unsigned long long)sl.offs[rows];
-          if (lane == 0)
-            while (ld_acquire_u64(S.progress) < need) __nanosleep(256);
+        if (S.piece_ready) {  // streamed upload: the chunk's adjacency must be resident
+          const long long lo = sl.offs[0], hi = sl.offs[rows];
+          if (lane == 0 && hi > lo)
+            for (long long p = lo >> S.piece_shift; p <= (hi - 1) >> S.piece_shift; ++p)
+              while (ld_acquire_u32(S.piece_ready + p) == 0u) __nanosleep(256);
           __syncwarp();
         }
         if (S.min_deg == INT_MAX) {
