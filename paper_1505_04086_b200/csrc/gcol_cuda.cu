@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <tuple>
@@ -159,6 +160,59 @@ int ensure_device(int device, int* chosen) {
   return GCOL_OK;
 }
 
+// Streams and events outlive graph handles in a per-process pool: creating
+// and destroying them costs tens of microseconds each, which the one-call
+// API would otherwise pay on every call.  Returned objects are idle or have
+// only stream-ordered frees pending.
+struct ResPool {
+  std::mutex mu;
+  std::map<int, std::vector<cudaStream_t>> streams;
+  std::map<int, std::vector<cudaEvent_t>> events[2];  // [0] no timing, [1] timing
+};
+
+ResPool& res_pool() {
+  static ResPool* p = new ResPool();  // never destroyed: outlives static teardown
+  return *p;
+}
+
+cudaError_t take_stream(int dev, cudaStream_t* s) {
+  {
+    std::lock_guard<std::mutex> lk(res_pool().mu);
+    auto& v = res_pool().streams[dev];
+    if (!v.empty()) {
+      *s = v.back();
+      v.pop_back();
+      return cudaSuccess;
+    }
+  }
+  return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+}
+
+void give_stream(int dev, cudaStream_t s) {
+  if (!s) return;
+  std::lock_guard<std::mutex> lk(res_pool().mu);
+  res_pool().streams[dev].push_back(s);
+}
+
+cudaError_t take_event(int dev, bool timing, cudaEvent_t* e) {
+  {
+    std::lock_guard<std::mutex> lk(res_pool().mu);
+    auto& v = res_pool().events[timing ? 1 : 0][dev];
+    if (!v.empty()) {
+      *e = v.back();
+      v.pop_back();
+      return cudaSuccess;
+    }
+  }
+  return timing ? cudaEventCreate(e) : cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+}
+
+void give_event(int dev, bool timing, cudaEvent_t e) {
+  if (!e) return;
+  std::lock_guard<std::mutex> lk(res_pool().mu);
+  res_pool().events[timing ? 1 : 0][dev].push_back(e);
+}
+
 template <class T>
 cudaError_t dalloc(T** p, size_t count, cudaStream_t s) {
   return cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T), s);
@@ -196,11 +250,11 @@ int ensure_run_buffers(gcol_cuda_graph* g) {
   g->max_k1_grid = g->sms * 32;  // >= any K1 grid (occupancy <= 32 CTAs/SM)
   GCOL_CK(dalloc(&g->d_pair_counts, static_cast<size_t>(g->max_k1_grid), g->stream));
   GCOL_CK(dalloc(&g->d_ctrl, 1, g->stream));
-  GCOL_CK(cudaEventCreate(&g->ev_start));
-  GCOL_CK(cudaEventCreate(&g->ev_k1));
-  GCOL_CK(cudaEventCreate(&g->ev_end));
-  GCOL_CK(cudaStreamCreateWithFlags(&g->out_stream, cudaStreamNonBlocking));
-  GCOL_CK(cudaEventCreateWithFlags(&g->ev_final, cudaEventDisableTiming));
+  GCOL_CK(take_event(g->device, true, &g->ev_start));
+  GCOL_CK(take_event(g->device, true, &g->ev_k1));
+  GCOL_CK(take_event(g->device, true, &g->ev_end));
+  GCOL_CK(take_stream(g->device, &g->out_stream));
+  GCOL_CK(take_event(g->device, false, &g->ev_final));
   if (g->gs.rows[1] > 0) {  // rows the rounds split into pieces
     g->hslots = static_cast<int>(std::min<unsigned long long>(g->gs.rows[1], 65536));
     g->hq_cap = static_cast<int>(g->gs.pieces[1]);
@@ -891,7 +945,7 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
   g->n = n;
   g->m = m;
   cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+  cudaError_t e = take_stream(dev, &g->stream);
   if (e != cudaSuccess) {
     delete g;
     return fail(GCOL_ERR_CUDA, std::string("stream create: ") + cudaGetErrorString(e));
@@ -925,10 +979,12 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
           copy_in(g, g->d_cols, cols, sizeof(int) * static_cast<size_t>(m), memory))
         return bail(GCOL_ERR_CUDA);
     } else {
-      // pieces of 2^shift entries (1M..4M) alternate between two copy streams,
-      // so one stream's DMA runs while the other publishes its flag
-      int shift = 20;
-      while (shift < 22 && (int64_t{1} << (shift + 5)) < m) ++shift;
+      // pieces of 2^shift entries alternate between two copy streams, so one
+      // stream's DMA runs while the other publishes its flag; m/16 per piece,
+      // 4M..16M entries (measured: smaller pieces lose PCIe efficiency, a
+      // single piece leaves all of K1 after the transfer)
+      int shift = 22;
+      while (shift < 24 && (int64_t{1} << (shift + 5)) <= m) ++shift;
       if (const char* pe = std::getenv("GCOL_UPLOAD_SHIFT")) shift = std::max(10, std::atoi(pe));
       const int64_t piece = int64_t{1} << shift;
       const int64_t npieces = (m + piece - 1) / piece;
@@ -937,12 +993,13 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
       if (dalloc(&g->d_ready, static_cast<size_t>(std::max<int64_t>(npieces, 1)), g->stream) != cudaSuccess ||
           cudaMemsetAsync(g->d_ready, 0, sizeof(unsigned) * static_cast<size_t>(std::max<int64_t>(npieces, 1)),
                           g->stream) != cudaSuccess ||
-          cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
-          cudaStreamCreateWithFlags(&g->copy_stream2, cudaStreamNonBlocking) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ev_off, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&g->ev_copied2, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreate(&g->ev_copied) != cudaSuccess || cudaEventCreate(&g->ev_copy0) != cudaSuccess)
+          take_stream(dev, &g->copy_stream) != cudaSuccess ||
+          take_stream(dev, &g->copy_stream2) != cudaSuccess ||
+          take_event(dev, false, &ev_alloc) != cudaSuccess ||
+          take_event(dev, false, &ev_off) != cudaSuccess ||
+          take_event(dev, false, &g->ev_copied2) != cudaSuccess ||
+          take_event(dev, true, &g->ev_copied) != cudaSuccess ||
+          take_event(dev, true, &g->ev_copy0) != cudaSuccess)
         return bail(fail(GCOL_ERR_CUDA, "streamed upload setup failed"));
       const auto mt = memory == GCOL_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
       cudaEventRecord(ev_alloc, g->stream);
@@ -961,8 +1018,9 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
       cudaStreamWaitEvent(g->copy_stream, g->ev_copied2, 0);
       cudaEventRecord(g->ev_copied, g->copy_stream);
       cudaStreamWaitEvent(g->stream, ev_off, 0);  // offsets first; the adjacency follows
-      cudaEventDestroy(ev_alloc);
-      cudaEventDestroy(ev_off);
+      if (std::getenv("GCOL_STREAM_SERIAL")) cudaStreamWaitEvent(g->stream, g->ev_copied, 0);
+      give_event(dev, false, ev_alloc);  // recorded work keeps them valid until it runs
+      give_event(dev, false, ev_off);
       if ((e = cudaGetLastError()) != cudaSuccess)
         return bail(fail(GCOL_ERR_CUDA, std::string("streamed upload: ") + cudaGetErrorString(e)));
     }
@@ -1006,11 +1064,12 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
   for (cudaStream_t* cs : {&g->copy_stream, &g->copy_stream2})
     if (*cs) {  // a streamed upload still in flight reads the caller's memory
       cudaStreamSynchronize(*cs);
-      cudaStreamDestroy(*cs);
+      give_stream(g->device, *cs);
       *cs = nullptr;
     }
-  for (cudaEvent_t ev : {g->ev_copied, g->ev_copied2, g->ev_copy0})
-    if (ev) cudaEventDestroy(ev);
+  give_event(g->device, true, g->ev_copied);
+  give_event(g->device, false, g->ev_copied2);
+  give_event(g->device, true, g->ev_copy0);
   if (g->d_ready && g->stream) cudaFreeAsync(g->d_ready, g->stream);
   for (auto& kv : g->execs) {
     cudaGraphExecDestroy(kv.second.second);
@@ -1033,15 +1092,15 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
                     static_cast<void*>(g->d_ctrl)})
       if (p) cudaFreeAsync(p, g->stream);
     if (g->d_pair_counts) cudaFreeAsync(g->d_pair_counts, g->stream);
-    cudaStreamSynchronize(g->stream);
-    cudaStreamDestroy(g->stream);
+    give_stream(g->device, g->stream);  // only the frees above may still be queued
   }
   if (g->out_stream) {
     cudaStreamSynchronize(g->out_stream);
-    cudaStreamDestroy(g->out_stream);
+    give_stream(g->device, g->out_stream);
   }
-  for (cudaEvent_t ev : {g->ev_start, g->ev_k1, g->ev_end, g->ev_final})
-    if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : {g->ev_start, g->ev_k1, g->ev_end})
+    give_event(g->device, true, ev);
+  give_event(g->device, false, g->ev_final);
   delete g;
   return GCOL_OK;
 }
