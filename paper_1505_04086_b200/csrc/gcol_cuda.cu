@@ -106,6 +106,7 @@ struct gcol_cuda_graph {
   int* d_heavy = nullptr;
   int* d_marks = nullptr;
   int* d_iota = nullptr;  // 0..n-1: Çatalyürek's first worklist
+  unsigned char* d_vacc = nullptr;  // verification accumulator + colour census
   int2* d_pairs = nullptr;
   int* d_pair_counts = nullptr;
   unsigned long long pair_cap = 0;
@@ -664,25 +665,38 @@ int verify_device(gcol_cuda_graph* g, const int* d_col, gcol_cuda_verify_report*
                   uint32_t* out_u, uint32_t* out_v, int32_t* out_c, int64_t cap) {
   const int n = static_cast<int>(g->n);
   if (int rc = ensure_verify_plan(g)) return rc;
-  VerifyAcc* d_acc = nullptr;
+  // accumulator + census bitmap of colours 0..max_degree + 1 (a proper First-Fit
+  // colouring never exceeds them), persistent per graph: one pass, one sync
+  const int census_max = g->max_degree + 1;
+  const size_t cwords = static_cast<size_t>(census_max) / 32 + 1;
+  if (!g->d_vacc) {
+    GCOL_CK(dalloc(reinterpret_cast<unsigned char**>(&g->d_vacc), sizeof(VerifyAcc) + 4 * cwords,
+                   g->stream));
+  }
+  VerifyAcc* d_acc = reinterpret_cast<VerifyAcc*>(g->d_vacc);
+  unsigned* d_census = reinterpret_cast<unsigned*>(g->d_vacc + sizeof(VerifyAcc));
   int* d_vcount = nullptr;
-  GCOL_CK(dalloc(&d_acc, 1, g->stream));
-  GCOL_CK(cudaMemsetAsync(d_acc, 0, sizeof(VerifyAcc), g->stream));
+  GCOL_CK(cudaMemsetAsync(d_acc, 0, sizeof(VerifyAcc) + 4 * cwords, g->stream));
   GCOL_CK(cudaMemsetAsync(&d_acc->max_color, 0xff, sizeof(int), g->stream));
   if (cap > 0) GCOL_CK(dalloc(&d_vcount, static_cast<size_t>(n), g->stream));
   const int grid = g->sms * 8;
   if (n > 0)
     k_verify_count<<<grid, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, d_col, d_acc, d_vcount,
-                                                   g->nvrows > 0 ? kHPiece : INT_MAX);
+                                                   g->nvrows > 0 ? kHPiece : INT_MAX, d_census,
+                                                   census_max);
   if (n > 0 && g->nvrows > 0)
     k_verify_big<<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, d_col, g->d_vrows,
                                                        g->d_vpre, g->nvrows, d_acc, d_vcount);
   GCOL_CK(cudaGetLastError());
   VerifyAcc acc;
+  std::vector<unsigned> census(cwords);
   GCOL_CK(cudaMemcpyAsync(&acc, d_acc, sizeof acc, cudaMemcpyDeviceToHost, g->stream));
+  GCOL_CK(cudaMemcpyAsync(census.data(), d_census, 4 * cwords, cudaMemcpyDeviceToHost, g->stream));
   GCOL_CK(cudaStreamSynchronize(g->stream));
   uint32_t distinct = 0;
-  if (acc.max_color >= 0) {
+  if (acc.max_color >= 0 && acc.max_color <= census_max) {
+    for (unsigned w : census) distinct += static_cast<uint32_t>(__builtin_popcount(w));
+  } else if (acc.max_color >= 0) {  // colours beyond any First-Fit bound: a full census
     const int words = acc.max_color / 32 + 1;
     unsigned* d_bitmap = nullptr;
     GCOL_CK(dalloc(&d_bitmap, words, g->stream));
@@ -726,8 +740,6 @@ int verify_device(gcol_cuda_graph* g, const int* d_col, gcol_cuda_verify_report*
     GCOL_CK(cudaFreeAsync(d_pos, g->stream));
     GCOL_CK(cudaFreeAsync(d_vcount, g->stream));
   }
-  GCOL_CK(cudaFreeAsync(d_acc, g->stream));
-  GCOL_CK(cudaStreamSynchronize(g->stream));
   if (rep) {
     rep->violations = acc.violations;
     rep->uncolored = acc.uncolored;
@@ -853,13 +865,15 @@ namespace {
 // Structural checks of a host CSR (graph.hpp:50-56: offsets cover the
 // adjacency and never decrease), split over host threads; called while the
 // upload DMA runs.
-int validate_offsets_host(const int64_t* off, int64_t n, GraphStats* gs) {
+int validate_offsets_host(const int64_t* off, int64_t n, GraphStats* gs,
+                          std::vector<int>* big_rows) {
   const int64_t kPer = 1 << 18;
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
   const int T = static_cast<int>(std::max<int64_t>(
       1, std::min<int64_t>({static_cast<int64_t>(hw), 16, (n + kPer - 1) / kPer})));
   std::atomic<bool> bad{false};
   std::vector<GraphStats> part(static_cast<size_t>(T));
+  std::vector<std::vector<int>> bigs(static_cast<size_t>(T));
   auto work = [&](int t) {
     const int64_t lo = n * t / T, hi = n * (t + 1) / T;
     GraphStats s{};
@@ -870,6 +884,7 @@ int validate_offsets_host(const int64_t* off, int64_t n, GraphStats* gs) {
         return;
       }
       gs_add(s, d);
+      if (d >= kHPiece) bigs[static_cast<size_t>(t)].push_back(static_cast<int>(v));
     }
     part[static_cast<size_t>(t)] = s;
   };
@@ -887,6 +902,10 @@ int validate_offsets_host(const int64_t* off, int64_t n, GraphStats* gs) {
     }
   }
   *gs = tot;
+  if (big_rows) {
+    big_rows->clear();
+    for (const auto& b : bigs) big_rows->insert(big_rows->end(), b.begin(), b.end());
+  }
   return GCOL_OK;
 }
 
@@ -1027,7 +1046,24 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
   }
   tmark("enqueue");
   if (memory == GCOL_MEM_HOST) {  // validation + degree statistics overlap the upload
-    if (int vr = validate_offsets_host(offsets, n, &g->gs)) return bail(vr);
+    std::vector<int> big;
+    if (int vr = validate_offsets_host(offsets, n, &g->gs, &big)) return bail(vr);
+    if (!big.empty()) {  // the verification's piece plan, from the host copy
+      std::vector<int> pre(big.size() + 1, 0);
+      for (size_t j = 0; j < big.size(); ++j) {
+        const int64_t d = offsets[big[j] + 1] - offsets[big[j]];
+        pre[j + 1] = pre[j] + static_cast<int>((d + kHPiece - 1) / kHPiece);
+      }
+      if (dalloc(&g->d_vrows, big.size(), g->stream) != cudaSuccess ||
+          dalloc(&g->d_vpre, pre.size(), g->stream) != cudaSuccess ||
+          cudaMemcpyAsync(g->d_vrows, big.data(), sizeof(int) * big.size(), cudaMemcpyHostToDevice,
+                          g->stream) != cudaSuccess ||
+          cudaMemcpyAsync(g->d_vpre, pre.data(), sizeof(int) * pre.size(), cudaMemcpyHostToDevice,
+                          g->stream) != cudaSuccess)
+        return bail(fail(GCOL_ERR_CUDA, "verification plan upload failed"));
+      g->nvrows = static_cast<int>(big.size());
+    }
+    g->vplan_done = true;
   } else {
     GraphStats* d_gs = nullptr;
     if (dalloc(&d_gs, 1, g->stream) != cudaSuccess) return bail(fail(GCOL_ERR_CUDA, "alloc"));
@@ -1082,6 +1118,7 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
       cudaFreeAsync(g->d_cols, g->stream);
     }
     if (g->d_iota) cudaFreeAsync(g->d_iota, g->stream);
+    if (g->d_vacc) cudaFreeAsync(g->d_vacc, g->stream);
     for (void* p : {static_cast<void*>(g->d_hq), static_cast<void*>(g->d_hslot),
                     static_cast<void*>(g->d_hslot_bm), static_cast<void*>(g->d_vrows),
                     static_cast<void*>(g->d_vpre)})

@@ -338,14 +338,19 @@ struct VerifyAcc {
 __global__ void __launch_bounds__(kBlock) k_verify_count(const long long* __restrict__ off,
                                                          const int* __restrict__ cols, int n,
                                                          const int* colors, VerifyAcc* acc,
-                                                         int* vcount, int big_min) {
-  // rows with deg >= big_min (a piece plan exists) are left to k_verify_big
+                                                         int* vcount, int big_min,
+                                                         unsigned* census, int census_max) {
+  // rows with deg >= big_min (a piece plan exists) are left to k_verify_big;
+  // colours 0..census_max are also marked in `census` (count_colors)
   constexpr int U = 4;
+  constexpr int kLocalWords = 128;
   __shared__ unsigned long long s_acc[4];
   __shared__ int s_max;
+  __shared__ unsigned s_bits[kLocalWords];
   const int lane = lane_id();
   if (threadIdx.x < 4) s_acc[threadIdx.x] = 0ull;
   if (threadIdx.x == 0) s_max = -1;
+  for (int i = threadIdx.x; i < kLocalWords; i += blockDim.x) s_bits[i] = 0u;
   __syncthreads();
   unsigned long long unc = 0, conf = 0, oob = 0, neg = 0;
   int mx = -1;
@@ -370,6 +375,10 @@ __global__ void __launch_bounds__(kBlock) k_verify_count(const long long* __rest
         if (c < -1 || c > deg) oob++;
         if (c < -1) neg++;
         if (c > mx) mx = c;
+        if (census && c >= 0 && c <= census_max) {
+          if (c < kLocalWords * 32) atomicOr(&s_bits[c >> 5], 1u << (c & 31));
+          else atomicOr(&census[c >> 5], 1u << (c & 31));
+        }
         big = deg > 32;
       }
     }
@@ -421,6 +430,9 @@ __global__ void __launch_bounds__(kBlock) k_verify_count(const long long* __rest
   atomicAdd(&s_acc[3], neg);
   atomicMax(&s_max, mx);
   __syncthreads();
+  if (census)
+    for (int i = threadIdx.x; i < kLocalWords && i * 32 <= census_max; i += blockDim.x)
+      if (s_bits[i]) atomicOr(&census[i], s_bits[i]);
   if (threadIdx.x == 0) {
     atomicAdd(&acc->uncolored, s_acc[0]);
     atomicAdd(&acc->conflict_edges, s_acc[1]);
