@@ -31,8 +31,7 @@ namespace dev {
 
 constexpr int kCW = 8;                    // consumer warps per CTA (narrow variant)
 constexpr int kCWWide = 16;               // consumer warps per CTA (wide variant)
-// producer warps (TMA bulk copies, alternate chunks); one keeps up with
-// both variants since the single-window staging
+// producer warps (TMA bulk copies)
 template <int CW>
 constexpr int k1_producers() {
   return 1;
@@ -799,15 +798,12 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
     long long pt_slot = 0, pt_drift = 0, pt_load = 0, pchunks = 0;
     const bool contig = worklist == nullptr;
     const long long m = ld_off(off + n, pol);  // adjacency length
-    // the first kSlots chunks' offsets; later ones are requested by the
-    // consumer warp that frees the slot
-    constexpr int kPW = k1_producers<CW>();
-    const int pw = warp - kCW;  // this producer stages chunks k = pw (mod kPW)
+    // offsets of the first chunk; each later chunk's go out one chunk ahead,
+    // as soon as its slot is free
     if (lane == 0 && contig)
-      for (int j = pw; j < kSlots; j += kPW)
-        k1_request_offsets<CW>(sm.slot[j], off, (blockIdx.x + j * G) * S.cstride + S.coffset,
-                               nitems, item0, n, pol);
-    for (int k = pw;; k += kPW) {
+      k1_request_offsets<CW>(sm.slot[0], off, blockIdx.x * S.cstride + S.coffset, nitems, item0,
+                             n, pol);
+    for (int k = 0;; ++k) {
       const int cl = blockIdx.x + k * G;                // local chunk index
       const int c = cl * S.cstride + S.coffset;         // global chunk index
       const int si = k % kSlots;
@@ -831,8 +827,16 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
       const int c0 = c * kChunk;
       const int rows = min(kChunk, nitems - c0);
       if (contig) {
-        mbar_wait(&sl.offb, par);              // offsets of chunk k (every lane; the
-                                               // slot was freed before they were requested)
+        mbar_wait(&sl.offb, par);              // offsets of chunk k (every lane)
+        if (lane == 0) {  // chunk k+1's offsets go out as soon as its slot is free
+          const int kn = k + 1;
+          if (kn >= kSlots)
+            while (*reinterpret_cast<volatile int*>(&s_consumed[kn % kSlots]) < kCW * (kn / kSlots))
+              __nanosleep(64);
+          k1_request_offsets<CW>(sm.slot[kn % kSlots], off,
+                                 (blockIdx.x + kn * G) * S.cstride + S.coffset, nitems, item0, n,
+                                 pol);
+        }
         if (S.piece_ready) {  // streamed upload: the chunk's adjacency must be resident
           const long long lo = sl.offs[0], hi = sl.offs[rows];
           if (lane == 0 && hi > lo)
@@ -1041,13 +1045,7 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
       __syncwarp();
       if (lane == 0) {
         const int old = atomicAdd(&s_consumed[si], 1);
-        if (old % kCW == kCW - 1) {  // last warp out: the slot is free
-          if (S.done_chunks) atomicAdd(S.done_chunks, 1u);
-          if (!worklist)
-            k1_request_offsets<CW>(sm.slot[si], off,
-                                   (blockIdx.x + (k + kSlots) * G) * S.cstride + S.coffset,
-                                   nitems, item0, n, pol);
-        }
+        if (old % kCW == kCW - 1 && S.done_chunks) atomicAdd(S.done_chunks, 1u);
       }
       t = -1;
       ++cnt;
