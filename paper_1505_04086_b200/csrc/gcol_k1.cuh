@@ -297,6 +297,18 @@ __device__ __forceinline__ void k1_medium(const int* __restrict__ cols, const in
   // so: offset of the row's entries in `stage`, -1 when not staged
   const int lane = lane_id();
   const bool park_mode = kLog && redo != nullptr;
+  // entries to visit: in a sorted staged row, only the lower-id prefix
+  // (binary search in shared memory); elsewhere the whole row
+  int lcnt = deg;
+  if (kLower && med && so >= 0) {
+    int lo = 0, hi = deg;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (stage[so + mid] < v) lo = mid + 1;
+      else hi = mid;
+    }
+    lcnt = lo;
+  }
   unsigned medmask = __ballot_sync(kFull, med);
   while (medmask) {
     // rows of this batch: medium rows in lane order while their words fit
@@ -315,7 +327,7 @@ __device__ __forceinline__ void k1_medium(const int* __restrict__ cols, const in
     // rows of the batch that may park (room reserved in the redo list)
     const int rank = __popc(batch & ((1u << lane) - 1u));
     const bool parkable = park_mode && inb && (*nredo + rank) < 32;
-    const int len = inb ? deg : 0;
+    const int len = inb ? lcnt : 0;
     int eincl = len;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
