@@ -365,3 +365,15 @@ def test_catalyurek_scaled_configs(oracle_mod):
         ref = sorted(oracle_mod.color_parallel(o, 8, "catalyurek")[1]["num_colors"]
                      for _ in range(3))[1]
         assert sorted(ours)[1] <= int(1.10 * ref) + 2, (name, ours, ref)
+
+
+def test_benchmark_report_on_device():
+    from paper_1505_04086_b200 import report
+    rng = np.random.default_rng(31)
+    g = random_graph(rng, 5000, 8.0)
+    for alg in (gcol.Algorithm.rsoc, gcol.Algorithm.catalyurek, gcol.Algorithm.seq):
+        rep = report.run_benchmark(g, "er5k", alg, [1, 8], 3)
+        j = report.to_json(rep)
+        assert len(j["runs"]) == 6 and [a["thread_count"] for a in j["aggregate"]] == [1, 8]
+        assert all(r["algorithm"] == gcol.to_string(alg) for r in j["runs"])
+        assert report.csv_string(rep).count("\n") == 7
