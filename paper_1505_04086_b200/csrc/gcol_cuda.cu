@@ -1001,9 +1001,11 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
       // pieces of 2^shift entries alternate between two copy streams, so one
       // stream's DMA runs while the other publishes its flag; m/16 per piece,
       // 4M..16M entries (measured: smaller pieces lose PCIe efficiency, a
-      // single piece leaves all of K1 after the transfer)
+      // single piece leaves all of K1 after the transfer).  Below 64M entries
+      // K1 is shorter than what the pieces cost: one piece.
       int shift = 22;
       while (shift < 24 && (int64_t{1} << (shift + 5)) <= m) ++shift;
+      if (m < (int64_t{1} << 26)) shift = 31;
       if (const char* pe = std::getenv("GCOL_UPLOAD_SHIFT")) shift = std::max(10, std::atoi(pe));
       const int64_t piece = int64_t{1} << shift;
       const int64_t npieces = (m + piece - 1) / piece;
