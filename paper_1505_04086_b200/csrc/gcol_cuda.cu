@@ -7,9 +7,12 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cub/device/device_scan.cuh>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -74,6 +77,12 @@ struct ExecKey {
 };
 
 // Long-row piece queue for one split threshold (sized so it never wraps).
+// A page-locked host buffer (see take_pinned).
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
 struct SplitPlan {
   int min_deg = 0;
   int nslots = 0;
@@ -124,6 +133,7 @@ struct gcol_cuda_graph {
   int piece_shift = 0;
   cudaEvent_t ev_copied = nullptr, ev_copied2 = nullptr;
   cudaEvent_t ev_copy0 = nullptr;  // GCOL_TRACE: start of the upload
+  PinnedBuf staging{};             // narrow degrees on their way up (small graphs)
   // heavy rows of the rounds, split into pieces (Ctrl::hq ...)
   int hslots = 0, hq_cap = 0;
   int2* d_hq = nullptr;
@@ -212,6 +222,33 @@ void give_event(int dev, bool timing, cudaEvent_t e) {
   if (!e) return;
   std::lock_guard<std::mutex> lk(res_pool().mu);
   res_pool().events[timing ? 1 : 0][dev].push_back(e);
+}
+
+// Page-locked staging buffers (host), pooled like the streams.
+std::vector<PinnedBuf>& pinned_pool() {
+  static auto* v = new std::vector<PinnedBuf>();
+  return *v;
+}
+
+cudaError_t take_pinned(size_t bytes, PinnedBuf* out) {
+  {
+    std::lock_guard<std::mutex> lk(res_pool().mu);
+    auto& v = pinned_pool();
+    for (size_t i = 0; i < v.size(); ++i)
+      if (v[i].cap >= bytes) {
+        *out = v[i];
+        v.erase(v.begin() + static_cast<std::ptrdiff_t>(i));
+        return cudaSuccess;
+      }
+  }
+  out->cap = std::max<size_t>(bytes, 1 << 20);
+  return cudaMallocHost(&out->p, out->cap);
+}
+
+void give_pinned(const PinnedBuf& b) {
+  if (!b.p) return;
+  std::lock_guard<std::mutex> lk(res_pool().mu);
+  pinned_pool().push_back(b);
 }
 
 template <class T>
@@ -862,21 +899,90 @@ int gcol_cuda_ipc_close(void* dev_ptr, uint64_t offset) {
 
 namespace {
 
-// Structural checks of a host CSR (graph.hpp:50-56: offsets cover the
-// adjacency and never decrease), split over host threads; called while the
-// upload DMA runs.
-int validate_offsets_host(const int64_t* off, int64_t n, GraphStats* gs,
-                          std::vector<int>* big_rows) {
+// A persistent pool of host threads for the passes over a host CSR
+// (spawning 16 threads per call costs about as much as the pass itself).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();  // never destroyed (workers detached)
+    return *p;
+  }
+  int size() const { return static_cast<int>(workers_) + 1; }
+  // Runs fn(0..tasks-1) on the pool and the caller; returns when all are done.
+  void run(int tasks, const std::function<void(int)>& fn) {
+    std::unique_lock<std::mutex> call(call_mu_);  // one job at a time
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      tasks_ = tasks;
+      next_.store(0);
+      left_ = tasks;
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return left_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    workers_ = std::min(hw, 16u) - 1;
+    for (unsigned i = 0; i < workers_; ++i)
+      std::thread([this] {
+        uint64_t seen = 0;
+        for (;;) {
+          {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return gen_ != seen; });
+            seen = gen_;
+          }
+          drain();
+        }
+      }).detach();
+  }
+  void drain() {
+    for (;;) {
+      const int t = next_.fetch_add(1);
+      const std::function<void(int)>* fn;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (t >= tasks_ || !fn_) return;
+        fn = fn_;
+      }
+      (*fn)(t);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--left_ == 0) done_cv_.notify_all();
+    }
+  }
+  unsigned workers_ = 0;
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int tasks_ = 0, left_ = 0;
+  std::atomic<int> next_{0};
+  uint64_t gen_ = 0;
+};
+
+// One pass over host offsets (graph.hpp:50-56: they cover the adjacency and
+// never decrease) on the host pool, run while the upload DMA is in flight:
+// degree statistics, the rows verified in pieces, and optionally the
+// degrees narrowed to `width` bytes into `narrow` (*overflow set if one
+// does not fit).
+int scan_offsets_host(const int64_t* off, int64_t n, GraphStats* gs, std::vector<int>* big_rows,
+                      void* narrow, int width, bool* overflow) {
   const int64_t kPer = 1 << 18;
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const int T = static_cast<int>(std::max<int64_t>(
-      1, std::min<int64_t>({static_cast<int64_t>(hw), 16, (n + kPer - 1) / kPer})));
-  std::atomic<bool> bad{false};
+  const int T = static_cast<int>(std::max<int64_t>(1, (n + kPer - 1) / kPer));
+  std::atomic<bool> bad{false}, ovf{false};
   std::vector<GraphStats> part(static_cast<size_t>(T));
   std::vector<std::vector<int>> bigs(static_cast<size_t>(T));
-  auto work = [&](int t) {
+  const int64_t lim = width == 1 ? 0xff : (width == 2 ? 0xffff : 0xffffffffLL);
+  std::function<void(int)> work = [&](int t) {
     const int64_t lo = n * t / T, hi = n * (t + 1) / T;
     GraphStats s{};
+    bool o = false;
     for (int64_t v = lo; v < hi; ++v) {
       const int64_t d = off[v + 1] - off[v];
       if (d < 0) {
@@ -885,13 +991,17 @@ int validate_offsets_host(const int64_t* off, int64_t n, GraphStats* gs,
       }
       gs_add(s, d);
       if (d >= kHPiece) bigs[static_cast<size_t>(t)].push_back(static_cast<int>(v));
+      if (narrow) {
+        o |= d > lim;
+        if (width == 1) static_cast<uint8_t*>(narrow)[v] = static_cast<uint8_t>(d);
+        else if (width == 2) static_cast<uint16_t*>(narrow)[v] = static_cast<uint16_t>(d);
+        else static_cast<uint32_t*>(narrow)[v] = static_cast<uint32_t>(d);
+      }
     }
+    if (o) ovf.store(true, std::memory_order_relaxed);
     part[static_cast<size_t>(t)] = s;
   };
-  std::vector<std::thread> th;
-  for (int t = 1; t < T; ++t) th.emplace_back(work, t);
-  work(0);
-  for (auto& x : th) x.join();
+  HostPool::get().run(T, work);
   if (bad.load()) return fail(GCOL_ERR_INVALID_ARGUMENT, "graph: offsets are not monotone");
   GraphStats tot{};
   for (const GraphStats& s : part) {
@@ -906,7 +1016,28 @@ int validate_offsets_host(const int64_t* off, int64_t n, GraphStats* gs,
     big_rows->clear();
     for (const auto& b : bigs) big_rows->insert(big_rows->end(), b.begin(), b.end());
   }
+  if (overflow) *overflow = ovf.load();
   return GCOL_OK;
+}
+
+template <class T>
+struct Widen {
+  __host__ __device__ long long operator()(T x) const { return static_cast<long long>(x); }
+};
+
+// Device: off[0] = 0, off[v+1] = deg[0] + ... + deg[v].
+template <class T>
+cudaError_t scan_degrees(const T* d_deg, int64_t n, long long* d_off, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(d_off, 0, sizeof(long long), s);
+  if (e != cudaSuccess || n == 0) return e;
+  auto it = thrust::make_transform_iterator(d_deg, Widen<T>());
+  size_t tmp = 0;
+  if ((e = cub::DeviceScan::InclusiveSum(nullptr, tmp, it, d_off + 1, n, s)) != cudaSuccess) return e;
+  void* d_tmp = nullptr;
+  if ((e = cudaMallocAsync(&d_tmp, std::max<size_t>(tmp, 1), s)) != cudaSuccess) return e;
+  e = cub::DeviceScan::InclusiveSum(d_tmp, tmp, it, d_off + 1, n, s);
+  cudaFreeAsync(d_tmp, s);
+  return e;
 }
 
 __global__ void k_publish(unsigned* p, unsigned v) {
@@ -979,6 +1110,32 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
     gcol_cuda_graph_destroy(g);
     return code;
   };
+  // Validation (graph.hpp:50-56) + degree statistics + the verification's
+  // piece plan, from the host copy; once, while the upload runs.
+  bool validated = false;
+  auto host_validate = [&](void* narrow = nullptr, int width = 0, bool* overflow = nullptr) -> int {
+    if (validated) return GCOL_OK;
+    validated = true;
+    std::vector<int> big;
+    if (int vr = scan_offsets_host(offsets, n, &g->gs, &big, narrow, width, overflow)) return vr;
+    if (!big.empty()) {
+      std::vector<int> pre(big.size() + 1, 0);
+      for (size_t j = 0; j < big.size(); ++j) {
+        const int64_t d = offsets[big[j] + 1] - offsets[big[j]];
+        pre[j + 1] = pre[j] + static_cast<int>((d + kHPiece - 1) / kHPiece);
+      }
+      if (dalloc(&g->d_vrows, big.size(), g->stream) != cudaSuccess ||
+          dalloc(&g->d_vpre, pre.size(), g->stream) != cudaSuccess ||
+          cudaMemcpyAsync(g->d_vrows, big.data(), sizeof(int) * big.size(), cudaMemcpyHostToDevice,
+                          g->stream) != cudaSuccess ||
+          cudaMemcpyAsync(g->d_vpre, pre.data(), sizeof(int) * pre.size(), cudaMemcpyHostToDevice,
+                          g->stream) != cudaSuccess)
+        return fail(GCOL_ERR_CUDA, "verification plan upload failed");
+      g->nvrows = static_cast<int>(big.size());
+    }
+    g->vplan_done = true;
+    return GCOL_OK;
+  };
   // K1 stages the CSR with TMA bulk copies, which need 16-byte aligned
   // bases: a caller's device arrays that are not aligned are copied once.
   const bool aligned = (reinterpret_cast<uintptr_t>(offsets) & 15u) == 0 &&
@@ -1026,14 +1183,51 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
       cudaEventRecord(ev_alloc, g->stream);
       cudaStreamWaitEvent(g->copy_stream, ev_alloc, 0);
       cudaStreamWaitEvent(g->copy_stream2, ev_alloc, 0);
+      // small graphs (one piece): K1 cannot overlap the transfer anyway, so
+      // the offsets go after the adjacency as degrees narrowed to the maximum
+      // degree's width (1 byte instead of 8 on tri), which the host prepares
+      // while the adjacency is in flight
+      const bool packed = memory == GCOL_MEM_HOST && npieces <= 1 && n > 0;
       cudaEventRecord(g->ev_copy0, g->copy_stream);
-      cudaMemcpyAsync(g->d_off, offsets, off_bytes, mt, g->copy_stream);
-      cudaEventRecord(ev_off, g->copy_stream);
+      if (!packed) {
+        cudaMemcpyAsync(g->d_off, offsets, off_bytes, mt, g->copy_stream);
+        cudaEventRecord(ev_off, g->copy_stream);
+      }
       for (int64_t p = 0; p < npieces; ++p) {
         cudaStream_t cs = (p & 1) ? g->copy_stream : g->copy_stream2;
         const int64_t b = p * piece, len = std::min(piece, m - b);
         cudaMemcpyAsync(g->d_cols + b, cols + b, sizeof(int) * static_cast<size_t>(len), mt, cs);
         publish_piece(cs, g->d_ready + p);
+      }
+      if (packed) {
+        // width guessed from a sample (with a 2x margin), checked in the pass
+        int64_t smax = 0;
+        for (int64_t v = 0; v < std::min<int64_t>(n, 1 << 16); ++v)
+          smax = std::max<int64_t>(smax, offsets[v + 1] - offsets[v]);
+        int width = smax < 128 ? 1 : (smax < 32768 ? 2 : 4);
+        if (take_pinned(static_cast<size_t>(n) * 4, &g->staging) != cudaSuccess)
+          return bail(fail(GCOL_ERR_CUDA, "staging allocation failed"));
+        bool overflow = false;
+        if (int vr = host_validate(g->staging.p, width, &overflow)) return bail(vr);
+        if (overflow) {  // a degree beyond the sample's width: widen (second pass)
+          width = 4;
+          for (int64_t v = 0; v < n; ++v)
+            static_cast<uint32_t*>(g->staging.p)[v] = static_cast<uint32_t>(offsets[v + 1] - offsets[v]);
+        }
+        void* d_deg = nullptr;
+        cudaError_t es = cudaMallocAsync(&d_deg, static_cast<size_t>(n) * width, g->copy_stream);
+        if (es == cudaSuccess)
+          es = cudaMemcpyAsync(d_deg, g->staging.p, static_cast<size_t>(n) * width,
+                               cudaMemcpyHostToDevice, g->copy_stream);
+        if (es == cudaSuccess) {
+          if (width == 1) es = scan_degrees(static_cast<const uint8_t*>(d_deg), n, g->d_off, g->copy_stream);
+          else if (width == 2) es = scan_degrees(static_cast<const uint16_t*>(d_deg), n, g->d_off, g->copy_stream);
+          else es = scan_degrees(static_cast<const uint32_t*>(d_deg), n, g->d_off, g->copy_stream);
+        }
+        if (d_deg) cudaFreeAsync(d_deg, g->copy_stream);
+        if (es != cudaSuccess)
+          return bail(fail(GCOL_ERR_CUDA, std::string("degree upload: ") + cudaGetErrorString(es)));
+        cudaEventRecord(ev_off, g->copy_stream);
       }
       cudaEventRecord(g->ev_copied2, g->copy_stream2);
       cudaStreamWaitEvent(g->copy_stream, g->ev_copied2, 0);
@@ -1048,24 +1242,7 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
   }
   tmark("enqueue");
   if (memory == GCOL_MEM_HOST) {  // validation + degree statistics overlap the upload
-    std::vector<int> big;
-    if (int vr = validate_offsets_host(offsets, n, &g->gs, &big)) return bail(vr);
-    if (!big.empty()) {  // the verification's piece plan, from the host copy
-      std::vector<int> pre(big.size() + 1, 0);
-      for (size_t j = 0; j < big.size(); ++j) {
-        const int64_t d = offsets[big[j] + 1] - offsets[big[j]];
-        pre[j + 1] = pre[j] + static_cast<int>((d + kHPiece - 1) / kHPiece);
-      }
-      if (dalloc(&g->d_vrows, big.size(), g->stream) != cudaSuccess ||
-          dalloc(&g->d_vpre, pre.size(), g->stream) != cudaSuccess ||
-          cudaMemcpyAsync(g->d_vrows, big.data(), sizeof(int) * big.size(), cudaMemcpyHostToDevice,
-                          g->stream) != cudaSuccess ||
-          cudaMemcpyAsync(g->d_vpre, pre.data(), sizeof(int) * pre.size(), cudaMemcpyHostToDevice,
-                          g->stream) != cudaSuccess)
-        return bail(fail(GCOL_ERR_CUDA, "verification plan upload failed"));
-      g->nvrows = static_cast<int>(big.size());
-    }
-    g->vplan_done = true;
+    if (int vr = host_validate()) return bail(vr);
   } else {
     GraphStats* d_gs = nullptr;
     if (dalloc(&d_gs, 1, g->stream) != cudaSuccess) return bail(fail(GCOL_ERR_CUDA, "alloc"));
@@ -1108,6 +1285,7 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
   give_event(g->device, true, g->ev_copied);
   give_event(g->device, false, g->ev_copied2);
   give_event(g->device, true, g->ev_copy0);
+  give_pinned(g->staging);
   if (g->d_ready && g->stream) cudaFreeAsync(g->d_ready, g->stream);
   for (auto& kv : g->execs) {
     cudaGraphExecDestroy(kv.second.second);
