@@ -134,6 +134,7 @@ struct gcol_cuda_graph {
   cudaEvent_t ev_copied = nullptr, ev_copied2 = nullptr;
   cudaEvent_t ev_copy0 = nullptr;  // GCOL_TRACE: start of the upload
   PinnedBuf staging{};             // narrow degrees on their way up (small graphs)
+  PinnedBuf out_staging{};         // narrow colours on their way down
   // heavy rows of the rounds, split into pieces (Ctrl::hq ...)
   int hslots = 0, hq_cap = 0;
   int2* d_hq = nullptr;
@@ -1020,6 +1021,23 @@ int scan_offsets_host(const int64_t* off, int64_t n, GraphStats* gs, std::vector
   return GCOL_OK;
 }
 
+// colours[v] = narrow[v] (1 or 2 bytes), on the host pool.
+void widen_colors_host(const void* narrow, int width, int32_t* colors, size_t n) {
+  const int64_t kPer = 1 << 19;
+  const int T = static_cast<int>(std::max<int64_t>(1, (static_cast<int64_t>(n) + kPer - 1) / kPer));
+  std::function<void(int)> work = [&](int t) {
+    const size_t lo = n * t / T, hi = n * (t + 1) / T;
+    if (width == 1) {
+      const uint8_t* src = static_cast<const uint8_t*>(narrow);
+      for (size_t v = lo; v < hi; ++v) colors[v] = src[v];
+    } else {
+      const uint16_t* src = static_cast<const uint16_t*>(narrow);
+      for (size_t v = lo; v < hi; ++v) colors[v] = src[v];
+    }
+  };
+  HostPool::get().run(T, work);
+}
+
 template <class T>
 struct Widen {
   __host__ __device__ long long operator()(T x) const { return static_cast<long long>(x); }
@@ -1286,6 +1304,7 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
   give_event(g->device, false, g->ev_copied2);
   give_event(g->device, true, g->ev_copy0);
   give_pinned(g->staging);
+  give_pinned(g->out_staging);
   if (g->d_ready && g->stream) cudaFreeAsync(g->d_ready, g->stream);
   for (auto& kv : g->execs) {
     cudaGraphExecDestroy(kv.second.second);
@@ -1369,11 +1388,24 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   // the colours are final here: a copy into pinned host memory overlaps the
   // verification pass below (both only read them)
   const bool early_out = colors_memory == GCOL_MEM_HOST && n > 0 && is_pinned_host(colors_out);
+  // First-Fit colours are <= the maximum degree: below 2^16 they cross PCIe
+  // narrowed (1 or 2 bytes) and are widened on the host pool
+  int out_width = 4;
   if (early_out) {
     GCOL_CK(cudaEventRecord(g->ev_final, g->stream));
     GCOL_CK(cudaStreamWaitEvent(g->out_stream, g->ev_final, 0));
-    GCOL_CK(cudaMemcpyAsync(colors_out, g->d_colors, sizeof(int) * n, cudaMemcpyDeviceToHost,
-                            g->out_stream));
+    if (g->max_degree < 65536 && n >= (size_t{1} << 20) &&
+        take_pinned(n * 2, &g->out_staging) == cudaSuccess) {
+      out_width = g->max_degree < 256 ? 1 : 2;
+      // d_marks (n ints) is free once the rounds are over
+      k_pack_colors<<<g->sms * 4, kBlock, 0, g->out_stream>>>(g->d_colors, static_cast<long long>(n),
+                                                              out_width, g->d_marks);
+      GCOL_CK(cudaMemcpyAsync(g->out_staging.p, g->d_marks, n * out_width, cudaMemcpyDeviceToHost,
+                              g->out_stream));
+    } else {
+      GCOL_CK(cudaMemcpyAsync(colors_out, g->d_colors, sizeof(int) * n, cudaMemcpyDeviceToHost,
+                              g->out_stream));
+    }
   }
   // Header + conflicts_per_round back in two copies.
   tmark("launch");
@@ -1415,10 +1447,12 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   gcol_cuda_verify_report rep{};
   if (int rc = verify_device(g, g->d_colors, &rep, nullptr, nullptr, nullptr, 0)) return rc;
   tmark("verify");
-  if (early_out)
+  if (early_out) {
     GCOL_CK(cudaStreamSynchronize(g->out_stream));
-  else if (int rc = copy_out(g, colors_out, g->d_colors, sizeof(int) * n, colors_memory))
+    if (out_width < 4) widen_colors_host(g->out_staging.p, out_width, colors_out, n);
+  } else if (int rc = copy_out(g, colors_out, g->d_colors, sizeof(int) * n, colors_memory)) {
     return rc;
+  }
   GCOL_CK(cudaStreamSynchronize(g->stream));
   tmark("out");
   if (stats) {

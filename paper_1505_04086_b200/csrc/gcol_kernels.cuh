@@ -670,6 +670,17 @@ __global__ void __launch_bounds__(kBlock) k_compact_flags(Ctrl* ctrl, const int*
   }
 }
 
+// Colours narrowed to `width` bytes for the copy to the host (all colours
+// are <= the maximum degree < 2^(8 width)).
+__global__ void k_pack_colors(const int* colors, long long n, int width, int* out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = colors[i];
+    if (width == 1) reinterpret_cast<unsigned char*>(out)[i] = (unsigned char)c;
+    else reinterpret_cast<unsigned short*>(out)[i] = (unsigned short)c;
+  }
+}
+
 __global__ void k_iota(int* p, int n) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)

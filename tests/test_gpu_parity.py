@@ -377,3 +377,19 @@ def test_benchmark_report_on_device():
         assert len(j["runs"]) == 6 and [a["thread_count"] for a in j["aggregate"]] == [1, 8]
         assert all(r["algorithm"] == gcol.to_string(alg) for r in j["runs"])
         assert report.csv_string(rep).count("\n") == 7
+
+
+def test_one_call_narrow_transfers():
+    """One-call path on a large low-degree graph: offsets go up as 1-byte
+    degrees, colours come down as 1-byte values (max degree < 256), and as
+    2-byte values on a wider graph; results as from the resident path."""
+    for off, cols in (graphs.tri_mesh(1100, 1000, 5, "cpu"),
+                      graphs.erdos_renyi(1 << 20, 300.0 / 64, 3, "cpu")):
+        h_off, h_cols = off.pin_memory(), cols.pin_memory()
+        n = off.numel() - 1
+        out = torch.full((n,), -7, dtype=torch.int32).pin_memory()
+        run = gcol.color_rsoc_csr(h_off, h_cols, 4, colors_out=out)
+        hg = gcol.Graph(off.numpy(), cols.numpy())
+        check_run(hg, gcol.ColoringRun(out.numpy(), run.stats), 4)
+        plain = gcol.color_rsoc_csr(off.numpy(), cols.numpy(), 4)  # pageable: no narrowing
+        check_run(hg, plain, 4)
