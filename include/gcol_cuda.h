@@ -95,9 +95,14 @@ typedef struct {
   int32_t k1_split_min_degree; /* rows at least this long are split into 1024-entry
                                   pieces that every warp helps colour; 0 = default
                                   (1024) */
-  int32_t k1_wide;           /* 0 auto (wide when max degree <= 16), 1 narrow (8 consumer
-                                warps per SM), 2 wide (16: twice the vertices in flight) */
-  int32_t reserved[3];
+  int32_t k1_wide;           /* initial-pass kernel: 0 auto (the waiting pass K1W when every
+                                row has degree <= 63, else wide k1_pipe when max degree
+                                <= 16, else narrow), 1 narrow k1_pipe (8 consumer warps
+                                per SM), 2 wide k1_pipe (16), 3 K1W where it applies */
+  int32_t k1_wait_polls;     /* K1W: re-checks of a row's in-flight lower neighbours before
+                                it colours past them and logs the reads for round 1;
+                                0 default (4096), < 0 none (purely optimistic) */
+  int32_t reserved[2];
 } gcol_cuda_options;
 
 /* ColoringStats (parallel.hpp:47-57) + device-side instrumentation. */

@@ -53,6 +53,7 @@ struct CudaOptions {
   bool k1_read_all = false;
   int k1_split_min_degree = 0;
   int k1_wide = 0;
+  int k1_wait_polls = 0;
 };
 
 // A gcol::Graph uploaded once to the device (reuse it across runs, like the
@@ -92,6 +93,7 @@ inline gcol_cuda_options to_c(unsigned thread_count, const ParallelOptions& opt,
   o.k1_read_all = co.k1_read_all ? 1 : 0;
   o.k1_split_min_degree = co.k1_split_min_degree;
   o.k1_wide = co.k1_wide;
+  o.k1_wait_polls = co.k1_wait_polls;
   return o;
 }
 

@@ -47,7 +47,8 @@ class Options(C.Structure):
         ("k1_read_all", C.c_int32),
         ("k1_split_min_degree", C.c_int32),
         ("k1_wide", C.c_int32),
-        ("reserved", C.c_int32 * 3),
+        ("k1_wait_polls", C.c_int32),
+        ("reserved", C.c_int32 * 2),
     ]
 
 

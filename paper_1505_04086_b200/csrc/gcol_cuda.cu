@@ -28,6 +28,7 @@
 
 #include "gcol_cuda.h"
 #include "gcol_kernels.cuh"
+#include "gcol_k1w.cuh"
 
 using namespace gcol::dev;
 
@@ -69,10 +70,10 @@ cudaError_t add_kernel(cudaGraphNode_t* node, cudaGraph_t g, const cudaGraphNode
 }
 
 struct ExecKey {
-  int rule, lower, k1_blocks, mega_min, wide;
+  int rule, lower, k1_blocks, mega_min, wide, polls;
   bool operator<(const ExecKey& o) const {
-    return std::tie(rule, lower, k1_blocks, mega_min, wide) <
-           std::tie(o.rule, o.lower, o.k1_blocks, o.mega_min, o.wide);
+    return std::tie(rule, lower, k1_blocks, mega_min, wide, polls) <
+           std::tie(o.rule, o.lower, o.k1_blocks, o.mega_min, o.wide, o.polls);
   }
 };
 
@@ -417,8 +418,9 @@ int reset_split(gcol_cuda_graph* g, const SplitPlan* P, int warps) {
 // Everything one K1 launch needs (grid, log slices, long-row queue).
 struct K1Launch {
   int grid1 = 0;
-  int cw = kCW;       // consumer warps per CTA (8 narrow, 16 wide)
+  int cw = kCW;       // consumer warps per CTA (8 narrow, 16 wide); 0: K1W
   size_t smem = 0;
+  WaitArgs W{};       // K1W (cw == 0)
   PairLogArgs L{};
   SplitArgs S{};
   const SplitPlan* plan = nullptr;
@@ -440,6 +442,49 @@ bool use_wide(const gcol_cuda_graph* g, int k1_wide) {
   if (k1_wide == 1) return false;
   if (k1_wide == 2) return true;
   return g->max_degree <= 16;
+}
+
+// K1 variant of the in-place initial pass: 0 narrow, 1 wide, 2 K1W (the
+// waiting pass, gcol_k1w.cuh; rows of degree <= kSmallMax only).  Option
+// k1_wide: 0 auto (K1W when every row is small), 1 narrow, 2 wide, 3 K1W.
+int k1_variant(const gcol_cuda_graph* g, int k1_wide) {
+  const bool small = g->max_degree <= kSmallMax;
+  if (k1_wide == 3 && small) return 2;
+  if (k1_wide == 0 && small) return 2;
+  return use_wide(g, k1_wide == 3 ? 0 : k1_wide) ? 1 : 0;
+}
+
+// option k1_wait_polls: 0 default, > 0 that many re-checks, < 0 none (every
+// stale read is logged at once, as an optimistic pass would)
+int wait_polls(int opt_polls) {
+  if (opt_polls < 0) return 0;
+  if (opt_polls > 0) return opt_polls;
+  if (const char* e = std::getenv("GCOL_K1_WAIT_POLLS")) return std::max(0, std::atoi(e));
+  return kWaitPollsDefault;
+}
+
+// K1W launch plan: a fully resident grid (every warp's tiles progress, so
+// waits on lower rows resolve), one pair-log slice per CTA.
+int plan_k1_wait(gcol_cuda_graph* g, K1Launch* K, int polls) {
+  int occ = 1;
+  if (g->d_ready)
+    GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_wait<true>, kWaitBlock, 0));
+  else
+    GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_wait<false>, kWaitBlock, 0));
+  occ = std::max(1, std::min(occ, 2048 / kWaitBlock));
+  if (const char* e = std::getenv("GCOL_K1_WAIT_BPS")) occ = std::max(1, std::min(occ, std::atoi(e)));
+  const long long tiles = (g->n + 31) / 32;
+  const long long wpb = kWaitBlock / 32;
+  K->grid1 = static_cast<int>(std::max(1LL, std::min<long long>(static_cast<long long>(g->sms) * occ,
+                                                                (tiles + wpb - 1) / wpb)));
+  K->cw = 0;
+  K->smem = 0;
+  K->plan = nullptr;
+  K->W = WaitArgs{g->d_ready, g->piece_shift, polls, 1, 0};
+  const unsigned long long per = g->pair_cap / static_cast<unsigned long long>(K->grid1);
+  K->L = PairLogArgs{g->d_pairs, static_cast<int>(std::min<unsigned long long>(per, 1u << 30)),
+                     g->d_pair_counts, &g->d_ctrl->pair_overflow};
+  return GCOL_OK;
 }
 
 template <bool kSnap, bool kLower, bool kLog, int CW>
@@ -501,16 +546,29 @@ int split_min_of(const gcol_cuda_options& opt) {
 }
 
 template <int R, bool kLower>
-int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, bool wide,
+int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int polls,
                      cudaGraph_t* out_graph, cudaGraphExec_t* out_exec) {
   K1Launch K;
-  if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K, wide)) return rc;
+  if (kLower && k1v == 2) {
+    if (int rc = plan_k1_wait(g, &K, polls)) return rc;
+  } else if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K, k1v == 1)) {
+    return rc;
+  }
   cudaGraph_t graph;
   GCOL_CK(cudaGraphCreate(&graph, 0));
   const int n = static_cast<int>(g->n);
   cudaGraphNode_t n_ev0, n_k1, n_ev1, n_cand, n_while, n_ev2;
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
-  {
+  if (K.cw == 0) {
+    void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &g->d_colors, &g->d_ctrl, &K.L, &K.W};
+    cudaKernelNodeParams p{};
+    p.func = g->d_ready ? reinterpret_cast<void*>(k1_wait<true>) : reinterpret_cast<void*>(k1_wait<false>);
+    p.gridDim = dim3(K.grid1);
+    p.blockDim = dim3(kWaitBlock);
+    p.sharedMemBytes = 0;
+    p.kernelParams = args;
+    GCOL_CK(cudaGraphAddKernelNode(&n_k1, graph, &n_ev0, 1, &p));
+  } else {
     int drift = drift_rounds(g);
     int item0 = 0;
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), const_cast<int*>(&n),
@@ -549,7 +607,7 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, bool wide
   GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle, 1));
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, graph, &n_while, 1, g->ev_end));
   GCOL_CK(cudaGraphInstantiate(out_exec, graph, 0));
-  g->k1_warps[*out_exec] = K.grid1 * K.cw;
+  g->k1_warps[*out_exec] = K.grid1 * (K.cw ? K.cw : kWaitBlock / 32);
   *out_graph = graph;
   return GCOL_OK;
 }
@@ -558,14 +616,23 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, bool wide
 // loop driven from the host.  Only for profilers that cannot see into
 // conditional graph nodes (GCOL_EAGER=1); the product path is the graph.
 template <int R, bool kLower>
-int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, bool wide) {
+int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int polls) {
   K1Launch K;
-  if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K, wide)) return rc;
-  if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
   const int n = static_cast<int>(g->n);
-  GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
-  launch_k1<false, kLower, true>(K, g->stream, g->d_off, g->d_cols, n, n, nullptr, g->d_colors,
-                                 g->d_colors, g->d_ctrl, drift_rounds(g), 0);
+  if (kLower && k1v == 2) {
+    if (int rc = plan_k1_wait(g, &K, polls)) return rc;
+    GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
+    if (g->d_ready)
+      k1_wait<true><<<K.grid1, kWaitBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors, g->d_ctrl, K.L, K.W);
+    else
+      k1_wait<false><<<K.grid1, kWaitBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors, g->d_ctrl, K.L, K.W);
+  } else {
+    if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K, k1v == 1)) return rc;
+    if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
+    GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
+    launch_k1<false, kLower, true>(K, g->stream, g->d_off, g->d_cols, n, n, nullptr, g->d_colors,
+                                   g->d_colors, g->d_ctrl, drift_rounds(g), 0);
+  }
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
   k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors,
                                                          g->d_ctrl, K.L, K.grid1, g->d_marks);
@@ -586,16 +653,16 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, bool wide) {
   return GCOL_OK;
 }
 
-int launch_eager(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, int mm, bool w) {
-  if (rule == kIdLow) return lower ? run_eager<kIdLow, true>(g, k1_blocks, mm, w) : run_eager<kIdLow, false>(g, k1_blocks, mm, w);
-  if (rule == kIdHigh) return lower ? run_eager<kIdHigh, true>(g, k1_blocks, mm, w) : run_eager<kIdHigh, false>(g, k1_blocks, mm, w);
-  if (rule == kDegId) return lower ? run_eager<kDegId, true>(g, k1_blocks, mm, w) : run_eager<kDegId, false>(g, k1_blocks, mm, w);
-  return lower ? run_eager<kOrdered, true>(g, k1_blocks, mm, w) : run_eager<kOrdered, false>(g, k1_blocks, mm, w);
+int launch_eager(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, int mm, int w, int polls) {
+  if (rule == kIdLow) return lower ? run_eager<kIdLow, true>(g, k1_blocks, mm, w, polls) : run_eager<kIdLow, false>(g, k1_blocks, mm, w, polls);
+  if (rule == kIdHigh) return lower ? run_eager<kIdHigh, true>(g, k1_blocks, mm, w, polls) : run_eager<kIdHigh, false>(g, k1_blocks, mm, w, polls);
+  if (rule == kDegId) return lower ? run_eager<kDegId, true>(g, k1_blocks, mm, w, polls) : run_eager<kDegId, false>(g, k1_blocks, mm, w, polls);
+  return lower ? run_eager<kOrdered, true>(g, k1_blocks, mm, w, polls) : run_eager<kOrdered, false>(g, k1_blocks, mm, w, polls);
 }
 
-int get_exec(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, int mm, bool w,
+int get_exec(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, int mm, int w, int polls,
              cudaGraphExec_t* exec) {
-  ExecKey key{rule, lower, k1_blocks, mm, w ? 1 : 0};
+  ExecKey key{rule, lower, k1_blocks, mm, w, polls};
   auto it = g->execs.find(key);
   if (it != g->execs.end()) {
     *exec = it->second.second;
@@ -605,17 +672,17 @@ int get_exec(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, int mm, boo
   cudaGraphExec_t ex = nullptr;
   int rc;
   if (rule == kIdLow)
-    rc = lower ? build_rsoc_graph<kIdLow, true>(g, k1_blocks, mm, w, &graph, &ex)
-               : build_rsoc_graph<kIdLow, false>(g, k1_blocks, mm, w, &graph, &ex);
+    rc = lower ? build_rsoc_graph<kIdLow, true>(g, k1_blocks, mm, w, polls, &graph, &ex)
+               : build_rsoc_graph<kIdLow, false>(g, k1_blocks, mm, w, polls, &graph, &ex);
   else if (rule == kIdHigh)
-    rc = lower ? build_rsoc_graph<kIdHigh, true>(g, k1_blocks, mm, w, &graph, &ex)
-               : build_rsoc_graph<kIdHigh, false>(g, k1_blocks, mm, w, &graph, &ex);
+    rc = lower ? build_rsoc_graph<kIdHigh, true>(g, k1_blocks, mm, w, polls, &graph, &ex)
+               : build_rsoc_graph<kIdHigh, false>(g, k1_blocks, mm, w, polls, &graph, &ex);
   else if (rule == kDegId)
-    rc = lower ? build_rsoc_graph<kDegId, true>(g, k1_blocks, mm, w, &graph, &ex)
-               : build_rsoc_graph<kDegId, false>(g, k1_blocks, mm, w, &graph, &ex);
+    rc = lower ? build_rsoc_graph<kDegId, true>(g, k1_blocks, mm, w, polls, &graph, &ex)
+               : build_rsoc_graph<kDegId, false>(g, k1_blocks, mm, w, polls, &graph, &ex);
   else
-    rc = lower ? build_rsoc_graph<kOrdered, true>(g, k1_blocks, mm, w, &graph, &ex)
-               : build_rsoc_graph<kOrdered, false>(g, k1_blocks, mm, w, &graph, &ex);
+    rc = lower ? build_rsoc_graph<kOrdered, true>(g, k1_blocks, mm, w, polls, &graph, &ex)
+               : build_rsoc_graph<kOrdered, false>(g, k1_blocks, mm, w, polls, &graph, &ex);
   if (rc != GCOL_OK) return rc;
   g->execs[key] = {graph, ex};
   *exec = ex;
@@ -1362,9 +1429,10 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   const char* eager_env = std::getenv("GCOL_EAGER");
   const bool eager = eager_env && eager_env[0] == '1';
   const int mm = split_min_of(opt);
-  const bool wide = use_wide(g, opt.k1_wide);
+  const int wide = k1_variant(g, opt.k1_wide);
+  const int polls = wait_polls(opt.k1_wait_polls);
   if (!eager)
-    if (int rc = get_exec(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide, &exec))
+    if (int rc = get_exec(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide, polls, &exec))
       return rc;
   tmark("exec");
   // Untimed prologue, like Coloring(n) before the reference's timer
@@ -1375,7 +1443,7 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   if (int rc = reset_ctrl(g, static_cast<int>(opt.round_cap), g->d_listA, g->d_listB, nullptr, 0))
     return rc;
   if (eager) {
-    if (int rc = launch_eager(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide))
+    if (int rc = launch_eager(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide, polls))
       return rc;
   } else {
     auto sp = g->splits.find(mm);

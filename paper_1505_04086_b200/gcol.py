@@ -112,6 +112,7 @@ class ParallelOptions:
     k1_read_all: bool = False
     k1_split_min_degree: int = 0
     k1_wide: int = 0
+    k1_wait_polls: int = 0
 
     def to_c(self, thread_count: int) -> _lib.Options:
         o = _lib.Options()
@@ -125,6 +126,7 @@ class ParallelOptions:
         o.k1_read_all = 1 if self.k1_read_all else 0
         o.k1_split_min_degree = self.k1_split_min_degree
         o.k1_wide = self.k1_wide
+        o.k1_wait_polls = self.k1_wait_polls
         return o
 
 

@@ -393,3 +393,74 @@ def test_one_call_narrow_transfers():
         check_run(hg, gcol.ColoringRun(out.numpy(), run.stats), 4)
         plain = gcol.color_rsoc_csr(off.numpy(), cols.numpy(), 4)  # pageable: no narrowing
         check_run(hg, plain, 4)
+
+
+# --- K1W: the waiting initial pass (gcol_k1w.cuh) ------------------------------
+def _k1w_graphs(rng):
+    """Graphs whose rows are all small (max degree <= 63): K1W's domain."""
+    out = [gcol.build_graph(np.zeros((0, 2), np.int64), 0),
+           gcol.build_graph(np.zeros((0, 2), np.int64), 1),
+           gcol.build_graph([(0, 1)], 2),
+           gcol.build_graph(np.zeros((0, 2), np.int64), 300)]  # isolated only
+    for n, avg in ((33, 3.0), (257, 8.0), (5000, 6.0), (70_001, 16.0), (200_003, 40.0)):
+        out.append(random_graph(rng, n, avg))
+    # a star of degree exactly 63 (the K1W bound) with its leaves chained
+    e = [(0, i) for i in range(1, 64)] + [(i, i + 1) for i in range(1, 63)]
+    out.append(gcol.build_graph(e, 64))
+    return [g for g in out if g.max_degree() <= 63]
+
+
+def test_k1w_is_serial_first_fit():
+    """Every wait of K1W resolves on a resident grid, so the initial pass sees
+    every lower neighbour's final colour: the result is sequential First-Fit
+    bit for bit (coloring.hpp:110-116), with no logged read and one round."""
+    rng = np.random.default_rng(1505)
+    for g in _k1w_graphs(rng):
+        ff = gcol.first_fit_sequential(g)
+        for k1_wide in (0, 3):
+            run = gcol.color_rsoc(g, 4, gcol.ParallelOptions(k1_wide=k1_wide))
+            check_run(g, run, 4)
+            assert run.stats.pairs_logged == 0
+            assert run.stats.rounds == 1 and run.stats.conflicts_per_round == [0]
+            assert np.array_equal(run.coloring, ff)
+
+
+@pytest.mark.parametrize("name", ["er", "tri", "stencil"])
+def test_k1w_configs_scaled_serial_ff(name):
+    off, cols = graphs.make_config(name, "cuda", scale_down=1)
+    g = gcol.Graph.from_device(off, cols)
+    hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
+    ff = gcol.first_fit_sequential(hg)
+    for _ in range(3):
+        run = gcol.color_rsoc(g, 1)
+        check_run(hg, run, 1)
+        assert run.stats.pairs_logged == 0
+        assert np.array_equal(run.coloring, ff)
+        # K1 gathered exactly the lower-id neighbours once: m / 2
+        assert run.stats.k1_gathers == int(off[-1]) // 2
+
+
+def test_k1w_optimistic_logging_path():
+    """k1_wait_polls < 0: K1W colours past every in-flight lower neighbour and
+    logs the read (the optimistic pass); round 1 repairs from the log."""
+    rng = np.random.default_rng(77)
+    logged = 0
+    for n, avg in ((20_000, 30.0), (300_000, 16.0), (1_000_003, 6.0)):
+        g = random_graph(rng, n, avg)
+        for prio in (gcol.Priority.degree_id, gcol.Priority.id_low, gcol.Priority.ordered):
+            run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wait_polls=-1, priority=prio))
+            check_run(g, run, 1)
+            logged += run.stats.pairs_logged
+    assert logged > 0  # the log path ran
+
+
+def test_k1w_streamed_one_call_is_serial_ff():
+    """The one-call host path with K1W following the upload pieces."""
+    off, cols = graphs.make_config("stencil", "cuda", scale_down=1)  # ~25M entries
+    h_off, h_cols = off.cpu().pin_memory(), cols.cpu().pin_memory()
+    hg = gcol.Graph(h_off.numpy(), h_cols.numpy())
+    ff = gcol.first_fit_sequential(hg)
+    out = torch.empty(off.numel() - 1, dtype=torch.int32).pin_memory()
+    run = gcol.color_rsoc_csr(h_off, h_cols, 1, colors_out=out)
+    check_run(hg, gcol.ColoringRun(out.numpy(), run.stats), 1)
+    assert np.array_equal(out.numpy(), ff)
