@@ -1125,20 +1125,19 @@ cudaError_t scan_degrees(const T* d_deg, int64_t n, long long* d_off, cudaStream
   return e;
 }
 
-__global__ void k_publish(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 
 // Publishing a resident piece: a stream memory operation executed by the
-// copy stream itself (no kernel has to be scheduled next to the running K1);
-// a one-thread release-store kernel where the driver lacks it.
+// copy stream itself, or else a 4-byte DMA copy of a pinned constant --
+// never a kernel: a kernel queued next to a running K1 that fills every SM
+// (K1W, a fully resident grid spinning on these flags) could not start.
 using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 WriteValue32Fn write_value32() {
   static WriteValue32Fn fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q{};
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+    // the _v2 entry point (CUDA >= 12.0: stream memory operations need no opt-in)
+    if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &p, 12000, cudaEnableDefault, &q) !=
+            cudaSuccess ||
         q != cudaDriverEntryPointSuccess) {
       cudaGetLastError();
       p = nullptr;
@@ -1148,11 +1147,32 @@ WriteValue32Fn write_value32() {
   return fn;
 }
 
-void publish_piece(cudaStream_t s, unsigned* flag) {
-  if (WriteValue32Fn fn = write_value32())
-    if (fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), 1u, 0) == CUDA_SUCCESS)
-      return;
-  k_publish<<<1, 1, 0, s>>>(flag, 1u);
+const unsigned* pinned_one() {
+  static unsigned* one = [] {
+    unsigned* p = nullptr;
+    if (cudaMallocHost(&p, sizeof(unsigned)) != cudaSuccess) {
+      cudaGetLastError();
+      return static_cast<unsigned*>(nullptr);
+    }
+    *p = 1u;
+    return p;
+  }();
+  return one;
+}
+
+cudaError_t publish_piece(cudaStream_t s, unsigned* flag) {
+  static bool memop_ok = true;
+  if (memop_ok)
+    if (WriteValue32Fn fn = write_value32()) {
+      if (fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), 1u, 0) == CUDA_SUCCESS)
+        return cudaSuccess;
+      memop_ok = false;  // not supported here: the DMA form from now on
+      tmark("memop-unsupported");
+    }
+  tmark("publish-dma");
+  const unsigned* one = pinned_one();
+  if (!one) return cudaErrorMemoryAllocation;
+  return cudaMemcpyAsync(flag, one, sizeof(unsigned), cudaMemcpyHostToDevice, s);
 }
 
 // Shared by graph_create and color_rsoc_csr.  `streamed`: the adjacency is
@@ -1282,7 +1302,8 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
         cudaStream_t cs = (p & 1) ? g->copy_stream : g->copy_stream2;
         const int64_t b = p * piece, len = std::min(piece, m - b);
         cudaMemcpyAsync(g->d_cols + b, cols + b, sizeof(int) * static_cast<size_t>(len), mt, cs);
-        publish_piece(cs, g->d_ready + p);
+        if (publish_piece(cs, g->d_ready + p) != cudaSuccess)
+          return bail(fail(GCOL_ERR_CUDA, "piece publication failed"));
       }
       if (packed) {
         // width guessed from a sample (with a 2x margin), checked in the pass

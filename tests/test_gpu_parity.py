@@ -454,13 +454,20 @@ def test_k1w_optimistic_logging_path():
     assert logged > 0  # the log path ran
 
 
-def test_k1w_streamed_one_call_is_serial_ff():
-    """The one-call host path with K1W following the upload pieces."""
+def test_k1w_streamed_one_call_is_serial_ff(monkeypatch):
+    """The one-call host path with K1W following the upload pieces.  Repeated
+    calls (the graph instantiation is cached after the first, so K1 starts
+    while pieces are still in flight) with 1M-entry pieces: K1W fills every SM
+    and spins on the piece flags, so publishing a piece must not need an SM
+    (a publish kernel queued behind it deadlocked)."""
     off, cols = graphs.make_config("stencil", "cuda", scale_down=1)  # ~25M entries
     h_off, h_cols = off.cpu().pin_memory(), cols.cpu().pin_memory()
     hg = gcol.Graph(h_off.numpy(), h_cols.numpy())
     ff = gcol.first_fit_sequential(hg)
     out = torch.empty(off.numel() - 1, dtype=torch.int32).pin_memory()
-    run = gcol.color_rsoc_csr(h_off, h_cols, 1, colors_out=out)
-    check_run(hg, gcol.ColoringRun(out.numpy(), run.stats), 1)
-    assert np.array_equal(out.numpy(), ff)
+    for shift in ("31", "20", "20", "20"):
+        monkeypatch.setenv("GCOL_UPLOAD_SHIFT", shift)
+        out.fill_(-7)
+        run = gcol.color_rsoc_csr(h_off, h_cols, 1, colors_out=out)
+        check_run(hg, gcol.ColoringRun(out.numpy(), run.stats), 1)
+        assert np.array_equal(out.numpy(), ff)
