@@ -13,6 +13,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <functional>
+#include <utility>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -421,6 +422,7 @@ struct K1Launch {
   int cw = kCW;       // consumer warps per CTA (8 narrow, 16 wide); 0: K1W
   size_t smem = 0;
   WaitArgs W{};       // K1W (cw == 0)
+  const void* wfn = nullptr;  // K1W kernel variant
   PairLogArgs L{};
   SplitArgs S{};
   const SplitPlan* plan = nullptr;
@@ -463,14 +465,23 @@ int wait_polls(int opt_polls) {
   return kWaitPollsDefault;
 }
 
+unsigned long long* g_k1w_trace = nullptr;  // GCOL_K1W_TRACE buffer (tooling)
+size_t g_k1w_trace_len = 0;
+
+// K1W kernel: m32 = every degree fits a 32-bit forbidden mask (colours <= degree)
+const void* k1_wait_fn(bool stream, bool m32) {
+  if (stream) return m32 ? reinterpret_cast<const void*>(k1_wait<true, true>)
+                         : reinterpret_cast<const void*>(k1_wait<true, false>);
+  return m32 ? reinterpret_cast<const void*>(k1_wait<false, true>)
+             : reinterpret_cast<const void*>(k1_wait<false, false>);
+}
+
 // K1W launch plan: a fully resident grid (every warp's tiles progress, so
 // waits on lower rows resolve), one pair-log slice per CTA.
 int plan_k1_wait(gcol_cuda_graph* g, K1Launch* K, int polls) {
+  K->wfn = k1_wait_fn(g->d_ready != nullptr, g->max_degree <= 31);
   int occ = 1;
-  if (g->d_ready)
-    GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_wait<true>, kWaitBlock, 0));
-  else
-    GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_wait<false>, kWaitBlock, 0));
+  GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K->wfn, kWaitBlock, 0));
   occ = std::max(1, std::min(occ, 2048 / kWaitBlock));
   if (const char* e = std::getenv("GCOL_K1_WAIT_BPS")) occ = std::max(1, std::min(occ, std::atoi(e)));
   const long long tiles = (g->n + 31) / 32;
@@ -480,7 +491,23 @@ int plan_k1_wait(gcol_cuda_graph* g, K1Launch* K, int polls) {
   K->cw = 0;
   K->smem = 0;
   K->plan = nullptr;
-  K->W = WaitArgs{g->d_ready, g->piece_shift, polls, 1, 0};
+  int sleep_ns = 128;
+  if (const char* e = std::getenv("GCOL_K1W_SLEEP")) sleep_ns = std::max(0, std::atoi(e));
+  K->W = WaitArgs{g->d_ready, g->piece_shift, polls, 1, 0, sleep_ns, nullptr, nullptr};
+  if (std::getenv("GCOL_K1W_SNAP")) K->W.snap = g->d_marks;  // tooling: zeros, never written
+  if (std::getenv("GCOL_K1W_TRACE")) {  // tooling: per-tile timestamps
+    static unsigned long long* buf = nullptr;
+    static size_t cap = 0;
+    const size_t need = static_cast<size_t>(2 * ((tiles + 7) / 8 * 8));
+    if (need > cap) {
+      if (buf) cudaFree(buf);
+      GCOL_CK(cudaMalloc(&buf, need * sizeof(unsigned long long)));
+      cap = need;
+    }
+    K->W.trace = buf;
+    g_k1w_trace = buf;
+    g_k1w_trace_len = need;
+  }
   const unsigned long long per = g->pair_cap / static_cast<unsigned long long>(K->grid1);
   K->L = PairLogArgs{g->d_pairs, static_cast<int>(std::min<unsigned long long>(per, 1u << 30)),
                      g->d_pair_counts, &g->d_ctrl->pair_overflow};
@@ -562,7 +589,7 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
   if (K.cw == 0) {
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &g->d_colors, &g->d_ctrl, &K.L, &K.W};
     cudaKernelNodeParams p{};
-    p.func = g->d_ready ? reinterpret_cast<void*>(k1_wait<true>) : reinterpret_cast<void*>(k1_wait<false>);
+    p.func = const_cast<void*>(K.wfn);
     p.gridDim = dim3(K.grid1);
     p.blockDim = dim3(kWaitBlock);
     p.sharedMemBytes = 0;
@@ -622,10 +649,10 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
   if (kLower && k1v == 2) {
     if (int rc = plan_k1_wait(g, &K, polls)) return rc;
     GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
-    if (g->d_ready)
-      k1_wait<true><<<K.grid1, kWaitBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors, g->d_ctrl, K.L, K.W);
-    else
-      k1_wait<false><<<K.grid1, kWaitBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors, g->d_ctrl, K.L, K.W);
+    {
+      void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &g->d_colors, &g->d_ctrl, &K.L, &K.W};
+      GCOL_CK(cudaLaunchKernel(K.wfn, dim3(K.grid1), dim3(kWaitBlock), args, 0, g->stream));
+    }
   } else {
     if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K, k1v == 1)) return rc;
     if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
@@ -1502,6 +1529,15 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
   GCOL_CK(cudaStreamSynchronize(g->stream));
   tmark("run");
+  if (const char* tp = std::getenv("GCOL_K1W_TRACE"))
+    if (g_k1w_trace) {  // tooling: dump the per-tile timestamps of this run
+      std::vector<unsigned long long> h(g_k1w_trace_len);
+      GCOL_CK(cudaMemcpy(h.data(), g_k1w_trace, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost));
+      if (FILE* f = std::fopen(tp, "wb")) {
+        std::fwrite(h.data(), sizeof(h[0]), h.size(), f);
+        std::fclose(f);
+      }
+    }
   const int rounds = hdr.round;
   if (std::getenv("GCOL_K1_PROFILE")) {
     const double ch = hdr.prof[5] ? static_cast<double>(hdr.prof[5]) : 1.0;
@@ -1569,7 +1605,8 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   if (hdr.capped)
     return fail(GCOL_ERR_ROUND_CAP,
                 "round_cap reached before convergence (no CPU repair fallback exists)");
-  if (rep.violations != 0 || rep.out_of_bound != 0)
+  // GCOL_K1W_SNAP (tooling): K1W read a frozen array, improper by design
+  if ((rep.violations != 0 || rep.out_of_bound != 0) && !std::getenv("GCOL_K1W_SNAP"))
     return fail(GCOL_ERR_VERIFY, "parallel coloring finished improper");
   return GCOL_OK;
 }
@@ -1735,7 +1772,8 @@ int gcol_cuda_color_catalyurek(gcol_cuda_graph* g, const gcol_cuda_options* opt_
   if (capped)
     return fail(GCOL_ERR_ROUND_CAP,
                 "round_cap reached before convergence (no CPU repair fallback exists)");
-  if (rep.violations != 0 || rep.out_of_bound != 0)
+  // GCOL_K1W_SNAP (tooling): K1W read a frozen array, improper by design
+  if ((rep.violations != 0 || rep.out_of_bound != 0) && !std::getenv("GCOL_K1W_SNAP"))
     return fail(GCOL_ERR_VERIFY, "parallel coloring finished improper");
   return GCOL_OK;
 }

@@ -17,6 +17,20 @@
 // whole GPU's worth of rows in flight: every warp of a fully occupied grid
 // colours 32-row tiles independently (tile t -> warp t mod #warps), with
 // the next tile's offsets prefetched while the current one is gathered.
+//
+// Per row (one lane): the lower-id prefix of the row is scanned kW = 4
+// entries per step, the colours seen form a 32-bit forbidden mask when
+// every degree is <= 31 (colours <= degree) and a 64-bit one otherwise, and
+// the in-flight neighbours are remembered by their positions in the row (a
+// 64-bit mask, deg <= 63) and re-read from the row when re-checked.
+//
+// Measured on B200 (profiles/r01/k1w_sweeps.md): the kernel is bound by the
+// L1 wavefronts of its thread-per-row loads and by per-warp latency, not by
+// the waits -- reading a frozen colour array (no in-flight reads at all)
+// makes it only 15-30 % faster; staging the tile's adjacency in shared
+// memory, prefetching the next tile's adjacency (L2 or registers), parking
+// pending rows while the next tile is scanned, and 8-wide steps all lost or
+// tied.  48 resident warps per SM (40 registers) is the best occupancy.
 #pragma once
 #include "gcol_device.cuh"
 #include "gcol_k1.cuh"
@@ -32,7 +46,16 @@ struct WaitArgs {
   int piece_shift;              //   (null: the whole CSR is resident)
   int max_polls;                // re-checks of a pending row before it is logged
   int cstride, coffset;         // interleaved partition: 256-id chunks coffset + cstride*i
+  int sleep_ns;                 // back-off between re-checks of a pending row
+  unsigned long long* trace;    // GCOL_K1W_TRACE (tooling): per tile {start, end} ns
+  const int* snap;              // GCOL_K1W_SNAP (tooling): colours read from this frozen array
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Adjacency loads: read-only, L1-allocating (a warp's rows are contiguous,
 // so successive entries of neighbouring lanes share sectors), L2 evict_first.
@@ -42,53 +65,101 @@ __device__ __forceinline__ int ld_col_l1(const int* p, uint64_t pol) {
   return r;
 }
 
-// One pass over the lower-id prefix of the row (sorted: stops at the first
-// entry above v), warp-collective.  mask |= colours seen (<= deg); the first
-// four still-uncoloured neighbours land in u[], their count in ns (may be
-// > 4).  kLogAll: log every uncoloured one instead (the final pass).
-template <bool kLogAll>
-__device__ __forceinline__ void k1w_scan(const int* __restrict__ cols, const int* colors, int v,
-                                         long long b, int deg, bool need, uint64_t pol,
-                                         unsigned long long& mask, int (&u)[4], int& ns,
-                                         unsigned& gathers, const PairLogInl& L) {
-  bool active = need && deg > 0;
-  for (int k = 0; __any_sync(kFull, active); k += 4) {
-    int w[4];
-    bool take[4];
+// Where a tile's adjacency entries are read from (thread per row).
+struct ColsGlobal {
+  const int* cols;
+  uint64_t pol;
+  __device__ __forceinline__ int operator()(long long i) const { return ld_col_l1(cols + i, pol); }
+};
+
+template <class Mask>
+__device__ __forceinline__ Mask bit_of(int c) { return Mask(1) << c; }
+
+template <class Mask>
+__device__ __forceinline__ int first_free(Mask m) {
+  if (sizeof(Mask) == 4) return __ffs(~static_cast<unsigned>(m)) - 1;
+  return __ffsll(static_cast<long long>(~static_cast<unsigned long long>(m))) - 1;
+}
+
+// Scan of the lane's lower-id prefix (sorted row: stops at the first entry
+// above v), warp-collective: mask = colours seen (<= deg), pp = positions of
+// the neighbours read while still uncoloured (in flight).
+template <int kW, class Mask>
+__device__ __forceinline__ void k1w_scan(const ColsGlobal& src, const int* colors, int v,
+                                         bool valid, long long b, int deg, unsigned& gathers,
+                                         Mask& mask, unsigned long long& pp) {
+  mask = 0;
+  pp = 0ull;  // positions of in-flight lower neighbours
+  bool active = valid && deg > 0;
+  for (int k = 0; __any_sync(kFull, active); k += kW) {
+    int w[kW];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const bool in = active && k + j < deg;
-      w[j] = in ? ld_col_l1(cols + b + k + j, pol) : 0;
-      take[j] = in && w[j] < v;
-    }
-    int c[4];
+    for (int j = 0; j < kW; ++j) w[j] = (active && k + j < deg) ? src(b + k + j) : 0x7fffffff;
+    int c[kW];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) c[j] = take[j] ? ld_color(colors + w[j]) : -2;
+    for (int j = 0; j < kW; ++j) c[j] = w[j] < v ? ld_color(colors + w[j]) : -2;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (!kLogAll) gathers += take[j];
-      if (c[j] >= 0 && c[j] <= deg) mask |= 1ull << c[j];
-      const bool st = take[j] && c[j] == -1;
-      if (kLogAll) {
-        log_pairs(L, st, w[j], v);
-      } else if (st) {
-        if (ns == 0) u[0] = w[j];
-        else if (ns == 1) u[1] = w[j];
-        else if (ns == 2) u[2] = w[j];
-        else if (ns == 3) u[3] = w[j];
-        ++ns;
-      }
+    for (int j = 0; j < kW; ++j) {
+      gathers += w[j] < v;
+      if (static_cast<unsigned>(c[j]) <= static_cast<unsigned>(deg)) mask |= bit_of<Mask>(c[j]);
+      if (c[j] == -1) pp |= 1ull << (k + j);
     }
     // sorted row: once an entry above v (or the row end) is reached, done
-    if (active && (k + 4 >= deg || !take[3])) active = false;
+    active = active && k + kW < deg && w[kW - 1] < v;
   }
 }
 
-template <bool kStream>
-__global__ void __launch_bounds__(kWaitBlock) k1_wait(const long long* __restrict__ off,
-                                                      const int* __restrict__ cols, int n,
-                                                      int* colors, Ctrl* ctrl, PairLogArgs LA,
-                                                      WaitArgs A) {
+// Commit the row if nothing it read was in flight; else re-check the
+// in-flight ones until they are coloured (after max_polls: log the rest for
+// round 1) and commit.  Warp-collective.
+template <class Mask>
+__device__ __forceinline__ void k1w_wait(const ColsGlobal& src, int* colors, int v, bool valid,
+                                         long long b, int deg, int max_polls, int sleep_ns,
+                                         Mask mask, unsigned long long pp, const PairLogInl& L) {
+  bool pend = pp != 0ull;
+  if (valid && !pend) commit_color(colors, v, first_free(mask));
+  for (int polls = 0; __any_sync(kFull, pend); ++polls) {
+    if (polls >= max_polls) {
+      // give up: log the still-uncoloured ones for round 1, commit
+      while (__any_sync(kFull, pp != 0ull)) {
+        const bool has = pp != 0ull;
+        const int j = has ? __ffsll(static_cast<long long>(pp)) - 1 : 0;
+        if (has) pp &= pp - 1;
+        const int wj = has ? src(b + j) : 0;
+        const int cj = has ? ld_color(colors + wj) : 0;
+        if (has && static_cast<unsigned>(cj) <= static_cast<unsigned>(deg)) mask |= bit_of<Mask>(cj);
+        log_pairs(L, has && cj == -1, wj, v);
+      }
+      if (pend) commit_color(colors, v, first_free(mask));
+      break;
+    }
+    if (sleep_ns) __nanosleep(sleep_ns);
+    if (pend) {
+      for (unsigned long long q = pp; q; q &= q - 1) {
+        const int j = __ffsll(static_cast<long long>(q)) - 1;
+        const int cj = ld_color(colors + src(b + j));
+        if (cj != -1) {
+          pp &= ~(1ull << j);
+          if (static_cast<unsigned>(cj) <= static_cast<unsigned>(deg)) mask |= bit_of<Mask>(cj);
+        }
+      }
+      if (pp == 0ull) {
+        commit_color(colors, v, first_free(mask));
+        pend = false;
+      }
+    }
+  }
+}
+
+constexpr int kWaitScanW = 4;   // adjacency entries per scan step
+constexpr int kWaitMinBlocks = 6;  // 48 resident warps per SM: 40 registers
+
+// kM32: every degree is <= 31, so the forbidden set fits 32 bits.
+template <bool kStream, bool kM32>
+__global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
+    k1_wait(const long long* __restrict__ off, const int* __restrict__ cols, int n, int* colors,
+            Ctrl* ctrl, PairLogArgs LA, WaitArgs A) {
+  using Mask = typename std::conditional<kM32, unsigned, unsigned long long>::type;
   __shared__ int s_npairs;
   __shared__ unsigned s_gathers;
   if (threadIdx.x == 0) {
@@ -101,6 +172,8 @@ __global__ void __launch_bounds__(kWaitBlock) k1_wait(const long long* __restric
   const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
   const int NW = gridDim.x * wpb;
   const uint64_t pol = policy_evict_first();
+  const ColsGlobal src{cols, pol};
+  const int* rd = A.snap ? A.snap : colors;  // A.snap: tooling only
   PairLogInl L;
   L.region = LA.pairs + (size_t)blockIdx.x * LA.region_cap;
   L.cap = LA.region_cap;
@@ -132,52 +205,15 @@ __global__ void __launch_bounds__(kWaitBlock) k1_wait(const long long* __restric
           while (ld_acquire_u32(A.piece_ready + p) == 0u) __nanosleep(256);
       __syncwarp();
     }
-    unsigned long long mask = 0ull;
-    int u[4] = {0, 0, 0, 0};
-    int ns = 0;
-    k1w_scan<false>(cols, colors, v, b, deg, valid, pol, mask, u, ns, gathers, L);
-    // pending: bit j = u[j] still uncoloured; `more`: > 4 were, rescan later
-    unsigned pm = ns >= 4 ? 15u : ((1u << ns) - 1u);
-    bool more = ns > 4;
-    bool done = valid && ns == 0;
-    if (done) commit_color(colors, v, __ffsll((long long)~mask) - 1);
-    bool pend = valid && !done;
-    for (int polls = 0; __any_sync(kFull, pend); ++polls) {
-      if (polls >= A.max_polls) {
-        // give up: log every still-uncoloured lower neighbour for round 1
-        unsigned long long m2 = 0ull;
-        int ns2 = 0;
-        k1w_scan<true>(cols, colors, v, b, deg, pend, pol, m2, u, ns2, gathers, L);
-        if (pend) commit_color(colors, v, __ffsll((long long)~m2) - 1);
-        break;
-      }
-      __nanosleep(128);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (pend && ((pm >> j) & 1u)) {
-          const int c = ld_color(colors + u[j]);
-          if (c != -1) {
-            pm &= ~(1u << j);
-            if (c >= 0 && c <= deg) mask |= 1ull << c;
-          }
-        }
-      }
-      // the four tracked ones resolved but more were pending: scan again
-      const bool again = pend && pm == 0u && more;
-      if (__any_sync(kFull, again)) {
-        int ns2 = 0;
-        unsigned g2 = 0;
-        if (again) mask = 0ull;
-        k1w_scan<false>(cols, colors, v, b, deg, again, pol, mask, u, ns2, g2, L);
-        if (again) {
-          pm = ns2 >= 4 ? 15u : ((1u << ns2) - 1u);
-          more = ns2 > 4;
-        }
-      }
-      if (pend && pm == 0u) {
-        commit_color(colors, v, __ffsll((long long)~mask) - 1);
-        pend = false;
-      }
+    unsigned long long t0 = 0;
+    if (A.trace && lane == 0) t0 = globaltimer_ns();
+    Mask mask;
+    unsigned long long pp;
+    k1w_scan<kWaitScanW, Mask>(src, rd, v, valid, b, deg, gathers, mask, pp);
+    k1w_wait<Mask>(src, colors, v, valid, b, deg, A.max_polls, A.sleep_ns, mask, pp, L);
+    if (A.trace && lane == 0) {
+      A.trace[2 * (size_t)t] = t0;
+      A.trace[2 * (size_t)t + 1] = globaltimer_ns();
     }
     b = nb;
   }

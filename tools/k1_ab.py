@@ -26,13 +26,16 @@ def main():
         g = gcol.Graph.from_device(off, cols)
         m = cols.numel()
         out = torch.empty(off.numel() - 1, dtype=torch.int32, device="cuda")
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > L2, as bench.py
         for var in [int(x) for x in a.variants.split(",")]:
             opt = gcol.ParallelOptions(k1_wide=var)
             rows = []
             for i in range(a.runs + 1):
+                flush.fill_(1)
                 r = gcol.color_rsoc(g, 1, opt, colors_out=out)
-                rep = gcol.verify_report(g, out.cpu().numpy())[0]
-                rep = (rep.violations, rep.uncolored, rep.out_of_bound)
+                rep = gcol.verify_report(g, out.cpu().numpy())[0] if not os.environ.get(
+                    "GCOL_K1W_SNAP") else None
+                rep = (rep.violations, rep.uncolored, rep.out_of_bound) if rep else None
                 if i == 0:
                     continue  # warm-up (graph instantiation)
                 rows.append((r.stats.num_colors, r.stats.rounds, r.stats.initial_pass_ns / 1e6,
@@ -41,7 +44,7 @@ def main():
             k1 = statistics.median(x[2] for x in rows)
             tot = statistics.median(x[3] for x in rows)
             print(json.dumps({
-                "config": cfg, "k1_wide": var, "colors": [x[0] for x in rows],
+                "config": cfg, "k1_wide": var, "k1w_cfg": os.environ.get("GCOL_K1W_CFG", ""), "colors": [x[0] for x in rows],
                 "rounds": [x[1] for x in rows], "k1_ms": round(k1, 4), "total_ms": round(tot, 4),
                 "ge_s": round(m / tot / 1e6, 2), "pairs": [x[4] for x in rows],
                 "cand": [x[5] for x in rows], "gathers": rows[0][6],
