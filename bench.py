@@ -368,7 +368,10 @@ def run_ours(args):
         tot = float(t.item())
     ms_per_step = tot / args.steps * 1e3
     value = world * m / (tot / args.steps) / 1e9
-    launches = sum(2 + 3 * r.stats.rounds for r in runs)
+    # K1 + k_candidates, then k_list + k_heavy + k_control per round; K1W
+    # (max degree <= 63) skips the loop when it logged nothing
+    launches = sum(2 + (0 if (maxdeg <= 63 and r.stats.pairs_logged == 0) else 3 * r.stats.rounds)
+                   for r in runs)
     colors = [r.stats.num_colors for r in runs]
     rounds = [r.stats.rounds for r in runs]
     last = runs[-1].stats
@@ -381,7 +384,8 @@ def run_ours(args):
     peak, peak_src = measured_peak()
     traffic = profile_traffic(args.config)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "kernel": "k1_pipe",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "k1_wait" if maxdeg <= 63 else "k1_pipe",
                 "algorithmic_bytes_per_launch": k1_bytes,
                 "bytes_formula": "8(n+1) offsets + 4m cols + 4*gathers (lower-id neighbour "
                                  "colours) + 4n colour stores",

@@ -585,8 +585,14 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
   GCOL_CK(cudaGraphCreate(&graph, 0));
   const int n = static_cast<int>(g->n);
   cudaGraphNode_t n_ev0, n_k1, n_ev1, n_cand, n_while, n_ev2;
+  // handle: the round loop (WHILE); K1W's last CTA clears it when nothing
+  // was logged (gcol_k1w.cuh).  (Also skipping k_candidates with an IF node
+  // measured no gain: the conditional node costs what the kernel does.)
+  cudaGraphConditionalHandle handle;
+  GCOL_CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
   if (K.cw == 0) {
+    K.W.loop = static_cast<unsigned long long>(handle);
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &g->d_colors, &g->d_ctrl, &K.L, &K.W};
     cudaKernelNodeParams p{};
     p.func = const_cast<void*>(K.wfn);
@@ -616,8 +622,6 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
                      g->d_off, g->d_cols, n, static_cast<const int*>(g->d_colors), g->d_ctrl, K.L,
                      K.grid1, g->d_marks));
 
-  cudaGraphConditionalHandle handle;
-  GCOL_CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
   cudaGraphNodeParams cp{};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = handle;

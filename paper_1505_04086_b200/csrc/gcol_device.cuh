@@ -70,6 +70,7 @@ struct Ctrl {
   int* hslot_left;                  // pieces not finished yet
   int* hslot_flag;                  // 1: the row is defective
   unsigned* hslot_bm;               // [hslots][kBWinWords] colours seen, 0..16383
+  unsigned k1_ctas_done;            // K1W: CTAs finished (the last one may end the run)
   unsigned long long prof[16];      // K1 phase cycle counters (GCOL_K1_PROFILE)
   unsigned long long cpr[kMaxRoundsRecorded];  // conflicts_per_round
 };

@@ -49,6 +49,7 @@ struct WaitArgs {
   int sleep_ns;                 // back-off between re-checks of a pending row
   unsigned long long* trace;    // GCOL_K1W_TRACE (tooling): per tile {start, end} ns
   const int* snap;              // GCOL_K1W_SNAP (tooling): colours read from this frozen array
+  unsigned long long loop;      // the round loop's WHILE handle (0: eager, no graph)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -225,6 +226,25 @@ __global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
     if (s_gathers) atomicAdd(&ctrl->k1_gathers, (unsigned long long)s_gathers);
     LA.counts[blockIdx.x] = min(s_npairs, LA.region_cap);
     atomicAdd(&ctrl->pair_len, (unsigned long long)s_npairs);
+    if (A.loop) {
+      // The last CTA to finish: with nothing logged (every in-flight read was
+      // waited for -- the usual case) round 1's worklist is empty, so it
+      // closes round 1 with no conflicts as k_control would
+      // (finish_round, parallel.hpp:140-154) and the graph skips the loop
+      // (k_candidates finds nothing to do).
+      __threadfence();
+      if (atomicAdd(&ctrl->k1_ctas_done, 1u) == gridDim.x - 1) {
+        __threadfence();
+        const unsigned long long pairs = atomicAdd(&ctrl->pair_len, 0ull);
+        const int ovf = atomicAdd(&ctrl->pair_overflow, 0);
+        if (pairs == 0ull && ovf == 0) {
+          ctrl->round = 1;
+          ctrl->cpr[0] = 0ull;
+          ctrl->done = 1;
+          cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(A.loop), 0u);
+        }
+      }
+    }
   }
 }
 
