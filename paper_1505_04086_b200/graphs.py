@@ -142,29 +142,107 @@ def stencil27(nx: int, ny: int, nz: int, seed: int, device="cpu"):
     return csr_from_edges(perm[u], perm[v], n)
 
 
+def _rmat_samples(scale: int, a: float, b: float, c: float, seed: int, s0: int, s1: int, device):
+    """Samples s0..s1-1 of the quadrant descent (one uniform draw per level)."""
+    ab, abc = a + b, a + b + c
+    idx = torch.arange(s0, s1, dtype=torch.int64, device=device)
+    u = torch.zeros_like(idx)
+    v = torch.zeros_like(idx)
+    for level in range(scale):
+        r = uniform01(seed, idx * scale + level, 3)
+        u = (u << 1) | (r >= ab).to(torch.int64)
+        v = (v << 1) | (((r >= a) & (r < ab)) | (r >= abc)).to(torch.int64)
+    return u, v
+
+
 def rmat(scale: int, edge_factor: int, a: float, b: float, c: float, seed: int, device="cpu",
-         chunk: int = 1 << 26):
+         chunk: int = 1 << 26, lean: bool = None):
     """R-MAT by recursive quadrant descent (generate_rmat, rmat.hpp:82-117):
     edge_factor * 2^scale samples, one uniform draw per level, then
-    symmetrise/dedup/drop loops; ids randomly permuted (shuffle_vertices)."""
+    symmetrise/dedup/drop loops; ids randomly permuted (shuffle_vertices).
+    Above 2^28 samples (scale 27: 2^31 samples, ~4.3 G directed entries) the
+    bucketed builder keeps the peak memory near 4x the adjacency."""
     n = 1 << scale
     samples = edge_factor * n
-    ab, abc = a + b, a + b + c
+    if lean is None:
+        lean = samples > (1 << 28)
+    perm = random_permutation(n, seed, device)
+    if lean:
+        return _rmat_csr_bucketed(scale, samples, a, b, c, seed, perm, device, chunk)
     us, vs = [], []
     for s0 in range(0, samples, chunk):
-        idx = torch.arange(s0, min(samples, s0 + chunk), dtype=torch.int64, device=device)
-        u = torch.zeros_like(idx)
-        v = torch.zeros_like(idx)
-        for level in range(scale):
-            r = uniform01(seed, idx * scale + level, 3)
-            u = (u << 1) | (r >= ab).to(torch.int64)
-            v = (v << 1) | (((r >= a) & (r < ab)) | (r >= abc)).to(torch.int64)
+        u, v = _rmat_samples(scale, a, b, c, seed, s0, min(samples, s0 + chunk), device)
         us.append(u)
         vs.append(v)
     u, v = torch.cat(us), torch.cat(vs)
     del us, vs
-    perm = random_permutation(n, seed, device)
     return csr_from_edges(perm[u], perm[v], n)
+
+
+def _rmat_csr_bucketed(scale, samples, a, b, c, seed, perm, device, chunk, nbuckets=None):
+    """The same canonical CSR as csr_from_edges(perm[u], perm[v]) without
+    materialising the edge list several times: directed keys src*n + dst
+    (both directions of every non-loop sample) are counted, then scattered,
+    per bucket of source ids (two passes over the counter-based samples),
+    and each bucket is sorted and deduplicated on its own.  Deduplicating
+    directed keys is deduplicating undirected pairs, since every pair
+    contributes both of its directions."""
+    n = 1 << scale
+    if nbuckets is None:
+        nbuckets = 64 if scale >= 20 else 4
+    shift = max(scale - (nbuckets.bit_length() - 1), 0)
+
+    def directed(s0, s1):
+        u, v = _rmat_samples(scale, a, b, c, seed, s0, s1, device)
+        u, v = perm[u], perm[v]
+        keep = u != v
+        u, v = u[keep], v[keep]
+        src = torch.cat([u, v])
+        dst = torch.cat([v, u])
+        return src, dst
+
+    counts = torch.zeros(nbuckets, dtype=torch.int64, device=device)
+    for s0 in range(0, samples, chunk):
+        src, _ = directed(s0, min(samples, s0 + chunk))
+        counts += torch.bincount(src >> shift, minlength=nbuckets)
+    starts = torch.zeros(nbuckets + 1, dtype=torch.int64, device=device)
+    torch.cumsum(counts, 0, out=starts[1:])
+    keys = torch.empty(int(starts[-1]), dtype=torch.int64, device=device)
+    cursor = starts[:-1].clone()
+    for s0 in range(0, samples, chunk):
+        src, dst = directed(s0, min(samples, s0 + chunk))
+        bkt = src >> shift
+        order = torch.argsort(bkt, stable=True)
+        k = (src * n + dst)[order]
+        bc = torch.bincount(bkt, minlength=nbuckets)
+        pos = torch.zeros(nbuckets + 1, dtype=torch.int64, device=device)
+        torch.cumsum(bc, 0, out=pos[1:])
+        for j, (p0, p1, cur) in enumerate(zip(pos[:-1].tolist(), pos[1:].tolist(), cursor.tolist())):
+            if p1 > p0:
+                keys[cur:cur + p1 - p0] = k[p0:p1]
+        cursor += bc
+        del src, dst, bkt, order, k
+    deg = torch.zeros(n, dtype=torch.int64, device=device)
+    col_parts = []
+    total = 0
+    for j in range(nbuckets):
+        kb = keys[int(starts[j]):int(starts[j + 1])]
+        if kb.numel() == 0:
+            continue
+        kb = torch.unique_consecutive(torch.sort(kb).values)
+        deg += torch.bincount(kb // n, minlength=n)
+        col_parts.append((kb % n).to(torch.int32))
+        total += kb.numel()
+    del keys
+    cols = torch.empty(total, dtype=torch.int32, device=device)
+    o = 0
+    for part in col_parts:
+        cols[o:o + part.numel()] = part
+        o += part.numel()
+    del col_parts
+    off = torch.zeros(n + 1, dtype=torch.int64, device=device)
+    torch.cumsum(deg, 0, out=off[1:])
+    return off, cols
 
 
 @dataclass(frozen=True)

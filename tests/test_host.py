@@ -110,6 +110,19 @@ def test_generators_valid_and_deterministic():
     assert cols.numel() == 2 * (3 * 900 + 6 * 810 + 4 * 729)
 
 
+def test_rmat_bucketed_builder_is_the_same_csr():
+    """The memory-lean bucketed R-MAT builder (used above 2^28 samples, i.e.
+    BASELINE configs[4], scale 27) yields exactly the canonical CSR of the
+    direct build, for several bucket counts and chunk sizes."""
+    from paper_1505_04086_b200 import graphs
+    o1, c1 = graphs.rmat(12, 16, .57, .19, .19, 7, lean=False)
+    perm = graphs.random_permutation(1 << 12, 7, "cpu")
+    for nb, chunk in ((1, 1 << 20), (8, 1 << 11), (64, 5000)):
+        o2, c2 = graphs._rmat_csr_bucketed(12, 16 << 12, .57, .19, .19, 7, perm, "cpu", chunk,
+                                           nbuckets=nb)
+        assert torch.equal(o1, o2) and torch.equal(c1, c2)
+
+
 def test_generators_reference_build_parity(oracle_mod):
     """Our torch CSR construction == the reference's build_graph on the same pairs."""
     from paper_1505_04086_b200 import graphs
