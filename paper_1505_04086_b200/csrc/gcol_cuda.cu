@@ -470,17 +470,10 @@ size_t g_k1w_trace_len = 0;
 
 // K1W kernel: m32 = every degree fits a 32-bit forbidden mask (colours <= degree)
 const void* k1_wait_fn(bool stream, bool m32) {
-  const bool v4 = !std::getenv("GCOL_K1W_SCALAR");  // tooling: the scalar scan for A/B
-  static const void* tab[2][2][2] = {
-      {{reinterpret_cast<const void*>(k1_wait<false, false, false>),
-        reinterpret_cast<const void*>(k1_wait<false, false, true>)},
-       {reinterpret_cast<const void*>(k1_wait<false, true, false>),
-        reinterpret_cast<const void*>(k1_wait<false, true, true>)}},
-      {{reinterpret_cast<const void*>(k1_wait<true, false, false>),
-        reinterpret_cast<const void*>(k1_wait<true, false, true>)},
-       {reinterpret_cast<const void*>(k1_wait<true, true, false>),
-        reinterpret_cast<const void*>(k1_wait<true, true, true>)}}};
-  return tab[stream ? 1 : 0][m32 ? 1 : 0][v4 ? 1 : 0];
+  if (stream) return m32 ? reinterpret_cast<const void*>(k1_wait<true, true>)
+                         : reinterpret_cast<const void*>(k1_wait<true, false>);
+  return m32 ? reinterpret_cast<const void*>(k1_wait<false, true>)
+             : reinterpret_cast<const void*>(k1_wait<false, false>);
 }
 
 // K1W launch plan: a fully resident grid (every warp's tiles progress, so

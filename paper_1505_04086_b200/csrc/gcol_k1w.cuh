@@ -28,8 +28,9 @@
 // L1 wavefronts of its thread-per-row loads and by per-warp latency, not by
 // the waits -- reading a frozen colour array (no in-flight reads at all)
 // makes it only 15-30 % faster; staging the tile's adjacency in shared
-// memory, prefetching the next tile's adjacency (L2 or registers), parking
-// pending rows while the next tile is scanned, and 8-wide steps all lost or
+// memory, 16-byte vector loads of aligned row chunks (1.4-1.8x slower),
+// prefetching the next tile's adjacency (L2 or registers), parking pending
+// rows while the next tile is scanned, and 8-wide steps all lost or
 // tied.  48 resident warps per SM (40 registers) is the best occupancy.
 #pragma once
 #include "gcol_device.cuh"
@@ -110,60 +111,6 @@ __device__ __forceinline__ void k1w_scan(const ColsGlobal& src, const int* color
   }
 }
 
-__device__ __forceinline__ int4 ld_col_v4_l1(const int* p, uint64_t pol) {
-  int4 r;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
-  return r;
-}
-
-// The same scan in 16-byte aligned chunks: one 4-entry vector load per lane
-// per step (entries of the neighbouring rows inside the chunk are masked
-// off).  A warp's rows are contiguous, so a step's 32 lanes touch the same
-// ~6 cache lines whether they load 4 bytes or 16: a quarter of the L1 tag
-// requests of the scalar scan for the same entries.  Needs a 16-byte
-// aligned `cols` (graph creation guarantees it); nothing at or past `mtot`
-// is read.
-template <class Mask>
-__device__ __forceinline__ void k1w_scan_v4(const ColsGlobal& src, const int* colors, int v,
-                                            bool valid, long long b, int deg, long long mtot,
-                                            unsigned& gathers, Mask& mask,
-                                            unsigned long long& pp) {
-  mask = 0;
-  pp = 0ull;
-  const long long e = b + deg;
-  bool active = valid && deg > 0;
-  for (long long a = b & ~3LL; __any_sync(kFull, active); a += 4) {
-    int w[4];
-    if (active) {
-      if (a + 4 <= mtot) {
-        const int4 x = ld_col_v4_l1(src.cols + a, src.pol);
-        w[0] = x.x;
-        w[1] = x.y;
-        w[2] = x.z;
-        w[3] = x.w;
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) w[j] = a + j < mtot ? src(a + j) : 0x7fffffff;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (!(active && a + j >= b && a + j < e)) w[j] = 0x7fffffff;
-    int c[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) c[j] = w[j] < v ? ld_color(colors + w[j]) : -2;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      gathers += w[j] < v;
-      if (static_cast<unsigned>(c[j]) <= static_cast<unsigned>(deg)) mask |= bit_of<Mask>(c[j]);
-      if (c[j] == -1) pp |= 1ull << static_cast<int>(a + j - b);
-    }
-    // sorted row: once an entry above v (or the row end) is reached, done
-    active = active && a + 4 < e && w[3] < v;
-  }
-}
-
 // Commit the row if nothing it read was in flight; else re-check the
 // in-flight ones until they are coloured (after max_polls: log the rest for
 // round 1) and commit.  Warp-collective.
@@ -210,7 +157,7 @@ constexpr int kWaitScanW = 4;   // adjacency entries per scan step
 constexpr int kWaitMinBlocks = 6;  // 48 resident warps per SM: 40 registers
 
 // kM32: every degree is <= 31, so the forbidden set fits 32 bits.
-template <bool kStream, bool kM32, bool kV4>
+template <bool kStream, bool kM32>
 __global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
     k1_wait(const long long* __restrict__ off, const int* __restrict__ cols, int n, int* colors,
             Ctrl* ctrl, PairLogArgs LA, WaitArgs A) {
@@ -243,7 +190,6 @@ __global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
   int t = gw;
   long long b = 0;
   if (t < ntiles) b = ld_off(off + min(tile_v0(t) + lane, n), pol);
-  const long long mtot = kV4 ? ld_off(off + n, pol) : 0;
   for (; t < ntiles; t += NW) {
     const int v = tile_v0(t) + lane;
     const bool valid = v < n;
@@ -265,8 +211,7 @@ __global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
     if (A.trace && lane == 0) t0 = globaltimer_ns();
     Mask mask;
     unsigned long long pp;
-    if (kV4) k1w_scan_v4<Mask>(src, rd, v, valid, b, deg, mtot, gathers, mask, pp);
-    else k1w_scan<kWaitScanW, Mask>(src, rd, v, valid, b, deg, gathers, mask, pp);
+    k1w_scan<kWaitScanW, Mask>(src, rd, v, valid, b, deg, gathers, mask, pp);
     k1w_wait<Mask>(src, colors, v, valid, b, deg, A.max_polls, A.sleep_ns, mask, pp, L);
     if (A.trace && lane == 0) {
       A.trace[2 * (size_t)t] = t0;

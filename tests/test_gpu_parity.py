@@ -410,15 +410,10 @@ def _k1w_graphs(rng):
     return [g for g in out if g.max_degree() <= 63]
 
 
-@pytest.mark.parametrize("scan", ["vector", "scalar"])
-def test_k1w_is_serial_first_fit(scan, monkeypatch):
+def test_k1w_is_serial_first_fit():
     """Every wait of K1W resolves on a resident grid, so the initial pass sees
     every lower neighbour's final colour: the result is sequential First-Fit
-    bit for bit (coloring.hpp:110-116), with no logged read and one round.
-    Both row scans: 16-byte aligned chunks (the default; rows start anywhere,
-    and graphs with m % 4 == 2 end mid-chunk) and scalar loads."""
-    if scan == "scalar":
-        monkeypatch.setenv("GCOL_K1W_SCALAR", "1")
+    bit for bit (coloring.hpp:110-116), with no logged read and one round."""
     rng = np.random.default_rng(1505)
     graphs_ = _k1w_graphs(rng)
     assert any(int(g.offsets()[-1]) % 4 == 2 for g in graphs_)
