@@ -493,8 +493,7 @@ int plan_k1_wait(gcol_cuda_graph* g, K1Launch* K, int polls) {
   K->plan = nullptr;
   int sleep_ns = 128;
   if (const char* e = std::getenv("GCOL_K1W_SLEEP")) sleep_ns = std::max(0, std::atoi(e));
-  K->W = WaitArgs{g->d_ready, g->piece_shift, polls, 1, 0, sleep_ns, nullptr, nullptr};
-  if (std::getenv("GCOL_K1W_SNAP")) K->W.snap = g->d_marks;  // tooling: zeros, never written
+  K->W = WaitArgs{g->d_ready, g->piece_shift, polls, 1, 0, sleep_ns, nullptr, 0ull};
   if (std::getenv("GCOL_K1W_TRACE")) {  // tooling: per-tile timestamps
     static unsigned long long* buf = nullptr;
     static size_t cap = 0;
@@ -1609,8 +1608,7 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   if (hdr.capped)
     return fail(GCOL_ERR_ROUND_CAP,
                 "round_cap reached before convergence (no CPU repair fallback exists)");
-  // GCOL_K1W_SNAP (tooling): K1W read a frozen array, improper by design
-  if ((rep.violations != 0 || rep.out_of_bound != 0) && !std::getenv("GCOL_K1W_SNAP"))
+  if (rep.violations != 0 || rep.out_of_bound != 0)
     return fail(GCOL_ERR_VERIFY, "parallel coloring finished improper");
   return GCOL_OK;
 }
@@ -1776,8 +1774,7 @@ int gcol_cuda_color_catalyurek(gcol_cuda_graph* g, const gcol_cuda_options* opt_
   if (capped)
     return fail(GCOL_ERR_ROUND_CAP,
                 "round_cap reached before convergence (no CPU repair fallback exists)");
-  // GCOL_K1W_SNAP (tooling): K1W read a frozen array, improper by design
-  if ((rep.violations != 0 || rep.out_of_bound != 0) && !std::getenv("GCOL_K1W_SNAP"))
+  if (rep.violations != 0 || rep.out_of_bound != 0)
     return fail(GCOL_ERR_VERIFY, "parallel coloring finished improper");
   return GCOL_OK;
 }

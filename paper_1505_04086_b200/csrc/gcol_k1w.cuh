@@ -49,7 +49,6 @@ struct WaitArgs {
   int cstride, coffset;         // interleaved partition: 256-id chunks coffset + cstride*i
   int sleep_ns;                 // back-off between re-checks of a pending row
   unsigned long long* trace;    // GCOL_K1W_TRACE (tooling): per tile {start, end} ns
-  const int* snap;              // GCOL_K1W_SNAP (tooling): colours read from this frozen array
   unsigned long long loop;      // the round loop's WHILE handle (0: eager, no graph)
 };
 
@@ -175,7 +174,6 @@ __global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
   const int NW = gridDim.x * wpb;
   const uint64_t pol = policy_evict_first();
   const ColsGlobal src{cols, pol};
-  const int* rd = A.snap ? A.snap : colors;  // A.snap: tooling only
   PairLogInl L;
   L.region = LA.pairs + (size_t)blockIdx.x * LA.region_cap;
   L.cap = LA.region_cap;
@@ -211,7 +209,7 @@ __global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
     if (A.trace && lane == 0) t0 = globaltimer_ns();
     Mask mask;
     unsigned long long pp;
-    k1w_scan<kWaitScanW, Mask>(src, rd, v, valid, b, deg, gathers, mask, pp);
+    k1w_scan<kWaitScanW, Mask>(src, colors, v, valid, b, deg, gathers, mask, pp);
     k1w_wait<Mask>(src, colors, v, valid, b, deg, A.max_polls, A.sleep_ns, mask, pp, L);
     if (A.trace && lane == 0) {
       A.trace[2 * (size_t)t] = t0;
