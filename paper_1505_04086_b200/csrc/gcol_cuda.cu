@@ -428,6 +428,16 @@ struct K1Launch {
   const SplitPlan* plan = nullptr;
 };
 
+// CTAs per SM of k_heavy (the split heavy rows of a round): GCOL_HEAVY_GRID
+// overrides for experiments.
+int heavy_grid() {
+  static const int v = [] {
+    const char* e = std::getenv("GCOL_HEAVY_GRID");
+    return e ? std::max(1, std::min(8, std::atoi(e))) : kHeavyGridPerSM;
+  }();
+  return v;
+}
+
 // K1 drift bound in rounds: on for skewed-degree graphs, where CTAs run at
 // uneven speeds and the colour count is sensitive to it; off for bounded
 // degree (GCOL_K1_DRIFT overrides for experiments; 0 = off).
@@ -638,7 +648,7 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
   cudaGraphNode_t b_list, b_heavy, b_ctl;
   GCOL_CK(add_kernel(&b_list, body, nullptr, 0, k_list<R, false>, dim3(g->sms * 4), dim3(kBlock),
                      g->d_off, g->d_cols, g->d_colors, g->d_ctrl, g->d_heavy, g->d_marks));
-  GCOL_CK(add_kernel(&b_heavy, body, &b_list, 1, k_heavy<R, false>, dim3(g->sms * 2),
+  GCOL_CK(add_kernel(&b_heavy, body, &b_list, 1, k_heavy<R, false>, dim3(g->sms * heavy_grid()),
                      dim3(kBlock), g->d_off, g->d_cols, g->d_colors, g->d_ctrl,
                      static_cast<const int*>(g->d_heavy), g->d_marks));
   GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle, 1));
@@ -676,7 +686,7 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
   for (;;) {
     k_list<R, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
                                                             g->d_ctrl, g->d_heavy, g->d_marks);
-    k_heavy<R, false><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
+    k_heavy<R, false><<<g->sms * heavy_grid(), kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
                                                              g->d_ctrl, g->d_heavy, g->d_marks);
     k_control<<<1, 1, 0, g->stream>>>(g->d_ctrl, cudaGraphConditionalHandle{}, 0);
     GCOL_CK(cudaGetLastError());
@@ -1704,7 +1714,7 @@ int run_catalyurek(gcol_cuda_graph* g, const gcol_cuda_options& opt,
     if (nin > 0) {
       k_list<R, true><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
                                                              g->d_ctrl, g->d_heavy, g->d_marks);
-      k_heavy<R, true><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
+      k_heavy<R, true><<<g->sms * heavy_grid(), kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
                                                               g->d_ctrl, g->d_heavy, g->d_marks);
       k_compact_flags<<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_ctrl, in, nin, g->d_marks);
     }
@@ -1881,7 +1891,7 @@ template <int R, bool kDetect>
 void launch_round(gcol_cuda_graph* g) {
   k_list<R, kDetect><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
                                                             g->d_ctrl, g->d_heavy, g->d_marks);
-  k_heavy<R, kDetect><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
+  k_heavy<R, kDetect><<<g->sms * heavy_grid(), kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
                                                              g->d_ctrl, g->d_heavy, g->d_marks);
 }
 
@@ -2191,13 +2201,13 @@ int gcol_cuda_round_list(gcol_cuda_graph* g, int32_t priority, int32_t* colors_d
     const int r = rule_of(priority);
     if (r == kIdLow) {
       k_list<kIdLow, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
-      k_heavy<kIdLow, false><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
+      k_heavy<kIdLow, false><<<g->sms * heavy_grid(), kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
     } else if (r == kIdHigh) {
       k_list<kIdHigh, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
-      k_heavy<kIdHigh, false><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
+      k_heavy<kIdHigh, false><<<g->sms * heavy_grid(), kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
     } else {  // degree_id (ordered needs per-round marks; treated as degree_id here)
       k_list<kDegId, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
-      k_heavy<kDegId, false><<<g->sms * 2, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
+      k_heavy<kDegId, false><<<g->sms * heavy_grid(), kBlock, 0, g->stream>>>(g->d_off, g->d_cols, colors_dev, g->d_ctrl, g->d_heavy, g->d_marks);
     }
   }
   GCOL_CK(cudaGetLastError());

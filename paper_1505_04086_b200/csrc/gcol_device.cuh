@@ -23,6 +23,7 @@ constexpr int kStage = 1024;            // staged adjacency entries per warp (4 
 constexpr int kStageStep = kStage - 64; // rows starting in a batch always fit the stage
 constexpr int kBWinWords = 512;         // block window: 16384 colours (2 KB)
 constexpr int kHPiece = 4096;           // entries per piece of a heavy row in the rounds
+constexpr int kHeavyGridPerSM = 2;      // k_heavy CTAs per SM
 constexpr int kMaxRoundsRecorded = 1 << 16;
 constexpr unsigned kFull = 0xffffffffu;
 
