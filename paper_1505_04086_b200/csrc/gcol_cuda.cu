@@ -2095,18 +2095,35 @@ int gcol_cuda_k1_owned(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, int3
   GCOL_CK(cudaSetDevice(g->device));
   if (int rc = ensure_run_buffers(g)) return rc;
   K1Launch K;
-  if (int rc = plan_k1<false, true, true>(g, opt.k1_blocks_per_sm, split_min_of(opt), &K, false))
-    return rc;
-  K.S.cstride = g->part_world;
-  K.S.coffset = g->part_rank;
   const int n = static_cast<int>(g->n);
+  // bounded degree: the waiting pass K1W on the owned chunks.  A row waits
+  // for an in-flight lower neighbour of any rank (its colour arrives in the
+  // local replica by the owner's push); waits are bounded by k1_wait_polls,
+  // after which the read is logged as in the optimistic pass, so a rank that
+  // starts late costs time, never correctness.
+  const bool wait = k1_variant(g, opt.k1_wide) == 2;
+  if (wait) {
+    if (int rc = plan_k1_wait(g, &K, wait_polls(opt.k1_wait_polls))) return rc;
+    K.W.cstride = g->part_world;
+    K.W.coffset = g->part_rank;
+  } else {
+    if (int rc = plan_k1<false, true, true>(g, opt.k1_blocks_per_sm, split_min_of(opt), &K, false))
+      return rc;
+    K.S.cstride = g->part_world;
+    K.S.coffset = g->part_rank;
+  }
   if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, nullptr, 0)) return rc;
-  if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
+  if (!wait)
+    if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
   if (int rc = set_peers(g, true)) return rc;
   GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
-  if (n > 0)
+  if (n > 0 && wait) {
+    void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &colors_dev, &g->d_ctrl, &K.L, &K.W};
+    GCOL_CK(cudaLaunchKernel(K.wfn, dim3(K.grid1), dim3(kWaitBlock), args, 0, g->stream));
+  } else if (n > 0) {
     launch_k1<false, true, true>(K, g->stream, g->d_off, g->d_cols, n, n, nullptr, colors_dev,
                                  colors_dev, g->d_ctrl, drift_rounds(g), 0);
+  }
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
   GCOL_CK(cudaGetLastError());
   if (int rc = set_peers(g, false)) return rc;

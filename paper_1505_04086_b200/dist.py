@@ -264,6 +264,15 @@ def color_rsoc_partitioned(ops, colors: torch.Tensor, n: int, rank: int, world: 
     _sync(colors)
     dist.barrier(group=group)                      # every K1 push performed
     cand = ops.candidates(colors)
+    # the usual case with the waiting initial pass: nothing was logged on any
+    # rank, so round 1's worklist is empty everywhere -- one all-reduce ends
+    # the run (finish_round with |R_1| = 0, parallel.hpp:140-154)
+    cnt = torch.tensor([cand.numel()], dtype=torch.int64, device=colors.device)
+    dist.all_reduce(cnt, group=group)
+    if int(cnt.item()) == 0:
+        st.rounds, st.conflicts_per_round, st.conflicts_total = 1, [0], 0
+        st.barrier_events = 2
+        return st
     allc = _all_gather_var(cand.to(torch.int32), world, group)
     every = torch.cat(allc) if allc else cand
     work = torch.unique(every[owner_of(every.long(), world) == rank]).to(torch.int32)

@@ -193,10 +193,13 @@ def test_partition_bounds():
             assert all(lo % 256 == 0 for lo, _ in parts)
 
 
-@pytest.mark.parametrize("seed,n,avg,world", [(4, 900, 6.0, 2), (5, 2000, 14.0, 2), (6, 1300, 5.0, 3)])
+@pytest.mark.parametrize("seed,n,avg,world", [(4, 900, 6.0, 2), (5, 2000, 14.0, 2), (6, 1300, 5.0, 3),
+                                               (7, 200, 5.0, 2)])
 def test_push_mode_world(seed, n, avg, world):
     """Push mode: interleaved 256-id chunks, commits written into every
-    replica, candidates gathered once, count all-reduced per round."""
+    replica, candidates gathered once, count all-reduced per round.  n = 200:
+    one chunk, so nothing is read in flight and the empty-candidate exit
+    (one all-reduce, rounds = 1) runs."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

@@ -75,7 +75,11 @@ def emulate_push(off, cols, n, P, priority=gcol.Priority.degree_id):
     (no rank waits on another): rank r's handle pushes every colour it
     commits into the other ranks' replicas through their device pointers,
     the same stores that go over NVLink between GPUs."""
-    ops = [gdist.DeviceOps(gcol.Graph.from_device(off, cols), priority=int(priority))
+    # no rank may wait on another here (they run one after another): the
+    # waiting initial pass is told not to wait (k1_wait_polls < 0), so every
+    # in-flight read of another rank's row is logged, as optimistic RSOC does
+    opt = gcol.ParallelOptions(priority=priority, k1_wait_polls=-1)
+    ops = [gdist.DeviceOps(gcol.Graph.from_device(off, cols), priority=int(priority), opt=opt)
            for _ in range(P)]
     reps = [torch.full((n,), -1, dtype=torch.int32, device="cuda") for _ in range(P)]
     ptrs = [t.data_ptr() for t in reps]
@@ -124,3 +128,20 @@ def test_push_mode_skewed_graph():
     c = reps[0].cpu().numpy()
     assert gcol.verify_coloring(hg, c).ok()
     assert (c <= np.diff(hg.offsets())).all()
+
+
+def test_push_mode_one_rank_k1w_is_serial_ff():
+    """Bounded degree under the partition (world of one): the owned-chunk
+    initial pass is K1W, which waits instead of logging -- serial First-Fit,
+    no candidates, one empty round."""
+    off, cols = graphs.erdos_renyi(50_000, 12, 4, "cuda")
+    n = off.numel() - 1
+    hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
+    assert hg.max_degree() <= 63
+    ops = gdist.DeviceOps(gcol.Graph.from_device(off, cols), priority=int(gcol.Priority.degree_id))
+    colors = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+    ops.partition(0, 1, [colors.data_ptr()])
+    ops.k1_owned(colors)
+    torch.cuda.synchronize()
+    assert ops.candidates(colors).numel() == 0
+    assert np.array_equal(colors.cpu().numpy(), gcol.first_fit_sequential(hg))
