@@ -259,15 +259,19 @@ def run_distributed(args):
     if push:  # peers' replicas mapped into this process (CUDA IPC over NVLink)
         peer_ptrs, unmap = gdist.map_peer_replicas(ops, colors, rank, world)
 
+    if push:
+        ops.partition(rank, world, peer_ptrs)
+
     def step():
         colors.fill_(-1)
         flush.fill_(1)
         torch.cuda.synchronize()
-        dist.barrier()
+        dist.barrier()  # every replica initialised (step 1 of push mode)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         if push:
-            st = gdist.color_rsoc_partitioned(ops, colors, n, rank, world, peer_ptrs)
+            st = gdist.color_rsoc_partitioned(ops, colors, n, rank, world, peer_ptrs,
+                                              initialized=True)
         else:
             st = gdist.color_rsoc_distributed(ops, colors, n, rank, world)
         e1.record()

@@ -140,7 +140,10 @@ class DeviceOps:
 
     def candidates(self, colors: torch.Tensor) -> torch.Tensor:
         """Round-1 candidates (any owner) from this GPU's K1 log."""
-        out = torch.empty(max(colors.numel(), 1), dtype=torch.int32, device=colors.device)
+        out = getattr(self, "_cand_buf", None)
+        if out is None or out.numel() < max(colors.numel(), 1) or out.device != colors.device:
+            out = torch.empty(max(colors.numel(), 1), dtype=torch.int32, device=colors.device)
+            self._cand_buf = out
         k = C.c_int64(0)
         self._check(self._lib.LIB.gcol_cuda_candidates(self.h, self.priority,
                                                        C.c_void_p(colors.data_ptr()),
@@ -251,15 +254,19 @@ def map_peer_replicas(ops, colors: torch.Tensor, rank: int, world: int, group=No
 
 
 def color_rsoc_partitioned(ops, colors: torch.Tensor, n: int, rank: int, world: int,
-                           peer_ptrs: List[int], group=None, round_cap: int = 1000) -> DistStats:
+                           peer_ptrs: List[int], group=None, round_cap: int = 1000,
+                           initialized: bool = False) -> DistStats:
     """Push-mode RSOC (module docstring).  `colors` (int32[n]) is this rank's
     replica, `peer_ptrs[q]` rank q's replica as seen from this process; on
-    return every replica holds the full final colouring."""
+    return every replica holds the full final colouring.  initialized=True:
+    the caller has already set every replica to -1 and passed a barrier
+    after it (step 1), with the partition set."""
     st = DistStats()
-    colors.fill_(-1)
-    ops.partition(rank, world, peer_ptrs)
-    _sync(colors)
-    dist.barrier(group=group)                      # every replica initialised
+    if not initialized:
+        colors.fill_(-1)
+        ops.partition(rank, world, peer_ptrs)
+        _sync(colors)
+        dist.barrier(group=group)                  # every replica initialised
     st.k1_ms = ops.k1_owned(colors)
     _sync(colors)
     dist.barrier(group=group)                      # every K1 push performed
