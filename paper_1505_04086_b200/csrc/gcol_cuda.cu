@@ -609,6 +609,7 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
   if (K.cw == 0) {
     K.W.loop = static_cast<unsigned long long>(handle);
+    K.W.close_round = 1;
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &g->d_colors, &g->d_ctrl, &K.L, &K.W};
     cudaKernelNodeParams p{};
     p.func = const_cast<void*>(K.wfn);
@@ -668,6 +669,7 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
   const int n = static_cast<int>(g->n);
   if (kLower && k1v == 2) {
     if (int rc = plan_k1_wait(g, &K, polls)) return rc;
+    K.W.close_round = 1;  // as in the graph: nothing logged -> round 1 closed, no loop
     GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
     {
       void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &g->d_colors, &g->d_ctrl, &K.L, &K.W};
@@ -683,6 +685,16 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
   k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors,
                                                          g->d_ctrl, K.L, K.grid1, g->d_marks);
+  if (K.cw == 0) {  // K1W may have closed round 1 already
+    int done = 0;
+    GCOL_CK(cudaMemcpyAsync(&done, &g->d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost,
+                            g->stream));
+    GCOL_CK(cudaStreamSynchronize(g->stream));
+    if (done) {
+      GCOL_CK(cudaEventRecord(g->ev_end, g->stream));
+      return GCOL_OK;
+    }
+  }
   for (;;) {
     k_list<R, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
                                                             g->d_ctrl, g->d_heavy, g->d_marks);

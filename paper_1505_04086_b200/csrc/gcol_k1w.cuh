@@ -49,7 +49,8 @@ struct WaitArgs {
   int cstride, coffset;         // interleaved partition: 256-id chunks coffset + cstride*i
   int sleep_ns;                 // back-off between re-checks of a pending row
   unsigned long long* trace;    // GCOL_K1W_TRACE (tooling): per tile {start, end} ns
-  unsigned long long loop;      // the round loop's WHILE handle (0: eager, no graph)
+  unsigned long long loop;      // the round loop's WHILE handle (0: none)
+  int close_round;              // the last CTA closes round 1 when nothing was logged
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
     if (s_gathers) atomicAdd(&ctrl->k1_gathers, (unsigned long long)s_gathers);
     LA.counts[blockIdx.x] = min(s_npairs, LA.region_cap);
     atomicAdd(&ctrl->pair_len, (unsigned long long)s_npairs);
-    if (A.loop) {
+    if (A.close_round) {
       // The last CTA to finish: with nothing logged (every in-flight read was
       // waited for -- the usual case) round 1's worklist is empty, so it
       // closes round 1 with no conflicts as k_control would
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
           ctrl->round = 1;
           ctrl->cpr[0] = 0ull;
           ctrl->done = 1;
-          cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(A.loop), 0u);
+          if (A.loop) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(A.loop), 0u);
         }
       }
     }
