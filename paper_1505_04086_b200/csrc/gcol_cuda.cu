@@ -1220,12 +1220,12 @@ const unsigned* pinned_one() {
 }
 
 cudaError_t publish_piece(cudaStream_t s, unsigned* flag) {
-  static bool memop_ok = true;
-  if (memop_ok)
+  static std::atomic<bool> memop_ok{true};
+  if (memop_ok.load(std::memory_order_relaxed))
     if (WriteValue32Fn fn = write_value32()) {
       if (fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), 1u, 0) == CUDA_SUCCESS)
         return cudaSuccess;
-      memop_ok = false;  // not supported here: the DMA form from now on
+      memop_ok.store(false, std::memory_order_relaxed);  // unsupported here: the DMA form from now on
       tmark("memop-unsupported");
     }
   tmark("publish-dma");
