@@ -47,7 +47,8 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-I", CSRC, "-I", os.path.join(REPO, "include"),
+    extra = os.environ.get("GCOL_NVCC_EXTRA", "").split()  # experiments, e.g. -DGCOL_DEBUG_HEAVY
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-shared", "-I", CSRC, "-I", os.path.join(REPO, "include"),
            "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or res.returncode != 0:

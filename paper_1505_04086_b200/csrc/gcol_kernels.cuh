@@ -301,6 +301,10 @@ __global__ void __launch_bounds__(kBlock) k_heavy(const long long* __restrict__ 
 __global__ void k_control(Ctrl* ctrl, cudaGraphConditionalHandle handle, int in_graph) {
   const int r = ctrl->round + 1;
   ctrl->round = r;
+#ifdef GCOL_DEBUG_HEAVY  // experiments: GCOL_NVCC_EXTRA=-DGCOL_DEBUG_HEAVY
+  printf("round %d in_len %d heavy_slots %d heavy_len %d pieces %d recolored %d\n", r, ctrl->in_len,
+         ctrl->heavy_slots, ctrl->heavy_len, ctrl->heavy_pieces, ctrl->recolored);
+#endif
   const int found = ctrl->out_len;  // next worklist (recoloured + pushed)
   if (r == 1) ctrl->cand_total = ctrl->in_len;
   if (r - 1 < kMaxRoundsRecorded) ctrl->cpr[r - 1] = (unsigned long long)ctrl->recolored;
