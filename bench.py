@@ -375,9 +375,10 @@ def run_ours(args):
         tot = float(t.item())
     ms_per_step = tot / args.steps * 1e3
     value = world * m / (tot / args.steps) / 1e9
-    # K1 + k_candidates, then k_list + k_heavy + k_control per round; K1W
-    # (max degree <= 63) skips the loop when it logged nothing
-    launches = sum(2 + (0 if (maxdeg <= 63 and r.stats.pairs_logged == 0) else 3 * r.stats.rounds)
+    # K1 + k_candidates, then k_list + k_heavy + k_control per round; with
+    # K1W (max degree <= 63) that logged nothing, K1W alone (the rest of its
+    # graph is launched only when a read was logged)
+    launches = sum(1 if (maxdeg <= 63 and r.stats.pairs_logged == 0) else 2 + 3 * r.stats.rounds
                    for r in runs)
     colors = [r.stats.num_colors for r in runs]
     rounds = [r.stats.rounds for r in runs]

@@ -125,6 +125,9 @@ struct gcol_cuda_graph {
   Ctrl* d_ctrl = nullptr;
   cudaEvent_t ev_start = nullptr, ev_k1 = nullptr, ev_end = nullptr;
   std::map<ExecKey, std::pair<cudaGraph_t, cudaGraphExec_t>> execs;
+  // K1W runs: the head graph holds only the initial pass; its tail (round-1
+  // candidates + the round loop) runs only if the pass logged a read
+  std::map<cudaGraphExec_t, std::pair<cudaGraph_t, cudaGraphExec_t>> tails;
   std::map<int, SplitPlan> splits;
   std::map<cudaGraphExec_t, int> k1_warps;  // K1 warps of each instantiated graph
   // streamed upload (gcol_cuda_color_rsoc_csr): the adjacency arrives in
@@ -601,14 +604,20 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
   GCOL_CK(cudaGraphCreate(&graph, 0));
   const int n = static_cast<int>(g->n);
   cudaGraphNode_t n_ev0, n_k1, n_ev1, n_cand, n_while, n_ev2;
-  // handle: the round loop (WHILE); K1W's last CTA clears it when nothing
-  // was logged (gcol_k1w.cuh).  (Also skipping k_candidates with an IF node
-  // measured no gain: the conditional node costs what the kernel does.)
-  cudaGraphConditionalHandle handle;
-  GCOL_CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
+  // K1W (K.cw == 0) logs nothing when every wait resolved -- the usual case --
+  // and its last CTA then closes round 1 itself (gcol_k1w.cuh).  Its graph is
+  // split: this head ends after the pass, and the tail (k_candidates + the
+  // round loop) is launched only if the pass logged a read.  Measured on tri:
+  // the candidate kernel and an empty WHILE node cost 13 us of a 103 us step
+  // (an IF node around them costs as much as they do).
+  const bool split = K.cw == 0;
+  cudaGraph_t tgraph = graph;  // where the candidate pass and the loop go
+  if (split) GCOL_CK(cudaGraphCreate(&tgraph, 0));
+  cudaGraphConditionalHandle handle;
+  GCOL_CK(cudaGraphConditionalHandleCreate(&handle, tgraph, 1, cudaGraphCondAssignDefault));
   if (K.cw == 0) {
-    K.W.loop = static_cast<unsigned long long>(handle);
+    K.W.loop = 0ull;
     K.W.close_round = 1;
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &g->d_colors, &g->d_ctrl, &K.L, &K.W};
     cudaKernelNodeParams p{};
@@ -635,16 +644,20 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
     GCOL_CK(cudaGraphAddKernelNode(&n_k1, graph, &n_ev0, 1, &p));
   }
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev1, graph, &n_k1, 1, g->ev_k1));
-  GCOL_CK(add_kernel(&n_cand, graph, &n_ev1, 1, k_candidates<R>, dim3(g->sms * 4), dim3(kBlock),
-                     g->d_off, g->d_cols, n, static_cast<const int*>(g->d_colors), g->d_ctrl, K.L,
-                     K.grid1, g->d_marks));
+  if (split) {
+    cudaGraphNode_t h_end;
+    GCOL_CK(cudaGraphAddEventRecordNode(&h_end, graph, &n_ev1, 1, g->ev_end));
+  }
+  GCOL_CK(add_kernel(&n_cand, tgraph, split ? nullptr : &n_ev1, split ? 0 : 1, k_candidates<R>,
+                     dim3(g->sms * 4), dim3(kBlock), g->d_off, g->d_cols, n,
+                     static_cast<const int*>(g->d_colors), g->d_ctrl, K.L, K.grid1, g->d_marks));
 
   cudaGraphNodeParams cp{};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = handle;
   cp.conditional.type = cudaGraphCondTypeWhile;
   cp.conditional.size = 1;
-  GCOL_CK(cudaGraphAddNode(&n_while, graph, &n_cand, 1, &cp));
+  GCOL_CK(cudaGraphAddNode(&n_while, tgraph, &n_cand, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   cudaGraphNode_t b_list, b_heavy, b_ctl;
   GCOL_CK(add_kernel(&b_list, body, nullptr, 0, k_list<R, false>, dim3(g->sms * 4), dim3(kBlock),
@@ -653,9 +666,14 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
                      dim3(kBlock), g->d_off, g->d_cols, g->d_colors, g->d_ctrl,
                      static_cast<const int*>(g->d_heavy), g->d_marks));
   GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle, 1));
-  GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, graph, &n_while, 1, g->ev_end));
+  GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, tgraph, &n_while, 1, g->ev_end));
   GCOL_CK(cudaGraphInstantiate(out_exec, graph, 0));
   g->k1_warps[*out_exec] = K.grid1 * (K.cw ? K.cw : kWaitBlock / 32);
+  if (split) {
+    cudaGraphExec_t tex = nullptr;
+    GCOL_CK(cudaGraphInstantiate(&tex, tgraph, 0));
+    g->tails[*out_exec] = {tgraph, tex};
+  }
   *out_graph = graph;
   return GCOL_OK;
 }
@@ -1457,6 +1475,10 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
     cudaGraphExecDestroy(kv.second.second);
     cudaGraphDestroy(kv.second.first);
   }
+  for (auto& kv : g->tails) {
+    cudaGraphExecDestroy(kv.second.second);
+    cudaGraphDestroy(kv.second.first);
+  }
   for (auto& kv : g->splits) free_split(g, kv.second);
   if (g->stream) {
     if (g->owns_csr) {
@@ -1530,6 +1552,14 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
     if (sp != g->splits.end())
       if (int rc = reset_split(g, &sp->second, g->k1_warps[exec])) return rc;
     GCOL_CK(cudaGraphLaunch(exec, g->stream));
+    auto tl = g->tails.find(exec);
+    if (tl != g->tails.end()) {  // K1W head: the tail only if a read was logged
+      int done = 0;
+      GCOL_CK(cudaMemcpyAsync(&done, &g->d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost,
+                              g->stream));
+      GCOL_CK(cudaStreamSynchronize(g->stream));
+      if (!done) GCOL_CK(cudaGraphLaunch(tl->second.second, g->stream));
+    }
   }
   // streamed upload: K1 followed the pieces; what comes next reads anything
   if (g->ev_copied) GCOL_CK(cudaStreamWaitEvent(g->stream, g->ev_copied, 0));
