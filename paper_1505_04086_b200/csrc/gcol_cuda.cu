@@ -701,18 +701,16 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
                                    g->d_colors, g->d_ctrl, drift_rounds(g), 0);
   }
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
-  k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors,
-                                                         g->d_ctrl, K.L, K.grid1, g->d_marks);
-  if (K.cw == 0) {  // K1W may have closed round 1 already
+  if (K.cw == 0) {  // as the split K1W graph: the tail only if a read was logged
+    GCOL_CK(cudaEventRecord(g->ev_end, g->stream));
     int done = 0;
     GCOL_CK(cudaMemcpyAsync(&done, &g->d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost,
                             g->stream));
     GCOL_CK(cudaStreamSynchronize(g->stream));
-    if (done) {
-      GCOL_CK(cudaEventRecord(g->ev_end, g->stream));
-      return GCOL_OK;
-    }
+    if (done) return GCOL_OK;
   }
+  k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors,
+                                                         g->d_ctrl, K.L, K.grid1, g->d_marks);
   for (;;) {
     k_list<R, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
                                                             g->d_ctrl, g->d_heavy, g->d_marks);
