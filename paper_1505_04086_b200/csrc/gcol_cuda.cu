@@ -125,9 +125,9 @@ struct gcol_cuda_graph {
   Ctrl* d_ctrl = nullptr;
   cudaEvent_t ev_start = nullptr, ev_k1 = nullptr, ev_end = nullptr;
   std::map<ExecKey, std::pair<cudaGraph_t, cudaGraphExec_t>> execs;
-  // K1W runs: the head graph holds only the initial pass; its tail (round-1
-  // candidates + the round loop) runs only if the pass logged a read
-  std::map<cudaGraphExec_t, std::pair<cudaGraph_t, cudaGraphExec_t>> tails;
+  // K1W runs: the pass is launched on its own; its tail (round-1 candidates +
+  // the round loop) is a graph instantiated and run only if it logged a read
+  std::map<ExecKey, std::pair<cudaGraph_t, cudaGraphExec_t>> tails;
   std::map<int, SplitPlan> splits;
   std::map<cudaGraphExec_t, int> k1_warps;  // K1 warps of each instantiated graph
   // streamed upload (gcol_cuda_color_rsoc_csr): the adjacency arrives in
@@ -604,21 +604,10 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
   GCOL_CK(cudaGraphCreate(&graph, 0));
   const int n = static_cast<int>(g->n);
   cudaGraphNode_t n_ev0, n_k1, n_ev1, n_cand, n_while, n_ev2;
-  GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
-  // K1W (K.cw == 0) logs nothing when every wait resolved -- the usual case --
-  // and its last CTA then closes round 1 itself (gcol_k1w.cuh).  Its graph is
-  // split: this head ends after the pass, and the tail (k_candidates + the
-  // round loop) is launched only if the pass logged a read.  Measured on tri:
-  // the candidate kernel and an empty WHILE node cost 13 us of a 103 us step
-  // (an IF node around them costs as much as they do).
-  const bool split = K.cw == 0;
-  cudaGraph_t tgraph = graph;  // where the candidate pass and the loop go
-  if (split) GCOL_CK(cudaGraphCreate(&tgraph, 0));
   cudaGraphConditionalHandle handle;
-  GCOL_CK(cudaGraphConditionalHandleCreate(&handle, tgraph, 1, cudaGraphCondAssignDefault));
+  GCOL_CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+  GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
   if (K.cw == 0) {
-    K.W.loop = 0ull;
-    K.W.close_round = 1;
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &g->d_colors, &g->d_ctrl, &K.L, &K.W};
     cudaKernelNodeParams p{};
     p.func = const_cast<void*>(K.wfn);
@@ -644,20 +633,16 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
     GCOL_CK(cudaGraphAddKernelNode(&n_k1, graph, &n_ev0, 1, &p));
   }
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev1, graph, &n_k1, 1, g->ev_k1));
-  if (split) {
-    cudaGraphNode_t h_end;
-    GCOL_CK(cudaGraphAddEventRecordNode(&h_end, graph, &n_ev1, 1, g->ev_end));
-  }
-  GCOL_CK(add_kernel(&n_cand, tgraph, split ? nullptr : &n_ev1, split ? 0 : 1, k_candidates<R>,
-                     dim3(g->sms * 4), dim3(kBlock), g->d_off, g->d_cols, n,
-                     static_cast<const int*>(g->d_colors), g->d_ctrl, K.L, K.grid1, g->d_marks));
+  GCOL_CK(add_kernel(&n_cand, graph, &n_ev1, 1, k_candidates<R>, dim3(g->sms * 4), dim3(kBlock),
+                     g->d_off, g->d_cols, n, static_cast<const int*>(g->d_colors), g->d_ctrl, K.L,
+                     K.grid1, g->d_marks));
 
   cudaGraphNodeParams cp{};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = handle;
   cp.conditional.type = cudaGraphCondTypeWhile;
   cp.conditional.size = 1;
-  GCOL_CK(cudaGraphAddNode(&n_while, tgraph, &n_cand, 1, &cp));
+  GCOL_CK(cudaGraphAddNode(&n_while, graph, &n_cand, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   cudaGraphNode_t b_list, b_heavy, b_ctl;
   GCOL_CK(add_kernel(&b_list, body, nullptr, 0, k_list<R, false>, dim3(g->sms * 4), dim3(kBlock),
@@ -666,14 +651,48 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
                      dim3(kBlock), g->d_off, g->d_cols, g->d_colors, g->d_ctrl,
                      static_cast<const int*>(g->d_heavy), g->d_marks));
   GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle, 1));
-  GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, tgraph, &n_while, 1, g->ev_end));
+  GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, graph, &n_while, 1, g->ev_end));
   GCOL_CK(cudaGraphInstantiate(out_exec, graph, 0));
   g->k1_warps[*out_exec] = K.grid1 * (K.cw ? K.cw : kWaitBlock / 32);
-  if (split) {
-    cudaGraphExec_t tex = nullptr;
-    GCOL_CK(cudaGraphInstantiate(&tex, tgraph, 0));
-    g->tails[*out_exec] = {tgraph, tex};
-  }
+  *out_graph = graph;
+  return GCOL_OK;
+}
+
+// K1W runs (gcol_k1w.cuh) log nothing when every wait resolved -- the usual
+// case -- and the pass's last CTA then closes round 1 itself.  So the pass is
+// launched on its own, and this tail (k_candidates + the device round loop)
+// is instantiated and launched only when it logged a read.  Measured on tri:
+// keeping the candidate kernel and an empty WHILE node in one graph with the
+// pass cost 13 us of a 103 us step (an IF node around them as much), and the
+// one-call path paid the graph's instantiation on every call.
+template <int R>
+int build_k1w_tail(gcol_cuda_graph* g, const K1Launch& K, cudaGraph_t* out_graph,
+                   cudaGraphExec_t* out_exec) {
+  cudaGraph_t graph;
+  GCOL_CK(cudaGraphCreate(&graph, 0));
+  const int n = static_cast<int>(g->n);
+  cudaGraphConditionalHandle handle;
+  GCOL_CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNode_t n_cand, n_while, n_ev2;
+  GCOL_CK(add_kernel(&n_cand, graph, nullptr, 0, k_candidates<R>, dim3(g->sms * 4), dim3(kBlock),
+                     g->d_off, g->d_cols, n, static_cast<const int*>(g->d_colors), g->d_ctrl, K.L,
+                     K.grid1, g->d_marks));
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  GCOL_CK(cudaGraphAddNode(&n_while, graph, &n_cand, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaGraphNode_t b_list, b_heavy, b_ctl;
+  GCOL_CK(add_kernel(&b_list, body, nullptr, 0, k_list<R, false>, dim3(g->sms * 4), dim3(kBlock),
+                     g->d_off, g->d_cols, g->d_colors, g->d_ctrl, g->d_heavy, g->d_marks));
+  GCOL_CK(add_kernel(&b_heavy, body, &b_list, 1, k_heavy<R, false>, dim3(g->sms * heavy_grid()),
+                     dim3(kBlock), g->d_off, g->d_cols, g->d_colors, g->d_ctrl,
+                     static_cast<const int*>(g->d_heavy), g->d_marks));
+  GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle, 1));
+  GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, graph, &n_while, 1, g->ev_end));
+  GCOL_CK(cudaGraphInstantiate(out_exec, graph, 0));
   *out_graph = graph;
   return GCOL_OK;
 }
@@ -1531,9 +1550,15 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   const int mm = split_min_of(opt);
   const int wide = k1_variant(g, opt.k1_wide);
   const int polls = wait_polls(opt.k1_wait_polls);
-  if (!eager)
+  const bool k1w = !eager && lower && wide == 2;  // the waiting pass, launched on its own
+  K1Launch KW;
+  if (k1w) {
+    if (int rc = plan_k1_wait(g, &KW, polls)) return rc;
+    KW.W.close_round = 1;
+  } else if (!eager) {
     if (int rc = get_exec(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide, polls, &exec))
       return rc;
+  }
   tmark("exec");
   // Untimed prologue, like Coloring(n) before the reference's timer
   // (parallel.hpp:258 vs :267): colours := -1, marks := 0, control reset.
@@ -1545,19 +1570,40 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   if (eager) {
     if (int rc = launch_eager(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide, polls))
       return rc;
+  } else if (k1w) {
+    const int nn = static_cast<int>(g->n);
+    void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&nn), &g->d_colors, &g->d_ctrl, &KW.L, &KW.W};
+    GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
+    GCOL_CK(cudaLaunchKernel(KW.wfn, dim3(KW.grid1), dim3(kWaitBlock), args, 0, g->stream));
+    GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
+    GCOL_CK(cudaEventRecord(g->ev_end, g->stream));
+    int done = 0;
+    GCOL_CK(cudaMemcpyAsync(&done, &g->d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost,
+                            g->stream));
+    GCOL_CK(cudaStreamSynchronize(g->stream));
+    if (!done) {  // a read was logged: round 1 from the log, then the device round loop
+      const ExecKey key{rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide, polls};
+      auto tl = g->tails.find(key);
+      if (tl == g->tails.end()) {
+        cudaGraph_t tg = nullptr;
+        cudaGraphExec_t te = nullptr;
+        int rc;
+        switch (rule_of(opt.priority)) {
+          case kIdLow: rc = build_k1w_tail<kIdLow>(g, KW, &tg, &te); break;
+          case kIdHigh: rc = build_k1w_tail<kIdHigh>(g, KW, &tg, &te); break;
+          case kDegId: rc = build_k1w_tail<kDegId>(g, KW, &tg, &te); break;
+          default: rc = build_k1w_tail<kOrdered>(g, KW, &tg, &te); break;
+        }
+        if (rc != GCOL_OK) return rc;
+        tl = g->tails.emplace(key, std::make_pair(tg, te)).first;
+      }
+      GCOL_CK(cudaGraphLaunch(tl->second.second, g->stream));
+    }
   } else {
     auto sp = g->splits.find(mm);
     if (sp != g->splits.end())
       if (int rc = reset_split(g, &sp->second, g->k1_warps[exec])) return rc;
     GCOL_CK(cudaGraphLaunch(exec, g->stream));
-    auto tl = g->tails.find(exec);
-    if (tl != g->tails.end()) {  // K1W head: the tail only if a read was logged
-      int done = 0;
-      GCOL_CK(cudaMemcpyAsync(&done, &g->d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost,
-                              g->stream));
-      GCOL_CK(cudaStreamSynchronize(g->stream));
-      if (!done) GCOL_CK(cudaGraphLaunch(tl->second.second, g->stream));
-    }
   }
   // streamed upload: K1 followed the pieces; what comes next reads anything
   if (g->ev_copied) GCOL_CK(cudaStreamWaitEvent(g->stream, g->ev_copied, 0));
