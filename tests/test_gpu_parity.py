@@ -473,3 +473,10 @@ def test_k1w_streamed_one_call_is_serial_ff(monkeypatch):
         run = gcol.color_rsoc_csr(h_off, h_cols, 1, colors_out=out)
         check_run(hg, gcol.ColoringRun(out.numpy(), run.stats), 1)
         assert np.array_equal(out.numpy(), ff)
+    # no waits: every in-flight read is logged, so the candidate pass and the
+    # round loop (launched only in that case) run after the streamed pass
+    out.fill_(-7)
+    run = gcol.color_rsoc_csr(h_off, h_cols, 1, gcol.ParallelOptions(k1_wait_polls=-1),
+                              colors_out=out)
+    assert run.stats.pairs_logged > 0
+    check_run(hg, gcol.ColoringRun(out.numpy(), run.stats), 1)
