@@ -37,7 +37,15 @@ constexpr int k1_producers() {
   return 1;
 }
 constexpr int kChunk = kCW * 32;          // vertices per chunk (narrow); ranges align to it
-constexpr int kSlots = 4;                 // staged chunks in flight per CTA (multiple of producers)
+constexpr int kSlotsMax = 5;              // staged chunks in flight per CTA (multiple of producers)
+// narrow K1 has the shared memory for a fifth slot (~217 of 227 KB), wide not
+#ifndef GCOL_K1_SLOTS
+#define GCOL_K1_SLOTS 5
+#endif
+template <int CW>
+constexpr int k1_slots() {
+  return CW <= 8 ? GCOL_K1_SLOTS : 4;
+}
 constexpr int kSlotStage = 6144;          // adjacency entries staged per chunk (24 KB)
 constexpr int kBmWords = 512;             // per-warp medium-row bitmap pool
 constexpr int kStaleMax = 4;              // stale neighbours remembered per parked row
@@ -92,7 +100,7 @@ struct alignas(16) K1Slot {
 
 template <int CW>
 struct alignas(16) K1Smem {
-  K1Slot<CW> slot[kSlots];
+  K1Slot<CW> slot[k1_slots<CW>()];
   K1Warp cw[CW];
 };
 
@@ -751,7 +759,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // ---------------------------------------------------------------------------
 // K1 kernel.  One CTA per SM: a producer warp stages chunks (256 rows:
 // offsets + a window of their adjacency) into a ring of shared-memory slots
-// with cp.async, up to kSlots chunks ahead; eight consumer warps colour them.
+// with cp.async, up to k1_slots<CW>() chunks ahead; eight consumer warps colour them.
 // Chunks are assigned round-robin (chunk c -> CTA c % G), so the producer
 // can prefetch without claiming anything: the vertices in flight are only
 // those being coloured (about G x 256), which is what governs the stale
@@ -769,8 +777,8 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
   constexpr int kCW = CW;
   constexpr int kChunk = CW * 32;
   K1Smem<CW>& sm = *reinterpret_cast<K1Smem<CW>*>(k1_raw);
-  __shared__ int s_ready[kSlots];
-  __shared__ int s_consumed[kSlots];
+  __shared__ int s_ready[kSlotsMax];
+  __shared__ int s_consumed[kSlotsMax];
   __shared__ int s_npairs, s_mbhead, s_next;
   __shared__ unsigned s_gathers;
   const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -779,7 +787,7 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
   const int nchunks_all = (nitems + kChunk - 1) / kChunk;
   // chunks of this launch: global chunk coffset + cstride * local index
   const int nchunks = nchunks_all > S.coffset ? (nchunks_all - S.coffset + S.cstride - 1) / S.cstride : 0;
-  if (threadIdx.x < kSlots) {
+  if (threadIdx.x < k1_slots<CW>()) {
     s_ready[threadIdx.x] = -1;
     s_consumed[threadIdx.x] = 0;
     mbar_init(&sm.slot[threadIdx.x].full, 1);
@@ -818,14 +826,14 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
     for (int k = 0;; ++k) {
       const int cl = blockIdx.x + k * G;                // local chunk index
       const int c = cl * S.cstride + S.coffset;         // global chunk index
-      const int si = k % kSlots;
+      const int si = k % k1_slots<CW>();
       K1Slot<CW>& sl = sm.slot[si];
-      const unsigned par = (unsigned)((k / kSlots) & 1);
+      const unsigned par = (unsigned)((k / k1_slots<CW>()) & 1);
       long long t0 = clock64();
       if (cl >= nchunks) {
         if (lane == 0) {
-          if (k >= kSlots)
-            while (*reinterpret_cast<volatile int*>(&s_consumed[si]) < kCW * (k / kSlots))
+          if (k >= k1_slots<CW>())
+            while (*reinterpret_cast<volatile int*>(&s_consumed[si]) < kCW * (k / k1_slots<CW>()))
               __nanosleep(64);
           sl.chunk = -1;
           mbar_arrive_expect_tx(&sl.full, 0u);
@@ -842,10 +850,10 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
         mbar_wait(&sl.offb, par);              // offsets of chunk k (every lane)
         if (lane == 0) {  // chunk k+1's offsets go out as soon as its slot is free
           const int kn = k + 1;
-          if (kn >= kSlots)
-            while (*reinterpret_cast<volatile int*>(&s_consumed[kn % kSlots]) < kCW * (kn / kSlots))
+          if (kn >= k1_slots<CW>())
+            while (*reinterpret_cast<volatile int*>(&s_consumed[kn % k1_slots<CW>()]) < kCW * (kn / k1_slots<CW>()))
               __nanosleep(64);
-          k1_request_offsets<CW>(sm.slot[kn % kSlots], off,
+          k1_request_offsets<CW>(sm.slot[kn % k1_slots<CW>()], off,
                                  (blockIdx.x + kn * G) * S.cstride + S.coffset, nitems, item0, n,
                                  pol);
         }
@@ -883,8 +891,8 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
           if (lane == 0) mbar_arrive(&sl.full);
         }
       } else {  // worklist mode: per-row loads, nothing staged
-        if (k >= kSlots)
-          while (*reinterpret_cast<volatile int*>(&s_consumed[si]) < kCW * (k / kSlots))
+        if (k >= k1_slots<CW>())
+          while (*reinterpret_cast<volatile int*>(&s_consumed[si]) < kCW * (k / k1_slots<CW>()))
             __nanosleep(64);
         for (int i = lane; i < kChunk; i += 32) {
           const bool valid = i < rows;
@@ -977,9 +985,9 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
       }
       k = t / kCW;
       j = t - k * kCW;
-      si = k % kSlots;
+      si = k % k1_slots<CW>();
       int ok = 0;
-      if (lane == 0) ok = mbar_try_wait(&sm.slot[si].full, (unsigned)((k / kSlots) & 1));
+      if (lane == 0) ok = mbar_try_wait(&sm.slot[si].full, (unsigned)((k / k1_slots<CW>()) & 1));
       if (!__shfl_sync(kFull, ok, 0)) {
         __nanosleep(32);
         continue;
