@@ -136,6 +136,7 @@ class DeviceOps:
         o = self.opt.to_c(1)
         self._check(self._lib.LIB.gcol_cuda_k1_owned(self.h, C.byref(o),
                                                      C.c_void_p(colors.data_ptr()), C.byref(st)))
+        self.last_pairs = int(st.pairs_logged) + int(st.pair_overflow)  # reads logged by K1
         return st.initial_pass_ns / 1e6
 
     def candidates(self, colors: torch.Tensor) -> torch.Tensor:
@@ -268,6 +269,18 @@ def color_rsoc_partitioned(ops, colors: torch.Tensor, n: int, rank: int, world: 
         _sync(colors)
         dist.barrier(group=group)                  # every replica initialised
     st.k1_ms = ops.k1_owned(colors)
+    pairs = getattr(ops, "last_pairs", None)
+    if pairs is not None:
+        # nothing logged on any rank (the waiting pass): no candidates anywhere.
+        # The all-reduce completes only after every rank's K1 -- and with it
+        # every push (kernels end with a system fence) -- so it also stands in
+        # for the barrier below.
+        cnt = torch.tensor([pairs], dtype=torch.int64, device=colors.device)
+        dist.all_reduce(cnt, group=group)
+        if int(cnt.item()) == 0:
+            st.rounds, st.conflicts_per_round, st.conflicts_total = 1, [0], 0
+            st.barrier_events = 2
+            return st
     _sync(colors)
     dist.barrier(group=group)                      # every K1 push performed
     cand = ops.candidates(colors)
