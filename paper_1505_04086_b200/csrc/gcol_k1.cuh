@@ -38,9 +38,10 @@ constexpr int k1_producers() {
 }
 constexpr int kChunk = kCW * 32;          // vertices per chunk (narrow); ranges align to it
 constexpr int kSlotsMax = 5;              // staged chunks in flight per CTA (multiple of producers)
-// narrow K1 has the shared memory for a fifth slot (~217 of 227 KB), wide not
+// narrow K1 has the shared memory for a fifth slot (~217 of 227 KB), wide not;
+// measured (A/B on one box): five make R-MAT 27 6 % slower, R-MAT 24 0.6 % faster
 #ifndef GCOL_K1_SLOTS
-#define GCOL_K1_SLOTS 5
+#define GCOL_K1_SLOTS 4
 #endif
 template <int CW>
 constexpr int k1_slots() {
