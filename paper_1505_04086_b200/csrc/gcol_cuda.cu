@@ -1745,7 +1745,24 @@ int gcol_cuda_first_fit_sequential(gcol_cuda_graph* g, int32_t* colors_out, int3
   if (int rc = ensure_run_buffers(g)) return rc;
   const size_t n = static_cast<size_t>(g->n);
   GCOL_CK(cudaMemsetAsync(g->d_colors, 0xff, sizeof(int) * n, g->stream));
-  if (n > 0)
+  bool exact = false;
+  if (n > 0 && g->max_degree <= kSmallMax) {
+    // bounded degree: the waiting pass K1W is First-Fit in id order whenever
+    // every wait resolved (nothing logged) -- the same colouring, in parallel
+    K1Launch K;
+    if (int rc = plan_k1_wait(g, &K, kWaitPollsDefault)) return rc;
+    if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, nullptr, 0)) return rc;
+    const int nn = static_cast<int>(n);
+    void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&nn), &g->d_colors, &g->d_ctrl, &K.L, &K.W};
+    GCOL_CK(cudaLaunchKernel(K.wfn, dim3(K.grid1), dim3(kWaitBlock), args, 0, g->stream));
+    Ctrl hdr;
+    GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
+    GCOL_CK(cudaStreamSynchronize(g->stream));
+    exact = hdr.pair_len == 0 && hdr.pair_overflow == 0;
+    if (!exact)  // a wait gave up (a warp was not resident): the serial kernel
+      GCOL_CK(cudaMemsetAsync(g->d_colors, 0xff, sizeof(int) * n, g->stream));
+  }
+  if (n > 0 && !exact)
     k_first_fit_seq<<<1, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, static_cast<int>(n),
                                                  g->d_colors);
   GCOL_CK(cudaGetLastError());

@@ -410,7 +410,7 @@ def _k1w_graphs(rng):
     return [g for g in out if g.max_degree() <= 63]
 
 
-def test_k1w_is_serial_first_fit():
+def test_k1w_is_serial_first_fit(oracle_mod):
     """Every wait of K1W resolves on a resident grid, so the initial pass sees
     every lower neighbour's final colour: the result is sequential First-Fit
     bit for bit (coloring.hpp:110-116), with no logged read and one round."""
@@ -418,7 +418,8 @@ def test_k1w_is_serial_first_fit():
     graphs_ = _k1w_graphs(rng)
     assert any(int(g.offsets()[-1]) % 4 == 2 for g in graphs_)
     for g in graphs_:
-        ff = gcol.first_fit_sequential(g)
+        ff = oracle_mod.first_fit_sequential(oracle_csr(oracle_mod, g))  # the C restatement
+        assert np.array_equal(gcol.first_fit_sequential(g), ff)  # device FF (K1W fast path)
         for k1_wide in (0, 3):
             run = gcol.color_rsoc(g, 4, gcol.ParallelOptions(k1_wide=k1_wide))
             check_run(g, run, 4)
@@ -428,11 +429,11 @@ def test_k1w_is_serial_first_fit():
 
 
 @pytest.mark.parametrize("name", ["er", "tri", "stencil"])
-def test_k1w_configs_scaled_serial_ff(name):
+def test_k1w_configs_scaled_serial_ff(name, oracle_mod):
     off, cols = graphs.make_config(name, "cuda", scale_down=1)
     g = gcol.Graph.from_device(off, cols)
     hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
-    ff = gcol.first_fit_sequential(hg)
+    ff = oracle_mod.first_fit_sequential(oracle_csr(oracle_mod, hg))
     for _ in range(3):
         run = gcol.color_rsoc(g, 1)
         check_run(hg, run, 1)
@@ -456,7 +457,7 @@ def test_k1w_optimistic_logging_path():
     assert logged > 0  # the log path ran
 
 
-def test_k1w_streamed_one_call_is_serial_ff(monkeypatch):
+def test_k1w_streamed_one_call_is_serial_ff(monkeypatch, oracle_mod):
     """The one-call host path with K1W following the upload pieces.  Repeated
     calls (the graph instantiation is cached after the first, so K1 starts
     while pieces are still in flight) with 1M-entry pieces: K1W fills every SM
@@ -465,7 +466,7 @@ def test_k1w_streamed_one_call_is_serial_ff(monkeypatch):
     off, cols = graphs.make_config("stencil", "cuda", scale_down=1)  # ~25M entries
     h_off, h_cols = off.cpu().pin_memory(), cols.cpu().pin_memory()
     hg = gcol.Graph(h_off.numpy(), h_cols.numpy())
-    ff = gcol.first_fit_sequential(hg)
+    ff = oracle_mod.first_fit_sequential(oracle_csr(oracle_mod, hg))
     out = torch.empty(off.numel() - 1, dtype=torch.int32).pin_memory()
     for shift in ("31", "20", "20", "20"):
         monkeypatch.setenv("GCOL_UPLOAD_SHIFT", shift)
