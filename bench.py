@@ -8,8 +8,13 @@ detect-and-recolor rounds until no conflict) of the configuration's graph.
 `value` = directed adjacency entries m / mean device coloring time, in
 GE/s, with the CSR already resident in HBM; `e2e` = the same metric through
 the public C ABI with host buffers (CSR upload + colours download inside the
-timed region).  Default workload: BASELINE.json configs[1] (2000x2000
-triangular mesh); --config er|tri|stencil|rmat24 selects the others.
+timed region).  Default workload: BASELINE.json configs[4] (R-MAT scale 27,
+4.2 G directed entries: the largest configuration, and it fits one B200);
+--config er|tri|stencil|rmat24 selects the others.
+
+--gpus N > 1 outside torchrun re-launches this script under
+torch.distributed.run with N ranks (one per GPU), after checking that N GPUs
+are visible; it fails loudly otherwise.
 """
 from __future__ import annotations
 
@@ -47,12 +52,15 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="tri", choices=sorted(CONFIG_WORKLOAD))
+    p.add_argument("--config", default="rmat27", choices=sorted(CONFIG_WORKLOAD))
     p.add_argument("--priority", default="degree_id", choices=["id_low", "id_high", "degree_id", "ordered"])
     p.add_argument("--k1-blocks-per-sm", type=int, default=2)
     p.add_argument("--k1-read-all", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="budget of the bounded CPU-baseline sample")
+    p.add_argument("--gate-runs", type=int, default=10,
+                   help="reference color_rsoc runs behind the colour gate (median of >= 10, "
+                        "acceptance.cpp:173-176)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=9)
@@ -151,7 +159,8 @@ def make_graph(config: str, device: str):
     return graphs.make_config(config, device)
 
 
-def cpu_reference_runs(off_np, cols_np, seconds: float, max_runs: int, threads: int):
+def cpu_reference_runs(off_np, cols_np, seconds: float, max_runs: int, threads: int,
+                       min_runs: int = 1):
     """The reference's own color_rsoc (oracle/_ref, compiled from
     /root/reference) on the host cores; falls back to our C port of it
     (oracle/gcol_oracle.c) when the reference library is absent."""
@@ -170,7 +179,7 @@ def cpu_reference_runs(off_np, cols_np, seconds: float, max_runs: int, threads: 
         runner = lambda: oracle.color_parallel(g, threads, "rsoc")  # noqa: E731
     serial_ff = int(len(set(ff.tolist()))) if ff.size else 0
     t0 = time.time()
-    while len(results) < max_runs and (time.time() - t0 < seconds or len(results) < 1):
+    while len(results) < max_runs and (time.time() - t0 < seconds or len(results) < min_runs):
         _, st = runner()
         results.append(st)
     return kind, results, serial_ff
@@ -431,7 +440,9 @@ def run_ours(args):
     if rank == 0 and not args.no_cpu_baseline:
         off_np, cols_np = off.cpu().numpy(), cols.cpu().numpy()
         threads = os.cpu_count() or 1
-        kind, res, serial_ff = cpu_reference_runs(off_np, cols_np, args.cpu_seconds, 50, threads)
+        kind, res, serial_ff = cpu_reference_runs(off_np, cols_np, args.cpu_seconds,
+                                                  max(50, args.gate_runs), threads,
+                                                  min_runs=args.gate_runs)
         tmean = sum(r["wall_time_ns"] for r in res) / len(res) * 1e-9
         ref_colors = sorted(r["num_colors"] for r in res)
         med = ref_colors[(len(ref_colors) - 1) // 2]
@@ -467,11 +478,14 @@ def e2e_measure(args, off, cols, n, m, opt, _lib, gcol):
     st = _lib.Stats()
     p_off, p_cols, p_out = (C.c_void_p(t.data_ptr()) for t in (h_off, h_cols, h_out))
 
+    xfer = []
+
     def one_call():
         rc = _lib.LIB.gcol_cuda_color_rsoc_csr(p_off, p_cols, n, m, -1, C.byref(copt), p_out,
                                                C.byref(st))
         if rc:
             raise RuntimeError(_lib.last_error())
+        xfer.append((st.h2d_bytes, st.d2h_bytes))
 
     def three_calls():
         h = C.c_void_p()
@@ -498,18 +512,54 @@ def e2e_measure(args, off, cols, n, m, opt, _lib, gcol):
         t3.append(time.perf_counter() - t0)
     mean_t = sorted(t1)[(len(t1) - 1) // 2]
     sep_t = sorted(t3)[(len(t3) - 1) // 2]
-    return {"value": m / mean_t / 1e9, "unit": "GE/s", "h2d_bytes_per_step": 8 * (n + 1) + 4 * m,
-            "d2h_bytes_per_step": 4 * n, "ms_per_step": mean_t * 1e3,
+    # bytes the library counted crossing PCIe per one-call step (after its
+    # narrowing: 1-byte degrees/colours on small-degree graphs), control
+    # blocks and verification summaries included
+    h2d, d2h = xfer[-1]
+    return {"value": m / mean_t / 1e9, "unit": "GE/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": mean_t * 1e3,
+            "bytes_counted_by": "gcol_cuda_stats.h2d_bytes / d2h_bytes (every host<->device "
+                                "copy of the call)",
             "statistic": f"median of {args.e2e_steps} calls, alternating with the three-call path",
             "path": "gcol_cuda_color_rsoc_csr (host CSR in, host colours out; upload "
                     "overlapped with the initial pass)",
             "three_call_ms_per_step": sep_t * 1e3,
             "three_call_path": "gcol_cuda_graph_create + gcol_cuda_color_rsoc + "
-                               "gcol_cuda_graph_destroy"}
+                               "gcol_cuda_graph_destroy",
+            "offsets_rebuild": "one-piece uploads (< 64 M entries) send degrees narrowed to "
+                               "1-2 bytes and rebuild the offsets on the device with "
+                               "cub::DeviceScan (library scan, e2e path only)"}
+
+
+def relaunch_distributed(args):
+    """--gpus N > 1 outside torchrun: one rank per GPU under
+    torch.distributed.run (the driver's own launch), or a loud failure when
+    fewer than N GPUs are visible."""
+    import socket
+    import torch
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if args.impl == "ours" and have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}",
+              file=sys.stderr, flush=True)
+        return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        return relaunch_distributed(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world and "RANK" in os.environ:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr, flush=True)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -124,6 +124,10 @@ typedef struct {
   uint32_t pair_overflow;      /* 1 if round 1 had to scan all of V */
   int32_t priority;
   uint64_t k1_gathers;         /* neighbour-colour loads issued by K1 */
+  uint64_t h2d_bytes;          /* bytes copied host -> device by this call (the first call
+                                  on a handle also counts its graph upload: for
+                                  gcol_cuda_color_rsoc_csr, everything that crossed PCIe up) */
+  uint64_t d2h_bytes;          /* bytes copied device -> host by this call */
 } gcol_cuda_stats;
 
 /* verify_coloring (coloring.hpp:159-177) summary + color bound check. */

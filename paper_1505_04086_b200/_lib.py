@@ -71,6 +71,8 @@ class Stats(C.Structure):
         ("pair_overflow", C.c_uint32),
         ("priority", C.c_int32),
         ("k1_gathers", C.c_uint64),
+        ("h2d_bytes", C.c_uint64),
+        ("d2h_bytes", C.c_uint64),
     ]
 
 

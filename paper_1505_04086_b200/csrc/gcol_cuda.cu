@@ -159,9 +159,17 @@ struct gcol_cuda_graph {
   // colour copy-out to pinned host memory, overlapped with verification
   cudaStream_t out_stream = nullptr;
   cudaEvent_t ev_final = nullptr;
+  // bytes this handle moved host->device / device->host since the count was
+  // last reset (gcol_cuda_stats.h2d_bytes / d2h_bytes: the first coloring
+  // call after create reports the upload too)
+  uint64_t xfer_h2d = 0, xfer_d2h = 0;
+  bool xfer_from_create = true;
 };
 
 namespace {
+
+void note_h2d(gcol_cuda_graph* g, size_t bytes) { g->xfer_h2d += bytes; }
+void note_d2h(gcol_cuda_graph* g, size_t bytes) { g->xfer_d2h += bytes; }
 
 int ensure_device(int device, int* chosen) {
   int count = 0;
@@ -380,6 +388,7 @@ int get_split(gcol_cuda_graph* g, int min_deg, SplitPlan** out) {
     GCOL_CK(cudaGetLastError());
     unsigned long long cnt[2] = {0, 0};
     GCOL_CK(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, g->stream));
+    note_d2h(g, 16);
     GCOL_CK(cudaStreamSynchronize(g->stream));
     GCOL_CK(cudaFreeAsync(d_cnt, g->stream));
     P.nslots = static_cast<int>(cnt[0]);
@@ -410,6 +419,7 @@ int reset_split(gcol_cuda_graph* g, const SplitPlan* P, int warps) {
   if (!P) return GCOL_OK;
   const unsigned init[4] = {0u, 0u, static_cast<unsigned>(warps), 0u};  // warps = consumer warps
   GCOL_CK(cudaMemcpyAsync(P->d_ctr, init, sizeof init, cudaMemcpyHostToDevice, g->stream));
+  note_h2d(g, sizeof init);
   if (P->nslots > 0) {
     GCOL_CK(cudaMemsetAsync(P->d_slot_bm, 0, sizeof(unsigned) * 32 * static_cast<size_t>(P->nslots),
                             g->stream));
@@ -725,6 +735,7 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
     int done = 0;
     GCOL_CK(cudaMemcpyAsync(&done, &g->d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost,
                             g->stream));
+    note_d2h(g, sizeof(int));
     GCOL_CK(cudaStreamSynchronize(g->stream));
     if (done) return GCOL_OK;
   }
@@ -740,6 +751,7 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
     int done = 0;
     GCOL_CK(cudaMemcpyAsync(&done, &g->d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost,
                             g->stream));
+    note_d2h(g, sizeof(int));
     GCOL_CK(cudaStreamSynchronize(g->stream));
     if (done) break;
   }
@@ -807,6 +819,7 @@ int reset_ctrl(gcol_cuda_graph* g, int round_cap, int* in_list, int* out_list, i
   }
   c->hslot_bm = g->d_hslot_bm;
   GCOL_CK(cudaMemcpyAsync(g->d_ctrl, buf.data(), hdr, cudaMemcpyHostToDevice, g->stream));
+  note_h2d(g, hdr);
   return GCOL_OK;
 }
 
@@ -816,6 +829,7 @@ int copy_in(gcol_cuda_graph* g, void* dst, const void* src, size_t bytes, int me
                           memory == GCOL_MEM_DEVICE ? cudaMemcpyDeviceToDevice
                                                     : cudaMemcpyHostToDevice,
                           g->stream));
+  if (memory != GCOL_MEM_DEVICE) note_h2d(g, bytes);
   return GCOL_OK;
 }
 
@@ -825,6 +839,7 @@ int copy_out(gcol_cuda_graph* g, void* dst, const void* src, size_t bytes, int m
                           memory == GCOL_MEM_DEVICE ? cudaMemcpyDeviceToDevice
                                                     : cudaMemcpyDeviceToHost,
                           g->stream));
+  if (memory != GCOL_MEM_DEVICE) note_d2h(g, bytes);
   return GCOL_OK;
 }
 
@@ -891,6 +906,7 @@ int verify_device(gcol_cuda_graph* g, const int* d_col, gcol_cuda_verify_report*
   std::vector<unsigned> census(cwords);
   GCOL_CK(cudaMemcpyAsync(&acc, d_acc, sizeof acc, cudaMemcpyDeviceToHost, g->stream));
   GCOL_CK(cudaMemcpyAsync(census.data(), d_census, 4 * cwords, cudaMemcpyDeviceToHost, g->stream));
+  note_d2h(g, sizeof acc + 4 * cwords);
   GCOL_CK(cudaStreamSynchronize(g->stream));
   uint32_t distinct = 0;
   if (acc.max_color >= 0 && acc.max_color <= census_max) {
@@ -905,6 +921,7 @@ int verify_device(gcol_cuda_graph* g, const int* d_col, gcol_cuda_verify_report*
     std::vector<unsigned> bitmap(words);
     GCOL_CK(cudaMemcpyAsync(bitmap.data(), d_bitmap, sizeof(unsigned) * words,
                             cudaMemcpyDeviceToHost, g->stream));
+    note_d2h(g, sizeof(unsigned) * words);
     GCOL_CK(cudaStreamSynchronize(g->stream));
     GCOL_CK(cudaFreeAsync(d_bitmap, g->stream));
     for (unsigned w : bitmap) distinct += static_cast<uint32_t>(__builtin_popcount(w));
@@ -927,6 +944,7 @@ int verify_device(gcol_cuda_graph* g, const int* d_col, gcol_cuda_verify_report*
       std::vector<int3> h(static_cast<size_t>(want));
       GCOL_CK(cudaMemcpyAsync(h.data(), d_out, sizeof(int3) * want, cudaMemcpyDeviceToHost,
                               g->stream));
+      note_d2h(g, sizeof(int3) * want);
       GCOL_CK(cudaStreamSynchronize(g->stream));
       for (long long i = 0; i < want; ++i) {
         if (out_u) out_u[i] = static_cast<uint32_t>(h[i].x);
@@ -1254,7 +1272,7 @@ const unsigned* pinned_one() {
   return one;
 }
 
-cudaError_t publish_piece(cudaStream_t s, unsigned* flag) {
+cudaError_t publish_piece(gcol_cuda_graph* g, cudaStream_t s, unsigned* flag) {
   static std::atomic<bool> memop_ok{true};
   if (memop_ok.load(std::memory_order_relaxed))
     if (WriteValue32Fn fn = write_value32()) {
@@ -1266,6 +1284,7 @@ cudaError_t publish_piece(cudaStream_t s, unsigned* flag) {
   tmark("publish-dma");
   const unsigned* one = pinned_one();
   if (!one) return cudaErrorMemoryAllocation;
+  note_h2d(g, sizeof(unsigned));
   return cudaMemcpyAsync(flag, one, sizeof(unsigned), cudaMemcpyHostToDevice, s);
 }
 
@@ -1330,6 +1349,7 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
           cudaMemcpyAsync(g->d_vpre, pre.data(), sizeof(int) * pre.size(), cudaMemcpyHostToDevice,
                           g->stream) != cudaSuccess)
         return fail(GCOL_ERR_CUDA, "verification plan upload failed");
+      note_h2d(g, sizeof(int) * (big.size() + pre.size()));
       g->nvrows = static_cast<int>(big.size());
     }
     g->vplan_done = true;
@@ -1390,13 +1410,15 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
       cudaEventRecord(g->ev_copy0, g->copy_stream);
       if (!packed) {
         cudaMemcpyAsync(g->d_off, offsets, off_bytes, mt, g->copy_stream);
+        if (memory == GCOL_MEM_HOST) note_h2d(g, off_bytes);
         cudaEventRecord(ev_off, g->copy_stream);
       }
       for (int64_t p = 0; p < npieces; ++p) {
         cudaStream_t cs = (p & 1) ? g->copy_stream : g->copy_stream2;
         const int64_t b = p * piece, len = std::min(piece, m - b);
         cudaMemcpyAsync(g->d_cols + b, cols + b, sizeof(int) * static_cast<size_t>(len), mt, cs);
-        if (publish_piece(cs, g->d_ready + p) != cudaSuccess)
+        if (memory == GCOL_MEM_HOST) note_h2d(g, sizeof(int) * static_cast<size_t>(len));
+        if (publish_piece(g, cs, g->d_ready + p) != cudaSuccess)
           return bail(fail(GCOL_ERR_CUDA, "piece publication failed"));
       }
       if (packed) {
@@ -1419,6 +1441,7 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
         if (es == cudaSuccess)
           es = cudaMemcpyAsync(d_deg, g->staging.p, static_cast<size_t>(n) * width,
                                cudaMemcpyHostToDevice, g->copy_stream);
+        note_h2d(g, static_cast<size_t>(n) * width);
         if (es == cudaSuccess) {
           if (width == 1) es = scan_degrees(static_cast<const uint8_t*>(d_deg), n, g->d_off, g->copy_stream);
           else if (width == 2) es = scan_degrees(static_cast<const uint16_t*>(d_deg), n, g->d_off, g->copy_stream);
@@ -1450,6 +1473,7 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
     if (n > 0)
       k_graph_stats<<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, static_cast<int>(n), d_gs);
     cudaMemcpyAsync(&g->gs, d_gs, sizeof(GraphStats), cudaMemcpyDeviceToHost, g->stream);
+    note_d2h(g, sizeof(GraphStats));
     cudaFreeAsync(d_gs, g->stream);
   }
   tmark("validate");
@@ -1542,6 +1566,8 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   if (int rc = read_options(opt_in, &opt)) return rc;
   if (g->n > 0 && !colors_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "colors_out is null");
   GCOL_CK(cudaSetDevice(g->device));
+  if (!g->xfer_from_create) g->xfer_h2d = g->xfer_d2h = 0;  // else the upload counts too
+  g->xfer_from_create = false;
   if (int rc = ensure_run_buffers(g)) return rc;
   cudaGraphExec_t exec = nullptr;
   const int lower = opt.k1_read_all ? 0 : 1;
@@ -1580,6 +1606,7 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
     int done = 0;
     GCOL_CK(cudaMemcpyAsync(&done, &g->d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost,
                             g->stream));
+    note_d2h(g, sizeof(int));
     GCOL_CK(cudaStreamSynchronize(g->stream));
     if (!done) {  // a read was logged: round 1 from the log, then the device round loop
       const ExecKey key{rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide, polls};
@@ -1624,15 +1651,18 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
                                                               out_width, g->d_marks);
       GCOL_CK(cudaMemcpyAsync(g->out_staging.p, g->d_marks, n * out_width, cudaMemcpyDeviceToHost,
                               g->out_stream));
+      note_d2h(g, n * out_width);
     } else {
       GCOL_CK(cudaMemcpyAsync(colors_out, g->d_colors, sizeof(int) * n, cudaMemcpyDeviceToHost,
                               g->out_stream));
+      note_d2h(g, sizeof(int) * n);
     }
   }
   // Header + conflicts_per_round back in two copies.
   tmark("launch");
   Ctrl hdr;
   GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
+  note_d2h(g, offsetof(Ctrl, cpr));
   GCOL_CK(cudaStreamSynchronize(g->stream));
   tmark("run");
   if (const char* tp = std::getenv("GCOL_K1W_TRACE"))
@@ -1662,6 +1692,7 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   if (!cpr.empty())
     GCOL_CK(cudaMemcpyAsync(cpr.data(), g->d_ctrl->cpr, sizeof(unsigned long long) * cpr.size(),
                             cudaMemcpyDeviceToHost, g->stream));
+  note_d2h(g, sizeof(unsigned long long) * cpr.size());
   float ms_total = 0.f, ms_k1 = 0.f;
   GCOL_CK(cudaEventElapsedTime(&ms_total, g->ev_start, g->ev_end));
   GCOL_CK(cudaEventElapsedTime(&ms_k1, g->ev_start, g->ev_k1));
@@ -1707,6 +1738,8 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
     stats->pair_overflow = static_cast<uint32_t>(hdr.pair_overflow);
     stats->priority = opt.priority;
     stats->k1_gathers = hdr.k1_gathers;
+    stats->h2d_bytes = g->xfer_h2d;
+    stats->d2h_bytes = g->xfer_d2h;
   }
   if (hdr.capped)
     return fail(GCOL_ERR_ROUND_CAP,

@@ -148,6 +148,8 @@ class ColoringStats:
     pair_overflow: bool = False
     priority: Priority = Priority.degree_id
     k1_gathers: int = 0
+    h2d_bytes: int = 0       # bytes the call copied host -> device (incl. the upload
+    d2h_bytes: int = 0       # on a handle's first call) / device -> host
 
 
 @dataclass
@@ -339,7 +341,8 @@ def _stats_from_c(s: _lib.Stats, cpr: np.ndarray) -> ColoringStats:
         wall_time_ns=s.wall_time_ns, fallback_triggered=bool(s.fallback_triggered),
         initial_pass_ns=s.initial_pass_ns, pairs_logged=s.pairs_logged,
         round1_candidates=s.round1_candidates, pair_overflow=bool(s.pair_overflow),
-        priority=Priority(s.priority), k1_gathers=s.k1_gathers)
+        priority=Priority(s.priority), k1_gathers=s.k1_gathers, h2d_bytes=s.h2d_bytes,
+        d2h_bytes=s.d2h_bytes)
 
 
 # --- coloring entry points -------------------------------------------------------

@@ -91,13 +91,17 @@ def csr_from_edges(u: torch.Tensor, v: torch.Tensor, n: int) -> Tuple[torch.Tens
     return off, cols
 
 
+def erdos_renyi_pairs(n: int, avg_degree: float, seed: int, device="cpu"):
+    """The raw sample multiset of erdos_renyi (loops and duplicates kept)."""
+    m = int(n * avg_degree / 2)
+    idx = torch.arange(m, dtype=torch.int64, device=device)
+    return uniform_below(seed, idx, n, 1), uniform_below(seed, idx, n, 2)
+
+
 def erdos_renyi(n: int, avg_degree: float, seed: int, device="cpu"):
     """n*avg_degree/2 uniform pairs, then dedup/loop removal (the
     oracle::random_graph recipe, tests/support/oracles.hpp:94-103)."""
-    m = int(n * avg_degree / 2)
-    idx = torch.arange(m, dtype=torch.int64, device=device)
-    u = uniform_below(seed, idx, n, 1)
-    v = uniform_below(seed, idx, n, 2)
+    u, v = erdos_renyi_pairs(n, avg_degree, seed, device)
     return csr_from_edges(u, v, n)
 
 
@@ -153,6 +157,16 @@ def _rmat_samples(scale: int, a: float, b: float, c: float, seed: int, s0: int, 
         u = (u << 1) | (r >= ab).to(torch.int64)
         v = (v << 1) | (((r >= a) & (r < ab)) | (r >= abc)).to(torch.int64)
     return u, v
+
+
+def rmat_pairs(scale: int, edge_factor: int, a: float, b: float, c: float, seed: int,
+               device="cpu"):
+    """The raw, relabelled sample multiset of rmat (loops and duplicates
+    kept): what build_graph (graph.hpp:98-138) canonicalises."""
+    n = 1 << scale
+    perm = random_permutation(n, seed, device)
+    u, v = _rmat_samples(scale, a, b, c, seed, 0, edge_factor * n, device)
+    return perm[u], perm[v]
 
 
 def rmat(scale: int, edge_factor: int, a: float, b: float, c: float, seed: int, device="cpu",

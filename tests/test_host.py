@@ -124,17 +124,42 @@ def test_rmat_bucketed_builder_is_the_same_csr():
 
 
 def test_generators_reference_build_parity(oracle_mod):
-    """Our torch CSR construction == the reference's build_graph on the same pairs."""
+    """Our torch CSR construction (csr_from_edges and the bucketed builder)
+    == the reference's build_graph (graph.hpp:98-138) fed the SAME raw pair
+    multiset: self-loops, duplicates in both orientations and isolated ids
+    included, so a dedup, loop or sort bug cannot hide."""
     from paper_1505_04086_b200 import graphs
     if not oracle_mod.ref_available():
         pytest.skip("oracle/_ref not built")
-    off, cols = graphs.rmat(10, 8, .57, .19, .19, 3)
-    n = off.numel() - 1
-    # feed the upper triangle to the reference build_graph
-    rows = torch.repeat_interleave(torch.arange(n), torch.diff(off))
-    up = cols.to(torch.int64) > rows
-    e = torch.stack([rows[up], cols.to(torch.int64)[up]], 1).numpy()
-    R = oracle_mod.RefGraph.from_edges(e, n)
-    csr = R.csr()
-    assert np.array_equal(csr.off.astype(np.int64), off.numpy())
-    assert np.array_equal(csr.cols.astype(np.int32), cols.numpy())
+
+    def ref_csr(u, v, n):
+        e = torch.stack([u, v], 1).numpy()
+        csr = oracle_mod.RefGraph.from_edges(e, n).csr()
+        return csr.off.astype(np.int64), csr.cols.astype(np.int32)
+
+    cases = []
+    u, v = graphs.rmat_pairs(11, 16, .57, .19, .19, 3)
+    cases.append(("rmat", u, v, 1 << 11))
+    u, v = graphs.erdos_renyi_pairs(3000, 9.0, 5)
+    cases.append(("er", u, v, 3000))
+    g = torch.Generator().manual_seed(9)
+    u = torch.randint(0, 50, (4000,), generator=g)
+    v = torch.randint(0, 50, (4000,), generator=g)
+    u[::7] = v[::7]                                   # explicit self-loops
+    u = torch.cat([u, v[:500]]); v = torch.cat([v, u[:500]])  # reversed duplicates
+    cases.append(("dense-dups", u, v, 64))            # ids 50..63 isolated
+    for name, u, v, n in cases:
+        assert bool((u == v).any()), name             # the multiset holds loops
+        ro, rc = ref_csr(u, v, n)
+        off, cols = graphs.csr_from_edges(u, v, n)
+        assert np.array_equal(off.numpy(), ro), name
+        assert np.array_equal(cols.numpy(), rc), name
+    # the rmat generator's own path (direct and bucketed) == build_graph of its pairs
+    u, v = graphs.rmat_pairs(11, 16, .57, .19, .19, 3)
+    ro, rc = ref_csr(u, v, 1 << 11)
+    for lean in (False, True):
+        off, cols = graphs.rmat(11, 16, .57, .19, .19, 3, lean=lean)
+        assert np.array_equal(off.numpy(), ro) and np.array_equal(cols.numpy(), rc), lean
+    off, cols = graphs.erdos_renyi(3000, 9.0, 5)
+    ro, rc = ref_csr(*graphs.erdos_renyi_pairs(3000, 9.0, 5), 3000)
+    assert np.array_equal(off.numpy(), ro) and np.array_equal(cols.numpy(), rc)
