@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define GCOL_CUDA_ABI_VERSION 1
+#define GCOL_CUDA_ABI_VERSION 2
 
 /* Status codes.  The C++ adapter (gcol_cuda.hpp) rethrows them as the
  * reference's exceptions (errors.hpp:11-52). */
@@ -96,9 +96,9 @@ typedef struct {
                                   pieces that every warp helps colour; 0 = default
                                   (1024) */
   int32_t k1_wide;           /* initial-pass kernel: 0 auto (the waiting pass K1W when every
-                                row has degree <= 63, else wide k1_pipe when max degree
-                                <= 16, else narrow), 1 narrow k1_pipe (8 consumer warps
-                                per SM), 2 wide k1_pipe (16), 3 K1W where it applies */
+                                row has degree <= 63, else the class-split pass K1H + K1L),
+                                1 narrow k1_pipe (8 consumer warps per SM), 2 wide k1_pipe
+                                (16), 3 K1W where it applies, 4 class split */
   int32_t k1_wait_polls;     /* K1W: re-checks of a row's in-flight lower neighbours before
                                 it colours past them and logs the reads for round 1;
                                 0 default (4096), < 0 none (purely optimistic) */
@@ -128,6 +128,9 @@ typedef struct {
                                   on a handle also counts its graph upload: for
                                   gcol_cuda_color_rsoc_csr, everything that crossed PCIe up) */
   uint64_t d2h_bytes;          /* bytes copied device -> host by this call */
+  uint64_t heavy_pass_ns;      /* class-split initial pass (skewed degree): device time of
+                                  the heavy-row pass K1H (0 when the pass is not split) */
+  uint64_t heavy_rows;         /* rows of that pass (degree >= 64) */
 } gcol_cuda_stats;
 
 /* verify_coloring (coloring.hpp:159-177) summary + color bound check. */

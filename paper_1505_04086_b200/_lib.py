@@ -73,6 +73,8 @@ class Stats(C.Structure):
         ("k1_gathers", C.c_uint64),
         ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64),
+        ("heavy_pass_ns", C.c_uint64),
+        ("heavy_rows", C.c_uint64),
     ]
 
 

@@ -30,6 +30,8 @@
 #include "gcol_cuda.h"
 #include "gcol_kernels.cuh"
 #include "gcol_k1w.cuh"
+#include "gcol_k1c.cuh"
+#include "gcol_round1.cuh"
 
 using namespace gcol::dev;
 
@@ -96,6 +98,15 @@ struct SplitPlan {
   int2* d_q = nullptr;
   unsigned* d_q_seq = nullptr;
   unsigned* d_ctr = nullptr;  // [0] pieces allocated, [1] slots, [2] live warps, [3] chunks done
+  HvPiece* d_q16 = nullptr;   // class-split K1H piece records (allocated on first use)
+};
+
+// Heavy-row table of the class-split initial pass (gcol_k1c.cuh), per
+// threshold T: the rows of degree >= T in ascending id order.
+struct ClassPlan {
+  int T = 0;
+  int nh = 0;
+  HeavyRow* d_rows = nullptr;
 };
 
 }  // namespace
@@ -124,6 +135,9 @@ struct gcol_cuda_graph {
   int max_k1_grid = 0;
   Ctrl* d_ctrl = nullptr;
   cudaEvent_t ev_start = nullptr, ev_k1 = nullptr, ev_end = nullptr;
+  cudaEvent_t ev_k1h = nullptr;  // class split: end of the heavy pass
+  std::map<int, ClassPlan> classes;
+  std::map<cudaGraphExec_t, int> exec_class;  // 1: the graph runs the class-split pass
   std::map<ExecKey, std::pair<cudaGraph_t, cudaGraphExec_t>> execs;
   // K1W runs: the pass is launched on its own; its tail (round-1 candidates +
   // the round loop) is a graph instantiated and run only if it logged a read
@@ -305,6 +319,7 @@ int ensure_run_buffers(gcol_cuda_graph* g) {
   GCOL_CK(take_event(g->device, true, &g->ev_start));
   GCOL_CK(take_event(g->device, true, &g->ev_k1));
   GCOL_CK(take_event(g->device, true, &g->ev_end));
+  GCOL_CK(take_event(g->device, true, &g->ev_k1h));
   GCOL_CK(take_stream(g->device, &g->out_stream));
   GCOL_CK(take_event(g->device, false, &g->ev_final));
   if (g->gs.rows[1] > 0) {  // rows the rounds split into pieces
@@ -410,7 +425,7 @@ void free_split(gcol_cuda_graph* g, SplitPlan& P) {
   for (void* p : {static_cast<void*>(P.d_slot_v), static_cast<void*>(P.d_slot_deg),
                   static_cast<void*>(P.d_slot_left), static_cast<void*>(P.d_slot_bm),
                   static_cast<void*>(P.d_q), static_cast<void*>(P.d_q_seq),
-                  static_cast<void*>(P.d_ctr)})
+                  static_cast<void*>(P.d_ctr), static_cast<void*>(P.d_q16)})
     if (p) cudaFreeAsync(p, g->stream);
 }
 
@@ -425,6 +440,12 @@ int reset_split(gcol_cuda_graph* g, const SplitPlan* P, int warps) {
                             g->stream));
     GCOL_CK(cudaMemsetAsync(P->d_q_seq, 0, sizeof(unsigned) * static_cast<size_t>(P->npieces),
                             g->stream));
+    if (P->d_q16) {  // K1H: records unpublished (all ones), slot counts from zero
+      GCOL_CK(cudaMemsetAsync(P->d_q16, 0xff, sizeof(HvPiece) * static_cast<size_t>(P->npieces),
+                              g->stream));
+      GCOL_CK(cudaMemsetAsync(P->d_slot_left, 0, sizeof(int) * static_cast<size_t>(P->nslots),
+                              g->stream));
+    }
   }
   return GCOL_OK;
 }
@@ -476,7 +497,8 @@ int k1_variant(const gcol_cuda_graph* g, int k1_wide) {
   const bool small = g->max_degree <= kSmallMax;
   if (k1_wide == 3 && small) return 2;
   if (k1_wide == 0 && small) return 2;
-  return use_wide(g, k1_wide == 3 ? 0 : k1_wide) ? 1 : 0;
+  if ((k1_wide == 0 || k1_wide == 4) && !small) return 3;  // class split
+  return use_wide(g, k1_wide == 3 || k1_wide == 4 ? 0 : k1_wide) ? 1 : 0;
 }
 
 // option k1_wait_polls: 0 default, > 0 that many re-checks, < 0 none (every
@@ -543,6 +565,189 @@ int plan_k1_wait(gcol_cuda_graph* g, K1Launch* K, int polls) {
   return GCOL_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Class-split initial pass (gcol_k1c.cuh): heavy-row table per graph, then a
+// launch plan for K1H (heavy rows, degree >= T) and K1L (the waiting pass over
+// the light rows).
+// ---------------------------------------------------------------------------
+int class_threshold() {
+  static const int v = [] {
+    const char* e = std::getenv("GCOL_CLASS_T");
+    return e ? std::max(2, std::min(kSmallMax + 1, std::atoi(e))) : kClassTDefault;
+  }();
+  return v;
+}
+
+int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* e = std::getenv(name);
+  return e ? std::max(lo, std::min(hi, std::atoi(e))) : dflt;
+}
+
+int get_class(gcol_cuda_graph* g, int T, ClassPlan** out) {
+  auto it = g->classes.find(T);
+  if (it != g->classes.end()) {
+    *out = &it->second;
+    return GCOL_OK;
+  }
+  ClassPlan P;
+  P.T = T;
+  const int n = static_cast<int>(g->n);
+  const int nb = static_cast<int>((g->n + kClassSpan - 1) / kClassSpan);
+  if (nb > 0) {
+    int* d_cnt = nullptr;
+    GCOL_CK(dalloc(&d_cnt, static_cast<size_t>(nb) + 1, g->stream));
+    k_class_count<<<nb, kBlock, 0, g->stream>>>(g->d_off, n, T, d_cnt);
+    k_class_scan<<<1, 1024, 0, g->stream>>>(d_cnt, nb, d_cnt + nb);
+    GCOL_CK(cudaGetLastError());
+    int nh = 0;
+    GCOL_CK(cudaMemcpyAsync(&nh, d_cnt + nb, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+    note_d2h(g, sizeof(int));
+    GCOL_CK(cudaStreamSynchronize(g->stream));
+    P.nh = nh;
+    GCOL_CK(dalloc(&P.d_rows, static_cast<size_t>(nh), g->stream));
+    if (nh > 0) k_class_write<<<nb, kBlock, 0, g->stream>>>(g->d_off, n, T, d_cnt, P.d_rows);
+    GCOL_CK(cudaGetLastError());
+    GCOL_CK(cudaFreeAsync(d_cnt, g->stream));
+  }
+  g->classes[T] = P;
+  *out = &g->classes[T];
+  return GCOL_OK;
+}
+
+// Both passes of the class split: K (light, K1W kClass) and KH (heavy).
+struct ClassLaunch {
+  K1Launch light;
+  int grid_h = 0;
+  PairLogArgs LH{};
+  SplitArgs S{};
+  HeavyArgs H{};
+  const SplitPlan* plan = nullptr;
+  int nregions = 0;
+};
+
+const void* k1_light_fn(bool m32) {
+  return m32 ? reinterpret_cast<const void*>(k1_wait<false, true, true>)
+             : reinterpret_cast<const void*>(k1_wait<false, false, true>);
+}
+
+int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
+  const int T = class_threshold();
+  ClassPlan* CP = nullptr;
+  if (int rc = get_class(g, T, &CP)) return rc;
+  // light pass: a fully resident waiting grid (as K1W)
+  K1Launch& K = C->light;
+  K.wfn = k1_light_fn(T <= 32);
+  int occ = 1;
+  GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K.wfn, kWaitBlock, 0));
+  occ = std::max(1, std::min(occ, 2048 / kWaitBlock));
+  occ = env_int("GCOL_K1L_BPS", occ, 1, occ);
+  const long long tiles = (g->n + 31) / 32;
+  const long long wpb = kWaitBlock / 32;
+  K.grid1 = static_cast<int>(std::max(1LL, std::min<long long>(static_cast<long long>(g->sms) * occ,
+                                                               (tiles + wpb - 1) / wpb)));
+  K.cw = 0;
+  K.smem = 0;
+  K.plan = nullptr;
+  K.W = WaitArgs{nullptr, 0, polls, 1, 0, env_int("GCOL_K1W_SLEEP", 128, 0, 100000), nullptr, 0ull};
+  K.W.light_lim = T;
+  // heavy pass: kHvWarps-warp CTAs, GCOL_K1H_BPS per SM (the in-flight window)
+  auto hfn = k1_heavy<PairLog>;
+  GCOL_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(hfn),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHvSmem)));
+  int hocc = 1;
+  GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hocc, hfn, kHvThreads, kHvSmem));
+  hocc = std::max(1, hocc);
+  const int bps = env_int("GCOL_K1H_BPS", 1, 1, hocc);
+  const long long chunks = (CP->nh + kHvWarps - 1) / kHvWarps;
+  C->grid_h = static_cast<int>(std::max(1LL, std::min<long long>(static_cast<long long>(g->sms) * bps,
+                                                                 chunks)));
+  SplitPlan* P = nullptr;
+  if (int rc = get_split(g, kSplitDefault, &P)) return rc;  // colours of non-split rows < 1024
+  if (P->nslots > kHvSlotMax) return fail(GCOL_ERR_CAPACITY, "too many split rows for K1H");
+  if (P->nslots > 0 && !P->d_q16) GCOL_CK(dalloc(&P->d_q16, static_cast<size_t>(P->npieces), g->stream));
+  C->plan = P;
+  C->S = SplitArgs{P->nslots > 0 ? kSplitDefault : INT_MAX, P->d_slot_v, P->d_slot_deg,
+                   P->d_slot_left, P->d_slot_bm, P->d_q, P->d_q_seq, P->d_ctr, P->d_ctr + 1,
+                   reinterpret_cast<int*>(P->d_ctr + 2), C->grid_h, P->d_ctr + 3,
+                   nullptr, 0, 0, 1, 0};
+  C->H = HeavyArgs{P->d_q16, CP->d_rows, CP->nh, env_int("GCOL_K1H_ROWW", 4, 1, kHvWarps - 1),
+                   env_int("GCOL_K1H_RECHECK", 1, 0, 1), P->d_ctr + 3,
+                   std::getenv("GCOL_K1_PROFILE") ? 1 : 0, static_cast<long long>(g->m)};
+  // log slices: [0, grid_h) heavy CTAs (15/16 of the log: K1H logs its stale
+  // reads), then the light CTAs (K1L logs only reads whose wait timed out)
+  C->nregions = C->grid_h + K.grid1;
+  const unsigned long long per_h = g->pair_cap * 15 / 16 / static_cast<unsigned long long>(C->grid_h);
+  const unsigned long long per_l = g->pair_cap / 16 / static_cast<unsigned long long>(K.grid1);
+  const int cap_h = static_cast<int>(std::min<unsigned long long>(per_h, 1u << 30));
+  const int cap_l = static_cast<int>(std::min<unsigned long long>(per_l, 1u << 30));
+  C->LH = PairLogArgs{g->d_pairs, cap_h, g->d_pair_counts, &g->d_ctrl->pair_overflow};
+  K.L = PairLogArgs{g->d_pairs + static_cast<size_t>(C->grid_h) * cap_h, cap_l,
+                    g->d_pair_counts + C->grid_h, &g->d_ctrl->pair_overflow};
+  return GCOL_OK;
+}
+
+// Adds mark -> K1H -> (event) -> K1L after `dep`; *last = the K1L node.
+// Both persistent kernels are cooperative launches: their waits (drift
+// bound, piece mailboxes, lower-row waits) need every CTA resident, and a
+// cooperative node fails instead of hanging when that cannot be guaranteed.
+int add_class_nodes(gcol_cuda_graph* g, cudaGraph_t graph, cudaGraphNode_t dep, ClassLaunch& C,
+                    cudaGraphNode_t* last) {
+  ClassPlan* CP = &g->classes[class_threshold()];
+  cudaGraphNode_t n_mark, n_h, n_evh, n_l;
+  GCOL_CK(add_kernel(&n_mark, graph, &dep, 1, k_mark_pending, dim3(g->sms * 4), dim3(kBlock),
+                     static_cast<const HeavyRow*>(CP->d_rows), CP->nh, g->d_colors));
+  {
+    const long long* off = g->d_off;
+    const int* cols = g->d_cols;
+    void* args[] = {&off, &cols, &g->d_colors, &g->d_ctrl, &C.LH, &C.S, &C.H};
+    cudaKernelNodeParams p{};
+    p.func = reinterpret_cast<void*>(k1_heavy<PairLog>);
+    p.gridDim = dim3(C.grid_h);
+    p.blockDim = dim3(kHvThreads);
+    p.sharedMemBytes = static_cast<unsigned>(kHvSmem);
+    p.kernelParams = args;
+    GCOL_CK(cudaGraphAddKernelNode(&n_h, graph, &n_mark, 1, &p));
+  }
+  cudaLaunchAttributeValue coop{};
+  coop.cooperative = 1;
+  GCOL_CK(cudaGraphKernelNodeSetAttribute(n_h, cudaLaunchAttributeCooperative, &coop));
+  GCOL_CK(cudaGraphAddEventRecordNode(&n_evh, graph, &n_h, 1, g->ev_k1h));
+  const int n = static_cast<int>(g->n);
+  void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &g->d_colors, &g->d_ctrl,
+                  &C.light.L, &C.light.W};
+  cudaKernelNodeParams p{};
+  p.func = const_cast<void*>(C.light.wfn);
+  p.gridDim = dim3(C.light.grid1);
+  p.blockDim = dim3(kWaitBlock);
+  p.sharedMemBytes = 0;
+  p.kernelParams = args;
+  GCOL_CK(cudaGraphAddKernelNode(&n_l, graph, &n_evh, 1, &p));
+  GCOL_CK(cudaGraphKernelNodeSetAttribute(n_l, cudaLaunchAttributeCooperative, &coop));
+  *last = n_l;
+  return GCOL_OK;
+}
+
+// The same two passes launched eagerly on the library stream.
+int launch_class_eager(gcol_cuda_graph* g, ClassLaunch& C) {
+  ClassPlan* CP = &g->classes[class_threshold()];
+  k_mark_pending<<<g->sms * 4, kBlock, 0, g->stream>>>(CP->d_rows, CP->nh, g->d_colors);
+  GCOL_CK(cudaGetLastError());
+  {
+    const long long* off = g->d_off;
+    const int* cols = g->d_cols;
+    void* args[] = {&off, &cols, &g->d_colors, &g->d_ctrl, &C.LH, &C.S, &C.H};
+    GCOL_CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k1_heavy<PairLog>),
+                                        dim3(C.grid_h), dim3(kHvThreads), args, kHvSmem, g->stream));
+  }
+  GCOL_CK(cudaEventRecord(g->ev_k1h, g->stream));
+  const int n = static_cast<int>(g->n);
+  void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &g->d_colors, &g->d_ctrl,
+                  &C.light.L, &C.light.W};
+  GCOL_CK(cudaLaunchCooperativeKernel(C.light.wfn, dim3(C.light.grid1), dim3(kWaitBlock), args, 0,
+                                      g->stream));
+  return GCOL_OK;
+}
+
 template <bool kSnap, bool kLower, bool kLog, int CW>
 int plan_k1_cw(gcol_cuda_graph* g, int k1_blocks, int split_min, long long nitems, K1Launch* K) {
   auto k1 = k1_pipe<kSnap, kLower, kLog, CW>;
@@ -601,11 +806,80 @@ int split_min_of(const gcol_cuda_options& opt) {
   return v > 0 ? std::max(v, kSmallMax + 1) : kSplitDefault;
 }
 
+// Ordered round 1 (gcol_round1.cuh): on unless GCOL_ORDERED_R1=0; not for
+// the kOrdered rule (its rounds push higher neighbours instead).
+bool ordered_round1(int rule) {
+  static const int on = env_int("GCOL_ORDERED_R1", 0, 0, 1);
+  return on && rule != kOrdered;
+}
+
+int ordered_grid(gcol_cuda_graph* g, const void* fn) {
+  int occ = 1;
+  GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, 0));
+  return g->sms * std::max(1, occ);
+}
+
+constexpr size_t kSortSmem = sizeof(unsigned long long) * kSortCap;
+
+// After `dep`: sort the round-1 worklist, the ordered round, k_control
+// (closes round 1 as finish_round does).  *last = the k_control node.
+template <int R>
+int add_round1_nodes(gcol_cuda_graph* g, cudaGraph_t graph, cudaGraphNode_t dep,
+                     cudaGraphConditionalHandle handle, cudaGraphNode_t* last) {
+  cudaGraphNode_t n_sort, n_ord, n_ctl;
+  GCOL_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_sort_members<R>),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(kSortSmem)));
+  {
+    const long long* off = g->d_off;
+    void* args[] = {&off, &g->d_ctrl};
+    cudaKernelNodeParams p{};
+    p.func = reinterpret_cast<void*>(k_sort_members<R>);
+    p.gridDim = dim3(1);
+    p.blockDim = dim3(1024);
+    p.sharedMemBytes = static_cast<unsigned>(kSortSmem);
+    p.kernelParams = args;
+    GCOL_CK(cudaGraphAddKernelNode(&n_sort, graph, &dep, 1, &p));
+  }
+  const int grid = ordered_grid(g, reinterpret_cast<const void*>(k_ordered_round<R>));
+  GCOL_CK(add_kernel(&n_ord, graph, &n_sort, 1, k_ordered_round<R>, dim3(grid), dim3(kBlock),
+                     static_cast<const long long*>(g->d_off), static_cast<const int*>(g->d_cols),
+                     g->d_colors, g->d_ctrl, g->d_marks));
+  cudaLaunchAttributeValue coop{};
+  coop.cooperative = 1;
+  GCOL_CK(cudaGraphKernelNodeSetAttribute(n_ord, cudaLaunchAttributeCooperative, &coop));
+  GCOL_CK(add_kernel(&n_ctl, graph, &n_ord, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle, 1));
+  *last = n_ctl;
+  return GCOL_OK;
+}
+
+template <int R>
+int launch_round1_eager(gcol_cuda_graph* g) {
+  GCOL_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_sort_members<R>),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(kSortSmem)));
+  k_sort_members<R><<<1, 1024, kSortSmem, g->stream>>>(g->d_off, g->d_ctrl);
+  GCOL_CK(cudaGetLastError());
+  const int grid = ordered_grid(g, reinterpret_cast<const void*>(k_ordered_round<R>));
+  const long long* off = g->d_off;
+  const int* cols = g->d_cols;
+  void* args[] = {&off, &cols, &g->d_colors, &g->d_ctrl, &g->d_marks};
+  GCOL_CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_ordered_round<R>), dim3(grid),
+                                      dim3(kBlock), args, 0, g->stream));
+  k_control<<<1, 1, 0, g->stream>>>(g->d_ctrl, cudaGraphConditionalHandle{}, 0);
+  GCOL_CK(cudaGetLastError());
+  return GCOL_OK;
+}
+
 template <int R, bool kLower>
 int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int polls,
                      cudaGraph_t* out_graph, cudaGraphExec_t* out_exec) {
   K1Launch K;
-  if (kLower && k1v == 2) {
+  ClassLaunch CL;
+  const bool cls = kLower && k1v == 3;
+  if (cls) {
+    if (int rc = plan_k1_class(g, &CL, polls)) return rc;
+  } else if (kLower && k1v == 2) {
     if (int rc = plan_k1_wait(g, &K, polls)) return rc;
   } else if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K, k1v == 1)) {
     return rc;
@@ -617,7 +891,9 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
   cudaGraphConditionalHandle handle;
   GCOL_CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev0, graph, nullptr, 0, g->ev_start));
-  if (K.cw == 0) {
+  if (cls) {
+    if (int rc = add_class_nodes(g, graph, n_ev0, CL, &n_k1)) return rc;
+  } else if (K.cw == 0) {
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &g->d_colors, &g->d_ctrl, &K.L, &K.W};
     cudaKernelNodeParams p{};
     p.func = const_cast<void*>(K.wfn);
@@ -644,15 +920,19 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
   }
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev1, graph, &n_k1, 1, g->ev_k1));
   GCOL_CK(add_kernel(&n_cand, graph, &n_ev1, 1, k_candidates<R>, dim3(g->sms * 4), dim3(kBlock),
-                     g->d_off, g->d_cols, n, static_cast<const int*>(g->d_colors), g->d_ctrl, K.L,
-                     K.grid1, g->d_marks));
+                     g->d_off, g->d_cols, n, static_cast<const int*>(g->d_colors), g->d_ctrl,
+                     cls ? CL.LH : K.L, cls ? CL.grid_h : K.grid1, g->d_marks,
+                     cls ? CL.light.L : PairLogArgs{}, cls ? CL.light.grid1 : 0));
+  cudaGraphNode_t n_pre_while = n_cand;
+  if (ordered_round1(R))
+    if (int rc = add_round1_nodes<R>(g, graph, n_cand, handle, &n_pre_while)) return rc;
 
   cudaGraphNodeParams cp{};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = handle;
   cp.conditional.type = cudaGraphCondTypeWhile;
   cp.conditional.size = 1;
-  GCOL_CK(cudaGraphAddNode(&n_while, graph, &n_cand, 1, &cp));
+  GCOL_CK(cudaGraphAddNode(&n_while, graph, &n_pre_while, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   cudaGraphNode_t b_list, b_heavy, b_ctl;
   GCOL_CK(add_kernel(&b_list, body, nullptr, 0, k_list<R, false>, dim3(g->sms * 4), dim3(kBlock),
@@ -663,7 +943,8 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
   GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle, 1));
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, graph, &n_while, 1, g->ev_end));
   GCOL_CK(cudaGraphInstantiate(out_exec, graph, 0));
-  g->k1_warps[*out_exec] = K.grid1 * (K.cw ? K.cw : kWaitBlock / 32);
+  g->k1_warps[*out_exec] = cls ? CL.grid_h * CL.H.row_warps : K.grid1 * (K.cw ? K.cw : kWaitBlock / 32);
+  g->exec_class[*out_exec] = cls ? 1 : 0;
   *out_graph = graph;
   return GCOL_OK;
 }
@@ -686,13 +967,16 @@ int build_k1w_tail(gcol_cuda_graph* g, const K1Launch& K, cudaGraph_t* out_graph
   cudaGraphNode_t n_cand, n_while, n_ev2;
   GCOL_CK(add_kernel(&n_cand, graph, nullptr, 0, k_candidates<R>, dim3(g->sms * 4), dim3(kBlock),
                      g->d_off, g->d_cols, n, static_cast<const int*>(g->d_colors), g->d_ctrl, K.L,
-                     K.grid1, g->d_marks));
+                     K.grid1, g->d_marks, PairLogArgs{}, 0));
+  cudaGraphNode_t n_pre_while = n_cand;
+  if (ordered_round1(R))
+    if (int rc = add_round1_nodes<R>(g, graph, n_cand, handle, &n_pre_while)) return rc;
   cudaGraphNodeParams cp{};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = handle;
   cp.conditional.type = cudaGraphCondTypeWhile;
   cp.conditional.size = 1;
-  GCOL_CK(cudaGraphAddNode(&n_while, graph, &n_cand, 1, &cp));
+  GCOL_CK(cudaGraphAddNode(&n_while, graph, &n_pre_while, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   cudaGraphNode_t b_list, b_heavy, b_ctl;
   GCOL_CK(add_kernel(&b_list, body, nullptr, 0, k_list<R, false>, dim3(g->sms * 4), dim3(kBlock),
@@ -714,7 +998,14 @@ template <int R, bool kLower>
 int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int polls) {
   K1Launch K;
   const int n = static_cast<int>(g->n);
-  if (kLower && k1v == 2) {
+  ClassLaunch CL;
+  const bool cls = kLower && k1v == 3;
+  if (cls) {
+    if (int rc = plan_k1_class(g, &CL, polls)) return rc;
+    if (int rc = reset_split(g, CL.plan, CL.grid_h * CL.H.row_warps)) return rc;
+    GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
+    if (int rc = launch_class_eager(g, CL)) return rc;
+  } else if (kLower && k1v == 2) {
     if (int rc = plan_k1_wait(g, &K, polls)) return rc;
     K.W.close_round = 1;  // as in the graph: nothing logged -> round 1 closed, no loop
     GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
@@ -730,7 +1021,7 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
                                    g->d_colors, g->d_ctrl, drift_rounds(g), 0);
   }
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
-  if (K.cw == 0) {  // as the split K1W graph: the tail only if a read was logged
+  if (!cls && K.cw == 0) {  // as the split K1W graph: the tail only if a read was logged
     GCOL_CK(cudaEventRecord(g->ev_end, g->stream));
     int done = 0;
     GCOL_CK(cudaMemcpyAsync(&done, &g->d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost,
@@ -740,7 +1031,21 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
     if (done) return GCOL_OK;
   }
   k_candidates<R><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, n, g->d_colors,
-                                                         g->d_ctrl, K.L, K.grid1, g->d_marks);
+                                                         g->d_ctrl, cls ? CL.LH : K.L,
+                                                         cls ? CL.grid_h : K.grid1, g->d_marks,
+                                                         cls ? CL.light.L : PairLogArgs{},
+                                                         cls ? CL.light.grid1 : 0);
+  if (ordered_round1(R)) {
+    if (int rc = launch_round1_eager<R>(g)) return rc;
+    int done = 0;
+    GCOL_CK(cudaMemcpyAsync(&done, &g->d_ctrl->done, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+    note_d2h(g, sizeof(int));
+    GCOL_CK(cudaStreamSynchronize(g->stream));
+    if (done) {
+      GCOL_CK(cudaEventRecord(g->ev_end, g->stream));
+      return GCOL_OK;
+    }
+  }
   for (;;) {
     k_list<R, false><<<g->sms * 4, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, g->d_colors,
                                                             g->d_ctrl, g->d_heavy, g->d_marks);
@@ -1521,6 +1826,8 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
     cudaGraphDestroy(kv.second.first);
   }
   for (auto& kv : g->splits) free_split(g, kv.second);
+  for (auto& kv : g->classes)
+    if (kv.second.d_rows && g->stream) cudaFreeAsync(kv.second.d_rows, g->stream);
   if (g->stream) {
     if (g->owns_csr) {
       cudaFreeAsync(g->d_off, g->stream);
@@ -1544,8 +1851,8 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
     cudaStreamSynchronize(g->out_stream);
     give_stream(g->device, g->out_stream);
   }
-  for (cudaEvent_t ev : {g->ev_start, g->ev_k1, g->ev_end})
-    give_event(g->device, true, ev);
+  for (cudaEvent_t ev : {g->ev_start, g->ev_k1, g->ev_end, g->ev_k1h})
+    if (ev) give_event(g->device, true, ev);
   give_event(g->device, false, g->ev_final);
   delete g;
   return GCOL_OK;
@@ -1627,9 +1934,13 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
       GCOL_CK(cudaGraphLaunch(tl->second.second, g->stream));
     }
   } else {
-    auto sp = g->splits.find(mm);
+    const bool cls = g->exec_class[exec] != 0;
+    auto sp = g->splits.find(cls ? kSplitDefault : mm);
     if (sp != g->splits.end())
       if (int rc = reset_split(g, &sp->second, g->k1_warps[exec])) return rc;
+    // the class-split passes read rows anywhere in the adjacency: a streamed
+    // upload must be complete first (they are not piece-aware)
+    if (cls && g->ev_copied) GCOL_CK(cudaStreamWaitEvent(g->stream, g->ev_copied, 0));
     GCOL_CK(cudaGraphLaunch(exec, g->stream));
   }
   // streamed upload: K1 followed the pieces; what comes next reads anything
@@ -1675,7 +1986,24 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
       }
     }
   const int rounds = hdr.round;
-  if (std::getenv("GCOL_K1_PROFILE")) {
+  const bool class_run = (exec && g->exec_class[exec]) || (eager && lower && wide == 3);
+  if (std::getenv("GCOL_K1_PROFILE") && class_run) {
+    const unsigned long long* P = hdr.prof;
+    const double r = std::max(1.0, static_cast<double>(P[6]));
+    const double pcs = std::max(1.0, static_cast<double>(P[7]));
+    std::fprintf(stderr,
+                 "[k1h profile] row warps: %.0f cycles per row (take %.0f, block0 %.0f, later blocks "
+                 "%.0f [%llu], re-check %.0f, rest %.0f) | piece warps: %.0f cycles per piece (pop "
+                 "%.0f, TMA wait %.0f, gathers %.0f, finish %.0f), busy %.1f%% | rows %llu pieces "
+                 "%llu\n",
+                 (P[0] + P[1] + P[2] + P[3] + P[4]) / r, P[0] / r, P[1] / r, P[2] / r,
+                 static_cast<unsigned long long>(P[8]), P[3] / r, P[4] / r,
+                 (P[9] + P[10] + P[11] + P[12]) / pcs, P[12] / pcs, P[9] / pcs, P[10] / pcs,
+                 P[11] / pcs,
+                 100.0 * (P[9] + P[10] + P[11] + P[12]) /
+                     std::max(1.0, static_cast<double>(P[9] + P[10] + P[11] + P[12] + P[5])),
+                 static_cast<unsigned long long>(P[6]), static_cast<unsigned long long>(P[7]));
+  } else if (std::getenv("GCOL_K1_PROFILE")) {
     const double ch = hdr.prof[5] ? static_cast<double>(hdr.prof[5]) : 1.0;
     const double pc = hdr.prof[11] ? static_cast<double>(hdr.prof[11]) : 1.0;
     std::fprintf(stderr,
@@ -1693,9 +2021,10 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
     GCOL_CK(cudaMemcpyAsync(cpr.data(), g->d_ctrl->cpr, sizeof(unsigned long long) * cpr.size(),
                             cudaMemcpyDeviceToHost, g->stream));
   note_d2h(g, sizeof(unsigned long long) * cpr.size());
-  float ms_total = 0.f, ms_k1 = 0.f;
+  float ms_total = 0.f, ms_k1 = 0.f, ms_k1h = 0.f;
   GCOL_CK(cudaEventElapsedTime(&ms_total, g->ev_start, g->ev_end));
   GCOL_CK(cudaEventElapsedTime(&ms_k1, g->ev_start, g->ev_k1));
+  if (class_run) GCOL_CK(cudaEventElapsedTime(&ms_k1h, g->ev_start, g->ev_k1h));
   if (g_trace && g->ev_copy0) {
     float a = 0.f, b = 0.f, c = 0.f;
     cudaEventSynchronize(g->ev_copied);
@@ -1729,6 +2058,8 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
     stats->fallback_triggered = 0;
     stats->wall_time_ns = static_cast<uint64_t>(static_cast<double>(ms_total) * 1e6);
     stats->initial_pass_ns = static_cast<uint64_t>(static_cast<double>(ms_k1) * 1e6);
+    stats->heavy_pass_ns = static_cast<uint64_t>(static_cast<double>(ms_k1h) * 1e6);
+    stats->heavy_rows = class_run ? static_cast<uint64_t>(g->classes[class_threshold()].nh) : 0;
     stats->cpr_len = static_cast<uint64_t>(rounds);
     if (stats->conflicts_per_round)
       for (uint64_t i = 0; i < cpr.size() && i < stats->cpr_cap; ++i)

@@ -43,7 +43,7 @@ enum Rule : int { kIdLow = 0, kIdHigh = 1, kDegId = 2, kOrdered = 3 };
 // Device control block: round state of the on-device round loop (the GPU
 // RoundState of parallel.hpp:115-138).
 struct Ctrl {
-  unsigned long long tile_cursor;   // K1 ascending tile claim (for_claimed_chunks analog)
+  unsigned long long ord_ticket;    // ordered round 1: members handed out in priority order
   unsigned long long pair_len;      // K1 in-flight observations logged
   unsigned long long k1_gathers;    // neighbour-colour loads issued by K1
   int* in_list;                     // current round's worklist
@@ -58,6 +58,7 @@ struct Ctrl {
   int pair_overflow;
   int capped;
   int cand_total;                   // round-1 candidates
+  int ord_sorted;                   // ordered round 1: the worklist is in priority order
   int done;                         // loop exit flag (eager mode reads it)
   // heavy rows (deg > kWarpMax) of a round, split into kHPiece-entry pieces
   // spread over the whole grid (k_heavy); slots are per heavy row
@@ -72,7 +73,7 @@ struct Ctrl {
   int* hslot_flag;                  // 1: the row is defective
   unsigned* hslot_bm;               // [hslots][kBWinWords] colours seen, 0..16383
   unsigned k1_ctas_done;            // K1W: CTAs finished (the last one may end the run)
-  unsigned long long prof[16];      // K1 phase cycle counters (GCOL_K1_PROFILE)
+  unsigned long long prof[24];      // K1 phase cycle counters (GCOL_K1_PROFILE)
   unsigned long long cpr[kMaxRoundsRecorded];  // conflicts_per_round
 };
 

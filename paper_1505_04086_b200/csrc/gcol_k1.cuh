@@ -509,17 +509,21 @@ __device__ bool k1_pop(const SplitArgs& S, int* s_mbhead, int& slot, int& start,
   return ok != 0;
 }
 
-template <bool kSnap, bool kLower, bool kLog, class PL>
+// win: 32 shared-memory words owned by the warp.  kPend: the colour value
+// of a lower neighbour that is still in flight (-1 in K1; -2, "pending
+// heavy row", in the class-split heavy pass, where -1 is a light row that
+// has not started and reads this row itself later).
+template <bool kSnap, bool kLower, bool kLog, class PL, int kPend = -1>
 __device__ __forceinline__ void k1_piece(const long long* __restrict__ off, const int* __restrict__ cols,
                          const int* csrc, int* cdst, const SplitArgs& S, int slot, int start,
-                         K1Warp& W, uint64_t pol, const PL& L, unsigned& gathers) {
+                         unsigned* win, uint64_t pol, const PL& L, unsigned& gathers) {
   constexpr int U = 8;
   const int lane = lane_id();
   const int v = S.slot_v[slot];
   const int deg = S.slot_deg[slot];
   const long long b = ld_off(off + v, pol);
   const int end = min(deg, start + kPiece);
-  W.win[lane] = 0u;
+  win[lane] = 0u;
   __syncwarp();
   unsigned long long reg = 0ull;
   // a piece that starts above v holds no lower neighbour (sorted row)
@@ -544,9 +548,9 @@ __device__ __forceinline__ void k1_piece(const long long* __restrict__ off, cons
         gathers += take[u];
         if (c[u] >= 0 && c[u] <= deg) {
           if (c[u] < 64) reg |= 1ull << c[u];
-          else if (c[u] < 1024) atomicOr(&W.win[c[u] >> 5], 1u << (c[u] & 31));
+          else if (c[u] < 1024) atomicOr(&win[c[u] >> 5], 1u << (c[u] & 31));
         }
-        if (kLog) log_pairs(L, take[u] && c[u] == -1, w[u], v);
+        if (kLog) log_pairs(L, take[u] && c[u] == kPend, w[u], v);
       }
       if (kLower && __any_sync(kFull, past)) break;
     }
@@ -554,7 +558,7 @@ __device__ __forceinline__ void k1_piece(const long long* __restrict__ off, cons
   const unsigned lo = __reduce_or_sync(kFull, (unsigned)reg);
   const unsigned hi = __reduce_or_sync(kFull, (unsigned)(reg >> 32));
   __syncwarp();
-  unsigned word = W.win[lane];
+  unsigned word = win[lane];
   if (lane == 0) word |= lo;
   if (lane == 1) word |= hi;
   if (word) atomicOr(S.slot_bm + (size_t)slot * 32 + lane, word);
@@ -573,7 +577,7 @@ __device__ __forceinline__ void k1_piece(const long long* __restrict__ off, cons
     } else {  // 1024 distinct lower colours: scan the next windows
       color = -1;
       for (int wb = 1024; color < 0 && wb <= deg; wb += 1024)
-        color = warp_ff_window<kSnap, kLower>(cols, csrc, v, b, deg, wb, W.win, pol);
+        color = warp_ff_window<kSnap, kLower>(cols, csrc, v, b, deg, wb, win, pol);
     }
     if (lane == 0) commit_color(cdst, v, color);
   }
@@ -619,6 +623,17 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
 
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 1-D TMA bulk copy global -> shared with an L2 cache policy (streamed CSR:
+// evict_first, so the colour array stays L2-resident).
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, unsigned bytes,
+                                                 unsigned long long* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 
 // 1-D TMA bulk copy global -> shared, completion counted on `bar`.
@@ -717,7 +732,7 @@ __device__ __forceinline__ void stage_chunk(K1Slot<CW>& sl, int rows, int min_de
   const int bulk = A + room <= m ? room : (avail & ~3);
   if (bulk) {
     mbar_expect_tx(&sl.full, (unsigned)bulk * 4u);
-    tma_load_1d(sl.stage + dst, cols + A, (unsigned)bulk * 4u, &sl.full);
+    tma_load_1d_hint(sl.stage + dst, cols + A, (unsigned)bulk * 4u, &sl.full, pol);
   }
   for (int j = bulk; j < avail; ++j) sl.stage[dst + j] = ld_col(cols + A + j, pol);
   // per-row stage offsets: row i lies in run (long rows before i), capped at 31
@@ -879,7 +894,7 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
             sl.rows = rows;
             sl.chunk = c;
             mbar_arrive_expect_tx(&sl.full, (unsigned)bulk * 4u);
-            if (bulk) tma_load_1d(sl.stage, cols + A, (unsigned)bulk * 4u, &sl.full);
+            if (bulk) tma_load_1d_hint(sl.stage, cols + A, (unsigned)bulk * 4u, &sl.full, pol);
           }
         } else {
           stage_chunk<CW>(sl, rows, S.min_deg, cols, m, pol);
@@ -968,7 +983,7 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
       }
       if (got) {
         const long long tp = clock64();
-        k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W, pol, L,
+        k1_piece<kSnap, kLower, kLog>(off, cols, csrc, cdst, S, pslot, pstart, W.win, pol, L,
                                       gathers);
         ct_piece += clock64() - tp;
         continue;

@@ -51,6 +51,8 @@ struct WaitArgs {
   unsigned long long* trace;    // GCOL_K1W_TRACE (tooling): per tile {start, end} ns
   unsigned long long loop;      // the round loop's WHILE handle (0: none)
   int close_round;              // the last CTA closes round 1 when nothing was logged
+  int light_lim;                // class-split light pass: rows of degree >= light_lim are
+                                //   the heavy pass's (already coloured, skipped)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -86,7 +88,11 @@ __device__ __forceinline__ int first_free(Mask m) {
 // Scan of the lane's lower-id prefix (sorted row: stops at the first entry
 // above v), warp-collective: mask = colours seen (<= deg), pp = positions of
 // the neighbours read while still uncoloured (in flight).
-template <int kW, class Mask>
+// kClass (light pass of the class-split initial pass, gcol_k1c.cuh): the
+// WHOLE row is read -- its heavy neighbours of any id were coloured by the
+// heavy pass and must be avoided -- and only an uncoloured LOWER neighbour
+// is in flight (an uncoloured higher one is a light row that reads this one).
+template <int kW, class Mask, bool kClass = false>
 __device__ __forceinline__ void k1w_scan(const ColsGlobal& src, const int* colors, int v,
                                          bool valid, long long b, int deg, unsigned& gathers,
                                          Mask& mask, unsigned long long& pp) {
@@ -99,15 +105,16 @@ __device__ __forceinline__ void k1w_scan(const ColsGlobal& src, const int* color
     for (int j = 0; j < kW; ++j) w[j] = (active && k + j < deg) ? src(b + k + j) : 0x7fffffff;
     int c[kW];
 #pragma unroll
-    for (int j = 0; j < kW; ++j) c[j] = w[j] < v ? ld_color(colors + w[j]) : -2;
+    for (int j = 0; j < kW; ++j)
+      c[j] = (kClass ? w[j] != 0x7fffffff : w[j] < v) ? ld_color(colors + w[j]) : -2;
 #pragma unroll
     for (int j = 0; j < kW; ++j) {
-      gathers += w[j] < v;
+      gathers += kClass ? w[j] != 0x7fffffff : w[j] < v;
       if (static_cast<unsigned>(c[j]) <= static_cast<unsigned>(deg)) mask |= bit_of<Mask>(c[j]);
-      if (c[j] == -1) pp |= 1ull << (k + j);
+      if (c[j] == -1 && (!kClass || w[j] < v)) pp |= 1ull << (k + j);
     }
     // sorted row: once an entry above v (or the row end) is reached, done
-    active = active && k + kW < deg && w[kW - 1] < v;
+    active = active && k + kW < deg && (kClass || w[kW - 1] < v);
   }
 }
 
@@ -157,7 +164,9 @@ constexpr int kWaitScanW = 4;   // adjacency entries per scan step
 constexpr int kWaitMinBlocks = 6;  // 48 resident warps per SM: 40 registers
 
 // kM32: every degree is <= 31, so the forbidden set fits 32 bits.
-template <bool kStream, bool kM32>
+// kClass: the light pass of the class-split initial pass (gcol_k1c.cuh):
+// rows of degree >= A.light_lim are skipped and whole rows are scanned.
+template <bool kStream, bool kM32, bool kClass = false>
 __global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
     k1_wait(const long long* __restrict__ off, const int* __restrict__ cols, int n, int* colors,
             Ctrl* ctrl, PairLogArgs LA, WaitArgs A) {
@@ -198,7 +207,9 @@ __global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
     const int tn = t + NW;
     long long nb = 0;
     if (tn < ntiles) nb = ld_off(off + min(tile_v0(tn) + lane, n), pol);
-    const int deg = valid ? (int)(e - b) : 0;
+    const int deg0 = valid ? (int)(e - b) : 0;
+    const bool mine = valid && (!kClass || deg0 < A.light_lim);
+    const int deg = mine ? deg0 : 0;
     if (kStream) {  // streamed upload: the tile's adjacency must be resident
       const long long lo = __shfl_sync(kFull, b, 0), hi = __shfl_sync(kFull, e, 31);
       if (lane == 0 && hi > lo)
@@ -210,8 +221,8 @@ __global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
     if (A.trace && lane == 0) t0 = globaltimer_ns();
     Mask mask;
     unsigned long long pp;
-    k1w_scan<kWaitScanW, Mask>(src, colors, v, valid, b, deg, gathers, mask, pp);
-    k1w_wait<Mask>(src, colors, v, valid, b, deg, A.max_polls, A.sleep_ns, mask, pp, L);
+    k1w_scan<kWaitScanW, Mask, kClass>(src, colors, v, mine, b, deg, gathers, mask, pp);
+    k1w_wait<Mask>(src, colors, v, mine, b, deg, A.max_polls, A.sleep_ns, mask, pp, L);
     if (A.trace && lane == 0) {
       A.trace[2 * (size_t)t] = t0;
       A.trace[2 * (size_t)t + 1] = globaltimer_ns();

@@ -25,16 +25,21 @@ template <int R>
 __global__ void __launch_bounds__(kBlock) k_candidates(const long long* __restrict__ off,
                                                        const int* __restrict__ cols, int n,
                                                        const int* colors, Ctrl* ctrl,
-                                                       PairLogArgs LA, int nregions, int* marks) {
+                                                       PairLogArgs LA, int nregions, int* marks,
+                                                       PairLogArgs LB = PairLogArgs{},
+                                                       int nregionsB = 0) {
   const uint64_t pol = policy_evict_first();
   int* list = ctrl->in_list;
   int* len = &ctrl->in_len;
   const int lane = lane_id();
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   if (!ctrl->pair_overflow) {
-    for (int rg = blockIdx.x; rg < nregions; rg += gridDim.x) {
-      const int cnt = LA.counts[rg];
-      const int2* pairs = LA.pairs + (size_t)rg * LA.region_cap;
+    // two slice sets (the class-split pass: heavy CTAs' slices, light CTAs')
+    for (int rg = blockIdx.x; rg < nregions + nregionsB; rg += gridDim.x) {
+      const bool a = rg < nregions;
+      const int r = a ? rg : rg - nregions;
+      const int cnt = a ? LA.counts[r] : LB.counts[r];
+      const int2* pairs = a ? LA.pairs + (size_t)r * LA.region_cap : LB.pairs + (size_t)r * LB.region_cap;
       for (int i0 = (threadIdx.x & ~31); i0 < cnt; i0 += blockDim.x) {
         const int i = i0 + lane;
         bool pred = false;
@@ -58,11 +63,28 @@ __global__ void __launch_bounds__(kBlock) k_candidates(const long long* __restri
         append_warp(list, len, pred, loser);
       }
     }
-  } else {
+  } else {  // the log overflowed: test every vertex (rows above 32 entries warp-wide)
     for (long long v0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); v0 < n;
          v0 += (long long)stride) {
       const int v = (int)(v0 + lane);
-      const bool pred = v < n && thread_defective<R>(off, cols, colors, v, pol);
+      long long b = 0;
+      int deg = 0;
+      if (v < n) {
+        b = ld_off(off + v, pol);
+        deg = (int)(ld_off(off + v + 1, pol) - b);
+      }
+      bool pred = v < n && deg <= 32 && thread_defective<R>(off, cols, colors, v, pol);
+      unsigned big = __ballot_sync(kFull, v < n && deg > 32);
+      while (big) {
+        const int r = __ffs(big) - 1;
+        big &= big - 1;
+        const int vr = __shfl_sync(kFull, v, r);
+        const long long br = __shfl_sync(kFull, b, r);
+        const int dr = __shfl_sync(kFull, deg, r);
+        const bool d = warp_defective<R>(off, cols, colors, vr, br, dr, pol);
+        if (lane == r) pred = d;
+      }
+      if (pred) marks[v] = 1;  // a member of round 1 (the ordered round waits on members)
       append_warp(list, len, pred, v);
     }
   }

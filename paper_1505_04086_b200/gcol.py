@@ -150,6 +150,8 @@ class ColoringStats:
     k1_gathers: int = 0
     h2d_bytes: int = 0       # bytes the call copied host -> device (incl. the upload
     d2h_bytes: int = 0       # on a handle's first call) / device -> host
+    heavy_pass_ns: int = 0   # class-split initial pass: device time of the heavy-row pass
+    heavy_rows: int = 0      # rows of that pass (degree >= 64); 0 when not split
 
 
 @dataclass
@@ -342,7 +344,7 @@ def _stats_from_c(s: _lib.Stats, cpr: np.ndarray) -> ColoringStats:
         initial_pass_ns=s.initial_pass_ns, pairs_logged=s.pairs_logged,
         round1_candidates=s.round1_candidates, pair_overflow=bool(s.pair_overflow),
         priority=Priority(s.priority), k1_gathers=s.k1_gathers, h2d_bytes=s.h2d_bytes,
-        d2h_bytes=s.d2h_bytes)
+        d2h_bytes=s.d2h_bytes, heavy_pass_ns=s.heavy_pass_ns, heavy_rows=s.heavy_rows)
 
 
 # --- coloring entry points -------------------------------------------------------

@@ -25,7 +25,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(_lib.LIB, s), f"{s} declared in include/gcol_cuda.h but not exported"
         assert s in _lib.SIGNATURES, f"{s} has no ctypes signature"
-    assert _lib.LIB.gcol_cuda_abi_version() == 1
+    assert _lib.LIB.gcol_cuda_abi_version() == 2
 
 
 def test_struct_layouts_match_header():
