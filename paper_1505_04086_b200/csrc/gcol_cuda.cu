@@ -670,9 +670,19 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
                    P->d_slot_left, P->d_slot_bm, P->d_q, P->d_q_seq, P->d_ctr, P->d_ctr + 1,
                    reinterpret_cast<int*>(P->d_ctr + 2), C->grid_h, P->d_ctr + 3,
                    nullptr, 0, 0, 1, 0};
-  C->H = HeavyArgs{P->d_q16, CP->d_rows, CP->nh, env_int("GCOL_K1H_ROWW", 4, 1, kHvWarps - 1),
+  // The in-flight window (row warps) and the piece warps, measured on B200
+  // (profiles/r02): with the colour array L2-resident (R-MAT
+  // 24) 4 row warps + 4 piece warps per CTA (more piece warps flood the LSU
+  // and slow the rows); when it is not (R-MAT 27: 537 MB of colours, gathers
+  // miss L2) pieces take longer and need 6, and the larger graph tolerates
+  // 5 row warps within the colour band.
+  const bool l2_colours = sizeof(int) * static_cast<size_t>(g->n) <= (size_t{64} << 20);
+  const int rw_default = CP->nh >= (4 << 20) ? 5 : 4;
+  const int pw_default = l2_colours ? 4 : 6;
+  C->H = HeavyArgs{P->d_q16, CP->d_rows, CP->nh, env_int("GCOL_K1H_ROWW", rw_default, 1, kHvWarps - 1),
                    env_int("GCOL_K1H_RECHECK", 1, 0, 1), P->d_ctr + 3,
-                   std::getenv("GCOL_K1_PROFILE") ? 1 : 0, static_cast<long long>(g->m)};
+                   std::getenv("GCOL_K1_PROFILE") ? 1 : 0, static_cast<long long>(g->m),
+                   env_int("GCOL_K1H_PIECEW", pw_default, 1, kHvPieceWarps)};
   // log slices: [0, grid_h) heavy CTAs (15/16 of the log: K1H logs its stale
   // reads), then the light CTAs (K1L logs only reads whose wait timed out)
   C->nregions = C->grid_h + K.grid1;
@@ -684,6 +694,34 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
   K.L = PairLogArgs{g->d_pairs + static_cast<size_t>(C->grid_h) * cap_h, cap_l,
                     g->d_pair_counts + C->grid_h, &g->d_ctrl->pair_overflow};
   return GCOL_OK;
+}
+
+// L2 residency of the colour array during the class-split passes: a
+// persisting access-policy window over it (GCOL_L2_PERSIST=0 disables).
+// Every colour gather of the passes goes to it; the CSR streams past with
+// evict_first.  Returns false when the device offers no persisting L2.
+bool colour_window(gcol_cuda_graph* g, cudaAccessPolicyWindow* w) {
+  static const int on = env_int("GCOL_L2_PERSIST", 1, 0, 1);
+  if (!on) return false;
+  int maxp = 0, maxw = 0;
+  cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g->device);
+  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
+  if (maxp <= 0 || maxw <= 0) return false;
+  static bool limit_set = false;
+  if (!limit_set) {
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(maxp)) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    limit_set = true;
+  }
+  const size_t bytes = std::min<size_t>(sizeof(int) * static_cast<size_t>(g->n), static_cast<size_t>(maxw));
+  w->base_ptr = g->d_colors;
+  w->num_bytes = bytes;
+  w->hitRatio = static_cast<float>(std::min(1.0, static_cast<double>(maxp) / static_cast<double>(bytes)));
+  w->hitProp = cudaAccessPropertyPersisting;
+  w->missProp = cudaAccessPropertyStreaming;
+  return true;
 }
 
 // Adds mark -> K1H -> (event) -> K1L after `dep`; *last = the K1L node.
@@ -723,6 +761,11 @@ int add_class_nodes(gcol_cuda_graph* g, cudaGraph_t graph, cudaGraphNode_t dep, 
   p.kernelParams = args;
   GCOL_CK(cudaGraphAddKernelNode(&n_l, graph, &n_evh, 1, &p));
   GCOL_CK(cudaGraphKernelNodeSetAttribute(n_l, cudaLaunchAttributeCooperative, &coop));
+  cudaLaunchAttributeValue apw{};
+  if (colour_window(g, &apw.accessPolicyWindow)) {
+    GCOL_CK(cudaGraphKernelNodeSetAttribute(n_h, cudaLaunchAttributeAccessPolicyWindow, &apw));
+    GCOL_CK(cudaGraphKernelNodeSetAttribute(n_l, cudaLaunchAttributeAccessPolicyWindow, &apw));
+  }
   *last = n_l;
   return GCOL_OK;
 }

@@ -93,6 +93,7 @@ struct HeavyArgs {
   unsigned* cursor;   // batches claimed (global, ascending)
   int prof;           // GCOL_K1_PROFILE: per-phase cycle counters into ctrl->prof
   long long m;        // adjacency length (bulk copies never read past it)
+  int piece_warps;    // active piece warps per CTA (1 .. kHvPieceWarps)
 };
 
 // --------------------------------------------------------------------------
@@ -344,6 +345,10 @@ __device__ __forceinline__ void hv_tick(int on, long long& t_last, long long& ac
 }
 
 constexpr int kHvPieceBuf = kPiece + 4;
+#ifndef GCOL_K1H_PB
+#define GCOL_K1H_PB 8
+#endif
+constexpr int kHvPieceBatch = GCOL_K1H_PB;  // colour gathers per lane in flight (piece warps)
 
 // One piece: staged by TMA into the warp's buffer, its lower neighbours'
 // colours gathered 16 per lane at a time, OR-ed into the row's bitmap; the
@@ -376,7 +381,7 @@ __device__ __forceinline__ void hv_piece(const long long* __restrict__ off,
   phase ^= 1u;
   hv_tick(prof, t_last, pp[0]);
   unsigned long long reg = 0ull;
-  constexpr int B = 16;
+  constexpr int B = kHvPieceBatch;
   for (int t0 = 0; t0 < 32; t0 += B) {
     int w[B], c[B];
     bool past = false;
@@ -492,7 +497,7 @@ __device__ __forceinline__ void hv_row(const int* __restrict__ cols, int* colors
   __syncwarp();
 }
 
-constexpr int kHvPieceWarps = 8;                       // piece warps per CTA
+constexpr int kHvPieceWarps = 8;                       // piece-warp slots per CTA
 constexpr int kHvBufs = 3;                             // staged batches per CTA
 constexpr int kHvThreads = (kHvWarps + kHvPieceWarps) * 32;
 // dynamic shared memory: piece buffers, then the staged rows' first blocks
@@ -561,7 +566,9 @@ __global__ void __launch_bounds__(kHvThreads, 1)
   long long pp[4] = {0, 0, 0, 0};
   long long t_last = clock64();
 
-  if (warp >= kHvWarps) {
+  if (warp >= kHvWarps + H.piece_warps) {
+    // idle piece slot
+  } else if (warp >= kHvWarps) {
     // ------------------------------ piece warps ------------------------------
     const int pw = warp - kHvWarps;
     unsigned pphase = 0, pc_hint = 0;

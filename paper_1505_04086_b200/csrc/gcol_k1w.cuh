@@ -118,6 +118,42 @@ __device__ __forceinline__ void k1w_scan(const ColsGlobal& src, const int* color
   }
 }
 
+// The light pass's scan (kClass): the WHOLE row, kW entries per step, with
+// the next step's adjacency loads issued before this step's colour gathers,
+// so a step costs one dependent round trip instead of two (light rows reach
+// degree 63: up to 8 steps, and the slowest lane sets the tile's time).
+template <int kW, class Mask>
+__device__ __forceinline__ void k1l_scan(const ColsGlobal& src, const int* colors, int v,
+                                         bool valid, long long b, int deg, unsigned& gathers,
+                                         Mask& mask, unsigned long long& pp) {
+  mask = 0;
+  pp = 0ull;
+  const int steps = valid ? (deg + kW - 1) / kW : 0;
+  const int maxs = (int)__reduce_max_sync(kFull, (unsigned)steps);
+  int wn[kW];
+#pragma unroll
+  for (int j = 0; j < kW; ++j) wn[j] = (valid && j < deg) ? src(b + j) : 0x7fffffff;
+  for (int s = 0; s < maxs; ++s) {
+    const int k = s * kW;
+    int w[kW];
+#pragma unroll
+    for (int j = 0; j < kW; ++j) w[j] = wn[j];
+    if (s + 1 < maxs) {
+#pragma unroll
+      for (int j = 0; j < kW; ++j) wn[j] = (valid && k + kW + j < deg) ? src(b + k + kW + j) : 0x7fffffff;
+    }
+    int c[kW];
+#pragma unroll
+    for (int j = 0; j < kW; ++j) c[j] = w[j] != 0x7fffffff ? ld_color(colors + w[j]) : -2;
+#pragma unroll
+    for (int j = 0; j < kW; ++j) {
+      gathers += w[j] != 0x7fffffff;
+      if (static_cast<unsigned>(c[j]) <= static_cast<unsigned>(deg)) mask |= bit_of<Mask>(c[j]);
+      if (c[j] == -1 && w[j] < v) pp |= 1ull << (k + j);
+    }
+  }
+}
+
 // Commit the row if nothing it read was in flight; else re-check the
 // in-flight ones until they are coloured (after max_polls: log the rest for
 // round 1) and commit.  Warp-collective.
@@ -161,13 +197,21 @@ __device__ __forceinline__ void k1w_wait(const ColsGlobal& src, int* colors, int
 }
 
 constexpr int kWaitScanW = 4;   // adjacency entries per scan step
+#ifndef GCOL_K1L_W
+#define GCOL_K1L_W 8
+#endif
+constexpr int kLightScanW = GCOL_K1L_W;  // light pass (kClass): entries per pipelined step
+#ifndef GCOL_K1L_MINB
+#define GCOL_K1L_MINB 4
+#endif
+constexpr int kLightMinBlocks = GCOL_K1L_MINB;  // light pass: 32 resident warps per SM (64 registers)
 constexpr int kWaitMinBlocks = 6;  // 48 resident warps per SM: 40 registers
 
 // kM32: every degree is <= 31, so the forbidden set fits 32 bits.
 // kClass: the light pass of the class-split initial pass (gcol_k1c.cuh):
 // rows of degree >= A.light_lim are skipped and whole rows are scanned.
 template <bool kStream, bool kM32, bool kClass = false>
-__global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
+__global__ void __launch_bounds__(kWaitBlock, kClass ? kLightMinBlocks : kWaitMinBlocks)
     k1_wait(const long long* __restrict__ off, const int* __restrict__ cols, int n, int* colors,
             Ctrl* ctrl, PairLogArgs LA, WaitArgs A) {
   using Mask = typename std::conditional<kM32, unsigned, unsigned long long>::type;
@@ -221,7 +265,10 @@ __global__ void __launch_bounds__(kWaitBlock, kWaitMinBlocks)
     if (A.trace && lane == 0) t0 = globaltimer_ns();
     Mask mask;
     unsigned long long pp;
-    k1w_scan<kWaitScanW, Mask, kClass>(src, colors, v, mine, b, deg, gathers, mask, pp);
+    if (kClass)
+      k1l_scan<kLightScanW, Mask>(src, colors, v, mine, b, deg, gathers, mask, pp);
+    else
+      k1w_scan<kWaitScanW, Mask>(src, colors, v, mine, b, deg, gathers, mask, pp);
     k1w_wait<Mask>(src, colors, v, mine, b, deg, A.max_polls, A.sleep_ns, mask, pp, L);
     if (A.trace && lane == 0) {
       A.trace[2 * (size_t)t] = t0;
