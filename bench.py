@@ -377,6 +377,8 @@ def run_ours(args):
 
     walls = [r.stats.wall_time_ns * 1e-9 for r in runs]
     k1s = [r.stats.initial_pass_ns * 1e-9 for r in runs]
+    k1hs = [r.stats.heavy_pass_ns * 1e-9 for r in runs]
+    class_split = runs[-1].stats.heavy_rows > 0
     tot = sum(walls)
     if dist:
         t = torch.tensor([tot], dtype=torch.float64, device="cuda")
@@ -384,29 +386,40 @@ def run_ours(args):
         tot = float(t.item())
     ms_per_step = tot / args.steps * 1e3
     value = world * m / (tot / args.steps) / 1e9
-    # K1 + k_candidates, then k_list + k_heavy + k_control per round; with
-    # K1W (max degree <= 63) that logged nothing, K1W alone (the rest of its
-    # graph is launched only when a read was logged)
-    launches = sum(1 if (maxdeg <= 63 and r.stats.pairs_logged == 0) else 2 + 3 * r.stats.rounds
-                   for r in runs)
+    # K1W (max degree <= 63) that logged nothing: K1W alone (the rest of its
+    # graph is launched only when a read was logged).  Class split (skewed
+    # degree): k_mark_pending + k1_heavy + k1_wait<light> + k_candidates, then
+    # k_list + k_heavy + k_control per round.  Else k1_pipe + k_candidates +
+    # 3 per round.
+    def launches_of(st):
+        if maxdeg <= 63 and st.pairs_logged == 0:
+            return 1
+        return (4 if st.heavy_rows > 0 else 2) + 3 * st.rounds
+    launches = sum(launches_of(r.stats) for r in runs)
     colors = [r.stats.num_colors for r in runs]
     rounds = [r.stats.rounds for r in runs]
     last = runs[-1].stats
 
-    # roofline of the dominant kernel (K1, the tentative-colour pass)
+    # roofline of the dominant kernel: the tentative-colour pass (one CUDA-
+    # event region: K1W, or k1_pipe, or the class split's mark + k1_heavy +
+    # k1_wait<light>)
     k1_mean = sum(k1s) / len(k1s)
     gathers = last.k1_gathers
     k1_bytes = 8 * (n + 1) + 4 * m + 4 * gathers + 4 * n
     achieved = k1_bytes / k1_mean / 1e9
     peak, peak_src = measured_peak()
     traffic = profile_traffic(args.config)
+    kname = ("k1_wait" if maxdeg <= 63 else
+             "k_mark_pending + k1_heavy + k1_wait<light> (class split)" if class_split else "k1_pipe")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": "k1_wait" if maxdeg <= 63 else "k1_pipe",
+                "kernel": kname,
                 "algorithmic_bytes_per_launch": k1_bytes,
                 "bytes_formula": "8(n+1) offsets + 4m cols + 4*gathers (lower-id neighbour "
                                  "colours) + 4n colour stores",
                 "k1_ms": k1_mean * 1e3, "k1_share_of_step": k1_mean / (tot / args.steps),
+                "k1_heavy_ms": (sum(k1hs) / len(k1hs) * 1e3) if class_split else None,
+                "heavy_rows": last.heavy_rows if class_split else None,
                 "peak_source": peak_src,
                 # north_star quotes the roofline against a nominal ~8 TB/s per B200
                 "frac_of_nominal_8tbs": achieved / 8000.0}

@@ -625,7 +625,10 @@ struct ClassLaunch {
   int nregions = 0;
 };
 
-const void* k1_light_fn(bool m32) {
+const void* k1_light_fn(bool m32, bool stream) {
+  if (stream)
+    return m32 ? reinterpret_cast<const void*>(k1_wait<true, true, true>)
+               : reinterpret_cast<const void*>(k1_wait<true, false, true>);
   return m32 ? reinterpret_cast<const void*>(k1_wait<false, true, true>)
              : reinterpret_cast<const void*>(k1_wait<false, false, true>);
 }
@@ -636,7 +639,7 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
   if (int rc = get_class(g, T, &CP)) return rc;
   // light pass: a fully resident waiting grid (as K1W)
   K1Launch& K = C->light;
-  K.wfn = k1_light_fn(T <= 32);
+  K.wfn = k1_light_fn(T <= 32, g->d_ready != nullptr);
   int occ = 1;
   GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K.wfn, kWaitBlock, 0));
   occ = std::max(1, std::min(occ, 2048 / kWaitBlock));
@@ -648,7 +651,8 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
   K.cw = 0;
   K.smem = 0;
   K.plan = nullptr;
-  K.W = WaitArgs{nullptr, 0, polls, 1, 0, env_int("GCOL_K1W_SLEEP", 128, 0, 100000), nullptr, 0ull};
+  K.W = WaitArgs{g->d_ready, g->piece_shift, polls, 1, 0, env_int("GCOL_K1W_SLEEP", 128, 0, 100000),
+                 nullptr, 0ull};
   K.W.light_lim = T;
   // heavy pass: kHvWarps-warp CTAs, GCOL_K1H_BPS per SM (the in-flight window)
   auto hfn = k1_heavy<PairLog>;
@@ -682,7 +686,7 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
   C->H = HeavyArgs{P->d_q16, CP->d_rows, CP->nh, env_int("GCOL_K1H_ROWW", rw_default, 1, kHvWarps - 1),
                    env_int("GCOL_K1H_RECHECK", 1, 0, 1), P->d_ctr + 3,
                    std::getenv("GCOL_K1_PROFILE") ? 1 : 0, static_cast<long long>(g->m),
-                   env_int("GCOL_K1H_PIECEW", pw_default, 1, kHvPieceWarps)};
+                   env_int("GCOL_K1H_PIECEW", pw_default, 1, kHvPieceWarps), g->d_ready, g->piece_shift};
   // log slices: [0, grid_h) heavy CTAs (15/16 of the log: K1H logs its stale
   // reads), then the light CTAs (K1L logs only reads whose wait timed out)
   C->nregions = C->grid_h + K.grid1;
@@ -1981,9 +1985,6 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
     auto sp = g->splits.find(cls ? kSplitDefault : mm);
     if (sp != g->splits.end())
       if (int rc = reset_split(g, &sp->second, g->k1_warps[exec])) return rc;
-    // the class-split passes read rows anywhere in the adjacency: a streamed
-    // upload must be complete first (they are not piece-aware)
-    if (cls && g->ev_copied) GCOL_CK(cudaStreamWaitEvent(g->stream, g->ev_copied, 0));
     GCOL_CK(cudaGraphLaunch(exec, g->stream));
   }
   // streamed upload: K1 followed the pieces; what comes next reads anything

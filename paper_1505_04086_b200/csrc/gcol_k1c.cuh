@@ -94,6 +94,8 @@ struct HeavyArgs {
   int prof;           // GCOL_K1_PROFILE: per-phase cycle counters into ctrl->prof
   long long m;        // adjacency length (bulk copies never read past it)
   int piece_warps;    // active piece warps per CTA (1 .. kHvPieceWarps)
+  const unsigned* piece_ready;  // streamed upload: flag per 2^piece_shift adjacency
+  int piece_shift;              //   entries resident (null: the whole CSR is resident)
 };
 
 // --------------------------------------------------------------------------
@@ -622,7 +624,14 @@ __global__ void __launch_bounds__(kHvThreads, 1)
       if (lane < avail) {
         e = s_pool[buf][lane];
         nc = hv_staged(e, H.m, S.min_deg);
+        // streamed upload: rows go out in ascending id = ascending adjacency
+        // order, following the upload front; a row is handed out only once
+        // its whole adjacency is resident
+        if (H.piece_ready && e.deg > 0)
+          for (long long q = e.b >> H.piece_shift; q <= (e.b + e.deg - 1) >> H.piece_shift; ++q)
+            while (ld_acquire_u32(H.piece_ready + q) == 0u) __nanosleep(256);
       }
+      __syncwarp();
       const unsigned bytes = __reduce_add_sync(kFull, (unsigned)nc * 4u);
       if (lane == 0) mbar_arrive_expect_tx(&s_colbar[buf], bytes);
       __syncwarp();

@@ -1,8 +1,7 @@
 set -x
-export PYTHONUNBUFFERED=1 PROBE_VERIFY=0
+export PYTHONUNBUFFERED=1
 OUT=gpurun_out/r2f
 mkdir -p $OUT
-for v in "4 6" "4 8" "5 6" "5 8"; do set -- $v
-( GCOL_K1H_ROWW=$1 GCOL_K1H_PIECEW=$2 timeout 900 python tools/class_probe.py rmat27 1 0 ) > "$OUT/probeS_rmat27_rw$1_pw$2.log" 2>&1
-done
-( GCOL_K1H_ROWW=4 GCOL_K1H_PIECEW=6 timeout 900 python tools/class_probe.py rmat24 2 0 ) > "$OUT/probeS_rmat24_rw4_pw6.log" 2>&1
+( timeout 900 python -m pytest tests -m gpu -x -q ) > $OUT/pytest_gpu3.log 2>&1
+( timeout 900 python bench.py --config rmat24 --steps 5 --warmup 3 --no-cpu-baseline ) > $OUT/bench24_e2e.json 2> $OUT/bench24_e2e.err
+( timeout 1200 python bench.py --config rmat27 --steps 5 --warmup 3 --no-cpu-baseline ) > $OUT/bench27_e2e.json 2> $OUT/bench27_e2e.err
