@@ -366,6 +366,17 @@ void tmark(const char* tag) {
   if (g_trace) g_trace->mark(tag);
 }
 
+// Peer pushes (multi-GPU) are switched on for the device by a __constant__
+// PeerSet that every colour-committing kernel of the module reads.  So that
+// no other handle's kernel can run while it is on: a partitioned call holds
+// the device's launch mutex from switching pushes on (after draining the
+// device) until they are off again and its stream has drained; every other
+// call holds the same mutex while it enqueues colour-committing kernels.
+std::mutex& device_launch_mutex(int dev) {
+  static std::mutex mus[64];
+  return mus[dev & 63];
+}
+
 bool is_pinned_host(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -835,17 +846,24 @@ int plan_k1(gcol_cuda_graph* g, int k1_blocks, int split_min, K1Launch* K, bool 
               : plan_k1_cw<kSnap, kLower, kLog, kCW>(g, k1_blocks, split_min, nitems, K);
 }
 
-// Launch of the planned K1 variant on `stream`.
+// Launch of the planned K1 variant on `stream`.  Cooperative: k1_pipe's
+// drift bound and piece mailboxes wait on other CTAs, so every CTA must be
+// resident; a cooperative launch that cannot guarantee it fails
+// (cudaErrorCooperativeLaunchTooLarge) instead of hanging.
 template <bool kSnap, bool kLower, bool kLog>
-void launch_k1(const K1Launch& K, cudaStream_t stream, const long long* off, const int* cols,
-               int n, int nitems, const int* wl, const int* csrc, int* cdst, Ctrl* ctrl,
-               int drift, int item0) {
+cudaError_t launch_k1(const K1Launch& K, cudaStream_t stream, const long long* off, const int* cols,
+                      int n, int nitems, const int* wl, const int* csrc, int* cdst, Ctrl* ctrl,
+                      int drift, int item0) {
+  PairLogArgs L = K.L;
+  SplitArgs S = K.S;
+  void* args[] = {&off, &cols, &n, &nitems, &wl, &csrc, &cdst, &ctrl, &L, &S, &drift, &item0};
   if (K.cw == kCWWide)
-    k1_pipe<kSnap, kLower, kLog, kCWWide><<<K.grid1, (kCWWide + k1_producers<kCWWide>()) * 32, K.smem, stream>>>(
-        off, cols, n, nitems, wl, csrc, cdst, ctrl, K.L, K.S, drift, item0);
-  else
-    k1_pipe<kSnap, kLower, kLog, kCW><<<K.grid1, (kCW + k1_producers<kCW>()) * 32, K.smem, stream>>>(
-        off, cols, n, nitems, wl, csrc, cdst, ctrl, K.L, K.S, drift, item0);
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k1_pipe<kSnap, kLower, kLog, kCWWide>),
+                                       dim3(K.grid1), dim3((kCWWide + k1_producers<kCWWide>()) * 32),
+                                       args, K.smem, stream);
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k1_pipe<kSnap, kLower, kLog, kCW>),
+                                     dim3(K.grid1), dim3((kCW + k1_producers<kCW>()) * 32), args,
+                                     K.smem, stream);
 }
 
 int split_min_of(const gcol_cuda_options& opt) {
@@ -949,6 +967,9 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
     p.sharedMemBytes = 0;
     p.kernelParams = args;
     GCOL_CK(cudaGraphAddKernelNode(&n_k1, graph, &n_ev0, 1, &p));
+    cudaLaunchAttributeValue coop{};
+    coop.cooperative = 1;
+    GCOL_CK(cudaGraphKernelNodeSetAttribute(n_k1, cudaLaunchAttributeCooperative, &coop));
   } else {
     int drift = drift_rounds(g);
     int item0 = 0;
@@ -964,6 +985,9 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
     p.sharedMemBytes = static_cast<unsigned>(K.smem);
     p.kernelParams = args;
     GCOL_CK(cudaGraphAddKernelNode(&n_k1, graph, &n_ev0, 1, &p));
+    cudaLaunchAttributeValue coop{};
+    coop.cooperative = 1;
+    GCOL_CK(cudaGraphKernelNodeSetAttribute(n_k1, cudaLaunchAttributeCooperative, &coop));
   }
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev1, graph, &n_k1, 1, g->ev_k1));
   GCOL_CK(add_kernel(&n_cand, graph, &n_ev1, 1, k_candidates<R>, dim3(g->sms * 4), dim3(kBlock),
@@ -1058,14 +1082,14 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
     GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
     {
       void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &g->d_colors, &g->d_ctrl, &K.L, &K.W};
-      GCOL_CK(cudaLaunchKernel(K.wfn, dim3(K.grid1), dim3(kWaitBlock), args, 0, g->stream));
+      GCOL_CK(cudaLaunchCooperativeKernel(K.wfn, dim3(K.grid1), dim3(kWaitBlock), args, 0, g->stream));
     }
   } else {
     if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K, k1v == 1)) return rc;
     if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
     GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
-    launch_k1<false, kLower, true>(K, g->stream, g->d_off, g->d_cols, n, n, nullptr, g->d_colors,
-                                   g->d_colors, g->d_ctrl, drift_rounds(g), 0);
+    GCOL_CK((launch_k1<false, kLower, true>(K, g->stream, g->d_off, g->d_cols, n, n, nullptr, g->d_colors,
+                                   g->d_colors, g->d_ctrl, drift_rounds(g), 0)));
   }
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
   if (!cls && K.cw == 0) {  // as the split K1W graph: the tail only if a read was logged
@@ -1947,6 +1971,8 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   GCOL_CK(cudaMemsetAsync(g->d_marks, 0, sizeof(int) * n, g->stream));
   if (int rc = reset_ctrl(g, static_cast<int>(opt.round_cap), g->d_listA, g->d_listB, nullptr, 0))
     return rc;
+  // colour-committing launches: under the device launch mutex (PeerScope)
+  std::unique_lock<std::mutex> launch_lk(device_launch_mutex(g->device));
   if (eager) {
     if (int rc = launch_eager(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide, polls))
       return rc;
@@ -1954,7 +1980,7 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
     const int nn = static_cast<int>(g->n);
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&nn), &g->d_colors, &g->d_ctrl, &KW.L, &KW.W};
     GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
-    GCOL_CK(cudaLaunchKernel(KW.wfn, dim3(KW.grid1), dim3(kWaitBlock), args, 0, g->stream));
+    GCOL_CK(cudaLaunchCooperativeKernel(KW.wfn, dim3(KW.grid1), dim3(kWaitBlock), args, 0, g->stream));
     GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
     GCOL_CK(cudaEventRecord(g->ev_end, g->stream));
     int done = 0;
@@ -1987,6 +2013,7 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
       if (int rc = reset_split(g, &sp->second, g->k1_warps[exec])) return rc;
     GCOL_CK(cudaGraphLaunch(exec, g->stream));
   }
+  launch_lk.unlock();
   // streamed upload: K1 followed the pieces; what comes next reads anything
   if (g->ev_copied) GCOL_CK(cudaStreamWaitEvent(g->stream, g->ev_copied, 0));
   // the colours are final here: a copy into pinned host memory overlaps the
@@ -2149,6 +2176,7 @@ int gcol_cuda_color_rsoc_csr(const int64_t* offsets, const int32_t* cols, int64_
 
 int gcol_cuda_first_fit_sequential(gcol_cuda_graph* g, int32_t* colors_out, int32_t colors_memory) {
   if (int rc = check_graph(g)) return rc;
+  std::lock_guard<std::mutex> launch_lk(device_launch_mutex(g->device));  // (PeerScope)
   GCOL_CK(cudaSetDevice(g->device));
   if (int rc = ensure_run_buffers(g)) return rc;
   const size_t n = static_cast<size_t>(g->n);
@@ -2162,7 +2190,7 @@ int gcol_cuda_first_fit_sequential(gcol_cuda_graph* g, int32_t* colors_out, int3
     if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, nullptr, 0)) return rc;
     const int nn = static_cast<int>(n);
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&nn), &g->d_colors, &g->d_ctrl, &K.L, &K.W};
-    GCOL_CK(cudaLaunchKernel(K.wfn, dim3(K.grid1), dim3(kWaitBlock), args, 0, g->stream));
+    GCOL_CK(cudaLaunchCooperativeKernel(K.wfn, dim3(K.grid1), dim3(kWaitBlock), args, 0, g->stream));
     Ctrl hdr;
     GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
     GCOL_CK(cudaStreamSynchronize(g->stream));
@@ -2211,9 +2239,9 @@ int run_catalyurek(gcol_cuda_graph* g, const gcol_cuda_options& opt,
         return rc;
       if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, nullptr, 0)) return rc;
       if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
-      launch_k1<false, false, false>(K, g->stream, g->d_off, g->d_cols, n, nin,
+      GCOL_CK((launch_k1<false, false, false>(K, g->stream, g->d_off, g->d_cols, n, nin,
                                      round == 1 ? nullptr : in, g->d_colors, g->d_colors,
-                                     g->d_ctrl, 0, 0);
+                                     g->d_ctrl, 0, 0)));
       if (round == 1) GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
     } else if (round == 1) {
       GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
@@ -2253,6 +2281,7 @@ extern "C" {
 int gcol_cuda_color_catalyurek(gcol_cuda_graph* g, const gcol_cuda_options* opt_in,
                                int32_t* colors_out, int32_t colors_memory, gcol_cuda_stats* stats) {
   if (int rc = check_graph(g)) return rc;
+  std::lock_guard<std::mutex> launch_lk(device_launch_mutex(g->device));  // (PeerScope)
   gcol_cuda_options opt;
   if (int rc = read_options(opt_in, &opt)) return rc;
   if (g->n > 0 && !colors_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "colors_out is null");
@@ -2358,6 +2387,7 @@ int gcol_cuda_tentative_snapshot(gcol_cuda_graph* g, const int32_t* colors_in,
                                  const int32_t* worklist, int64_t nwl, int32_t lower_only,
                                  int32_t* colors_out, int32_t memory) {
   if (int rc = check_graph(g)) return rc;
+  std::lock_guard<std::mutex> launch_lk(device_launch_mutex(g->device));  // (PeerScope)
   if (!colors_in || !colors_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "null colour buffer");
   GCOL_CK(cudaSetDevice(g->device));
   if (int rc = ensure_run_buffers(g)) return rc;
@@ -2380,11 +2410,11 @@ int gcol_cuda_tentative_snapshot(gcol_cuda_graph* g, const int32_t* colors_in,
     if (int r2 = reset_split(g, K.plan, K.grid1 * K.cw)) return r2;
     K.L = PairLogArgs{};
     if (lower_only)
-      launch_k1<true, true, false>(K, g->stream, g->d_off, g->d_cols, static_cast<int>(n), nitems,
-                                   d_wl, d_in, d_out, g->d_ctrl, 0, 0);
+      GCOL_CK((launch_k1<true, true, false>(K, g->stream, g->d_off, g->d_cols, static_cast<int>(n), nitems,
+                                   d_wl, d_in, d_out, g->d_ctrl, 0, 0)));
     else
-      launch_k1<true, false, false>(K, g->stream, g->d_off, g->d_cols, static_cast<int>(n),
-                                    nitems, d_wl, d_in, d_out, g->d_ctrl, 0, 0);
+      GCOL_CK((launch_k1<true, false, false>(K, g->stream, g->d_off, g->d_cols, static_cast<int>(n),
+                                    nitems, d_wl, d_in, d_out, g->d_ctrl, 0, 0)));
   }
   GCOL_CK(cudaGetLastError());
   if (int rc = copy_out(g, colors_out, d_out, sizeof(int) * n, memory)) return rc;
@@ -2418,6 +2448,7 @@ void launch_round_rule(gcol_cuda_graph* g, int rule) {
 int run_list_api(gcol_cuda_graph* g, const int32_t* colors, const int32_t* pending,
                  int64_t npending, int32_t priority, bool detect_only, int32_t* out,
                  int64_t* nout, int32_t memory, int32_t* colors_back) {
+  std::lock_guard<std::mutex> launch_lk(device_launch_mutex(g ? g->device : 0));  // (PeerScope)
   if (int rc = check_graph(g)) return rc;
   if (priority == GCOL_PRIORITY_DEFAULT) priority = GCOL_PRIORITY_DEGREE_ID;
   if (priority < GCOL_PRIORITY_ID_LOW || priority > GCOL_PRIORITY_ORDERED)
@@ -2543,9 +2574,9 @@ int gcol_cuda_k1_range(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, int3
   if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
   GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
   if (hi > lo)
-    launch_k1<false, true, true>(K, g->stream, g->d_off, g->d_cols, static_cast<int>(g->n),
+    GCOL_CK((launch_k1<false, true, true>(K, g->stream, g->d_off, g->d_cols, static_cast<int>(g->n),
                                  static_cast<int>(hi - lo), nullptr, colors_dev, colors_dev,
-                                 g->d_ctrl, drift_rounds(g), static_cast<int>(lo));
+                                 g->d_ctrl, drift_rounds(g), static_cast<int>(lo))));
   GCOL_CK(cudaGetLastError());
   GCOL_CK(cudaEventRecord(g->ev_end, g->stream));
   GCOL_CK(cudaStreamSynchronize(g->stream));
@@ -2561,13 +2592,33 @@ int gcol_cuda_k1_range(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, int3
 
 namespace {
 
-// Peer pushes on (the handle's partition) or off, in stream order.
-int set_peers(gcol_cuda_graph* g, bool on) {
-  static const PeerSet none{};
-  GCOL_CK(cudaMemcpyToSymbolAsync(c_peers, on ? &g->peers : &none, sizeof(PeerSet), 0,
-                                  cudaMemcpyHostToDevice, g->stream));
-  return GCOL_OK;
-}
+// Peer pushes on (the handle's partition) for the lifetime of the scope:
+// holds the device launch mutex, drains the device before switching them on
+// (no other handle's kernel can see them), switches them off and drains the
+// handle's stream before releasing it.
+struct PeerScope {
+  gcol_cuda_graph* g;
+  std::unique_lock<std::mutex> lk;
+  bool on_ = false;
+  explicit PeerScope(gcol_cuda_graph* g_) : g(g_), lk(device_launch_mutex(g_->device)) {}
+  int on() {
+    GCOL_CK(cudaDeviceSynchronize());
+    GCOL_CK(cudaMemcpyToSymbolAsync(c_peers, &g->peers, sizeof(PeerSet), 0, cudaMemcpyHostToDevice,
+                                    g->stream));
+    on_ = true;
+    return GCOL_OK;
+  }
+  int off() {
+    if (!on_) return GCOL_OK;
+    static const PeerSet none{};
+    on_ = false;
+    GCOL_CK(cudaMemcpyToSymbolAsync(c_peers, &none, sizeof(PeerSet), 0, cudaMemcpyHostToDevice,
+                                    g->stream));
+    GCOL_CK(cudaStreamSynchronize(g->stream));
+    return GCOL_OK;
+  }
+  ~PeerScope() { off(); }
+};
 
 template <int R>
 void launch_candidates(gcol_cuda_graph* g, const K1Launch& K, const int* colors) {
@@ -2626,18 +2677,19 @@ int gcol_cuda_k1_owned(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, int3
   if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, nullptr, 0)) return rc;
   if (!wait)
     if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
-  if (int rc = set_peers(g, true)) return rc;
+  PeerScope peers(g);
+  if (int rc = peers.on()) return rc;
   GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
   if (n > 0 && wait) {
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &colors_dev, &g->d_ctrl, &K.L, &K.W};
-    GCOL_CK(cudaLaunchKernel(K.wfn, dim3(K.grid1), dim3(kWaitBlock), args, 0, g->stream));
+    GCOL_CK(cudaLaunchCooperativeKernel(K.wfn, dim3(K.grid1), dim3(kWaitBlock), args, 0, g->stream));
   } else if (n > 0) {
-    launch_k1<false, true, true>(K, g->stream, g->d_off, g->d_cols, n, n, nullptr, colors_dev,
-                                 colors_dev, g->d_ctrl, drift_rounds(g), 0);
+    GCOL_CK((launch_k1<false, true, true>(K, g->stream, g->d_off, g->d_cols, n, n, nullptr, colors_dev,
+                                 colors_dev, g->d_ctrl, drift_rounds(g), 0)));
   }
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
   GCOL_CK(cudaGetLastError());
-  if (int rc = set_peers(g, false)) return rc;
+  if (int rc = peers.off()) return rc;
   g->owned_k1_grid = K.grid1;  // the log's slices, for gcol_cuda_candidates
   g->owned_k1_log = K.L;
   Ctrl hdr;
@@ -2724,7 +2776,8 @@ int gcol_cuda_round_list(gcol_cuda_graph* g, int32_t priority, int32_t* colors_d
   if (int rc = ensure_run_buffers(g)) return rc;
   if (int rc = reset_ctrl(g, 1, const_cast<int*>(in_dev), out_dev, nullptr, static_cast<int>(nin)))
     return rc;
-  if (int rc = set_peers(g, true)) return rc;  // recolours reach the peers' replicas
+  PeerScope peers(g);  // recolours reach the peers' replicas
+  if (int rc = peers.on()) return rc;
   if (nin > 0) {
     const int r = rule_of(priority);
     if (r == kIdLow) {
@@ -2739,7 +2792,7 @@ int gcol_cuda_round_list(gcol_cuda_graph* g, int32_t priority, int32_t* colors_d
     }
   }
   GCOL_CK(cudaGetLastError());
-  if (int rc = set_peers(g, false)) return rc;
+  if (int rc = peers.off()) return rc;
   Ctrl hdr;
   GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
   GCOL_CK(cudaStreamSynchronize(g->stream));

@@ -519,3 +519,113 @@ def test_k1w_streamed_one_call_is_serial_ff(monkeypatch, oracle_mod):
                               colors_out=out)
     assert run.stats.pairs_logged > 0
     check_run(hg, gcol.ColoringRun(out.numpy(), run.stats), 1)
+
+
+# --------------------------------------------------------------------------
+# Class-split initial pass (gcol_k1c.cuh): heavy rows (degree >= 64) by K1H,
+# light rows by the waiting pass K1L.
+# --------------------------------------------------------------------------
+def hub_graph(rng, n, hubs, hub_deg, avg):
+    """ER background plus `hubs` rows of degree ~hub_deg (split into
+    1024-entry pieces) and a band of degree-64..1023 rows: every K1H path."""
+    u = rng.integers(0, n, int(n * avg / 2))
+    v = rng.integers(0, n, u.size)
+    hu, hv = [], []
+    for h in rng.choice(n, hubs, replace=False):
+        nb = rng.choice(n, hub_deg, replace=False)
+        hu.append(np.full(nb.size, h))
+        hv.append(nb)
+    for m in rng.choice(n, max(1, n // 50), replace=False):
+        nb = rng.choice(n, int(rng.integers(64, 700)), replace=False)
+        hu.append(np.full(nb.size, m))
+        hv.append(nb)
+    u = np.concatenate([u] + hu)
+    v = np.concatenate([v] + hv)
+    return gcol.build_graph(np.stack([u, v], axis=1), n)
+
+
+def test_class_split_paths_valid(oracle_mod):
+    """Hubs (pieces + piece warps), medium rows (staged blocks), light rows
+    (waits), all three priority rules; properness/bounds judged on the CPU."""
+    rng = np.random.default_rng(2024)
+    for n, hubs, hd, avg in ((5000, 3, 2500, 4.0), (60_000, 40, 5000, 6.0), (200_000, 12, 40_000, 3.0)):
+        g = hub_graph(rng, n, hubs, hd, avg)
+        assert g.max_degree() >= 1024
+        for prio in (gcol.Priority.degree_id, gcol.Priority.id_low, gcol.Priority.id_high):
+            run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(priority=prio, k1_wide=4))
+            check_run(g, run, 1)
+            assert run.stats.heavy_rows > 0  # the class split ran
+            assert 0 < run.stats.heavy_pass_ns <= run.stats.initial_pass_ns
+
+
+def test_class_split_is_default_for_skewed_degree():
+    rng = np.random.default_rng(7)
+    g = hub_graph(rng, 20000, 5, 3000, 4.0)
+    run = gcol.color_rsoc(g, 1)
+    check_run(g, run, 1)
+    assert run.stats.heavy_rows > 0
+    # the single-sweep k1_pipe stays selectable
+    run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=1))
+    check_run(g, run, 1)
+    assert run.stats.heavy_rows == 0
+
+
+def test_class_split_rmat_scaled_band(oracle_mod):
+    """R-MAT (scale 18): class split valid and within the colour band of the
+    oracle's multi-threaded RSOC; the k1_pipe stays valid beside it."""
+    off, cols = graphs.make_config("rmat24", "cuda", scale_down=6)
+    g = gcol.Graph.from_device(off, cols)
+    hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
+    ours = []
+    for _ in range(3):
+        run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=4))
+        check_run(hg, run, 1)
+        assert run.stats.heavy_rows > 0
+        ours.append(run.stats.num_colors)
+    check_run(hg, gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=1)), 1)
+    o = oracle_mod.CSR(hg.offsets(), hg.adjacency())
+    counts = sorted(oracle_mod.color_parallel(o, 8, "rsoc")[1]["num_colors"] for _ in range(3))
+    assert sorted(ours)[1] <= int(1.05 * counts[1]), (ours, counts)
+
+
+def test_class_split_streamed_one_call(monkeypatch):
+    """One-call host path: K1H's producer follows the upload pieces (1M-entry
+    pieces here), the light pass its streaming variant."""
+    off, cols = graphs.make_config("rmat24", "cuda", scale_down=5)
+    h_off, h_cols = off.cpu().pin_memory(), cols.cpu().pin_memory()
+    hg = gcol.Graph(h_off.numpy(), h_cols.numpy())
+    out = torch.empty(off.numel() - 1, dtype=torch.int32).pin_memory()
+    for shift in ("31", "20", "20"):
+        monkeypatch.setenv("GCOL_UPLOAD_SHIFT", shift)
+        out.fill_(-7)
+        run = gcol.color_rsoc_csr(h_off, h_cols, 1, colors_out=out)
+        assert run.stats.heavy_rows > 0
+        check_run(hg, gcol.ColoringRun(out.numpy(), run.stats), 1)
+
+
+def test_concurrent_handles_complete():
+    """Two handles coloured at once from two host threads on one device: the
+    persistent passes are cooperative launches, so they either co-reside or
+    run one after the other -- never a hang -- and both colourings are
+    proper."""
+    import threading
+    rng = np.random.default_rng(31)
+    gs = [hub_graph(rng, 80_000, 20, 4000, 5.0), random_graph(rng, 300_000, 12.0)]
+    results, errors = [None, None], []
+
+    def work(i):
+        try:
+            results[i] = [gcol.color_rsoc(gs[i], 1) for _ in range(3)]
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in th), "a concurrent colouring hung"
+    assert not errors, errors
+    for g, runs in zip(gs, results):
+        for run in runs:
+            check_run(g, run, 1)
