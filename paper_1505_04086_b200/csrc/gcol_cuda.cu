@@ -129,6 +129,8 @@ struct gcol_cuda_graph {
   int* d_marks = nullptr;
   int* d_iota = nullptr;  // 0..n-1: Çatalyürek's first worklist
   unsigned char* d_vacc = nullptr;  // verification accumulator + colour census
+  unsigned long long* d_rowbad = nullptr;  // row-invariant check (k_check_rows)
+  int rows_state = 0;                      // 0 unchecked, 1 queued, 2 ok, 3 bad
   int2* d_pairs = nullptr;
   int* d_pair_counts = nullptr;
   unsigned long long pair_cap = 0;
@@ -299,6 +301,77 @@ __global__ void k_count_long(const long long* __restrict__ off, int n, int min_d
     atomicAdd(out, rows);
     atomicAdd(out + 1, pieces);
   }
+}
+
+// Row invariants the lower-id passes rely on (graph.hpp:47-76: rows sorted
+// strictly ascending, no self-loop, ids in range): one pass over the
+// adjacency, once per graph.  *bad = number of offending entries.
+__global__ void __launch_bounds__(kBlock) k_check_rows(const long long* __restrict__ off,
+                                                      const int* __restrict__ cols, int n,
+                                                      unsigned long long* bad) {
+  const int lane = lane_id();
+  unsigned long long cnt = 0;
+  for (long long v0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); v0 < n;
+       v0 += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(v0 + lane);
+    long long b = 0, e = 0;
+    if (v < n) {
+      b = __ldg(off + v);
+      e = __ldg(off + v + 1);
+    }
+    const bool big = e - b > 32;
+    if (v < n && !big) {  // thread per short row
+      int prev = -1;
+      for (long long i = b; i < e; ++i) {
+        const int w = __ldg(cols + i);
+        cnt += (w <= prev || w == v || w < 0 || w >= n) ? 1 : 0;
+        prev = w;
+      }
+    }
+    unsigned bm = __ballot_sync(kFull, v < n && big);
+    while (bm) {  // warp per long row: coalesced, each entry against its predecessor
+      const int r = __ffs(bm) - 1;
+      bm &= bm - 1;
+      const int vr = __shfl_sync(kFull, v, r);
+      const long long br = __shfl_sync(kFull, b, r), er = __shfl_sync(kFull, e, r);
+      for (long long i = br + lane; i < er; i += 32) {
+        const int w = __ldg(cols + i);
+        const int p = i > br ? __ldg(cols + i - 1) : -1;
+        cnt += (w <= p || w == vr || w < 0 || w >= n) ? 1 : 0;
+      }
+    }
+  }
+  cnt = __reduce_add_sync(kFull, (unsigned)min(cnt, 0xffffffffull));
+  if (lane == 0 && cnt) atomicAdd(bad, cnt);
+}
+
+// Launches the row check once per graph (after `stream`'s prior work); the
+// result is read with the next synchronisation (rows_checked).
+int queue_row_check(gcol_cuda_graph* g) {
+  if (g->rows_state != 0 || g->n == 0) return GCOL_OK;
+  if (!g->d_rowbad) GCOL_CK(dalloc(&g->d_rowbad, 1, g->stream));
+  GCOL_CK(cudaMemsetAsync(g->d_rowbad, 0, sizeof(unsigned long long), g->stream));
+  k_check_rows<<<g->sms * 8, kBlock, 0, g->stream>>>(g->d_off, g->d_cols, static_cast<int>(g->n),
+                                                     g->d_rowbad);
+  GCOL_CK(cudaGetLastError());
+  g->rows_state = 1;  // queued
+  return GCOL_OK;
+}
+
+// After a synchronisation: GCOL_ERR_INVALID_ARGUMENT if the rows break the
+// reference's invariants (graph.hpp:60-68 input_error).
+int rows_checked(gcol_cuda_graph* g) {
+  if (g->rows_state == 1) {
+    unsigned long long bad = 0;
+    GCOL_CK(cudaMemcpy(&bad, g->d_rowbad, sizeof(bad), cudaMemcpyDeviceToHost));
+    note_d2h(g, sizeof(bad));
+    g->rows_state = bad ? 3 : 2;
+  }
+  if (g->rows_state == 3)
+    return fail(GCOL_ERR_INVALID_ARGUMENT,
+                "graph: adjacency list not sorted strictly ascending, a self-loop, or an id out of "
+                "range (graph.hpp:60-68)");
+  return GCOL_OK;
 }
 
 int ensure_run_buffers(gcol_cuda_graph* g) {
@@ -1673,7 +1746,9 @@ int create_impl(const int64_t* offsets, const int32_t* cols, int64_t n, int64_t 
   if (!out) return fail(GCOL_ERR_INVALID_ARGUMENT, "out is null");
   *out = nullptr;
   if (n < 0 || m < 0) return fail(GCOL_ERR_INVALID_ARGUMENT, "negative size");
-  if (n >= 0x7fffffffLL)
+  // ids are int32 and the passes' 256-id chunk arithmetic is int: n below
+  // INT_MAX - 1024 keeps every chunk/tile index in range
+  if (n >= 0x7fffffffLL - 1024)
     return fail(GCOL_ERR_CAPACITY, "vertex count exceeds the 31-bit id space of int32 columns");
   if (!offsets) return fail(GCOL_ERR_INVALID_ARGUMENT, "offsets is null");
   if (m > 0 && !cols) return fail(GCOL_ERR_INVALID_ARGUMENT, "cols is null");
@@ -1906,6 +1981,7 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
     }
     if (g->d_iota) cudaFreeAsync(g->d_iota, g->stream);
     if (g->d_vacc) cudaFreeAsync(g->d_vacc, g->stream);
+    if (g->d_rowbad) cudaFreeAsync(g->d_rowbad, g->stream);
     for (void* p : {static_cast<void*>(g->d_hq), static_cast<void*>(g->d_hslot),
                     static_cast<void*>(g->d_hslot_bm), static_cast<void*>(g->d_vrows),
                     static_cast<void*>(g->d_vpre)})
@@ -2016,6 +2092,9 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   launch_lk.unlock();
   // streamed upload: K1 followed the pieces; what comes next reads anything
   if (g->ev_copied) GCOL_CK(cudaStreamWaitEvent(g->stream, g->ev_copied, 0));
+  // the lower-id passes rely on sorted rows: checked once per graph, behind
+  // the colouring (a graph that fails gets an error, not its colours)
+  if (int rc = queue_row_check(g)) return rc;
   // the colours are final here: a copy into pinned host memory overlaps the
   // verification pass below (both only read them)
   const bool early_out = colors_memory == GCOL_MEM_HOST && n > 0 && is_pinned_host(colors_out);
@@ -2046,6 +2125,7 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
   note_d2h(g, offsetof(Ctrl, cpr));
   GCOL_CK(cudaStreamSynchronize(g->stream));
+  if (int rc = rows_checked(g)) return rc;
   tmark("run");
   if (const char* tp = std::getenv("GCOL_K1W_TRACE"))
     if (g_k1w_trace) {  // tooling: dump the per-tile timestamps of this run
@@ -2182,11 +2262,14 @@ int gcol_cuda_first_fit_sequential(gcol_cuda_graph* g, int32_t* colors_out, int3
   const size_t n = static_cast<size_t>(g->n);
   GCOL_CK(cudaMemsetAsync(g->d_colors, 0xff, sizeof(int) * n, g->stream));
   bool exact = false;
+  if (int rc = queue_row_check(g)) return rc;
+  GCOL_CK(cudaStreamSynchronize(g->stream));
+  if (int rc = rows_checked(g)) return rc;  // K1W stops each row at its first entry above v
   if (n > 0 && g->max_degree <= kSmallMax) {
     // bounded degree: the waiting pass K1W is First-Fit in id order whenever
     // every wait resolved (nothing logged) -- the same colouring, in parallel
     K1Launch K;
-    if (int rc = plan_k1_wait(g, &K, kWaitPollsDefault)) return rc;
+    if (int rc = plan_k1_wait(g, &K, wait_polls(0))) return rc;  // GCOL_K1_WAIT_POLLS=0: serial kernel
     if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, nullptr, 0)) return rc;
     const int nn = static_cast<int>(n);
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&nn), &g->d_colors, &g->d_ctrl, &K.L, &K.W};

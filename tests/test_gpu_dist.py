@@ -144,4 +144,7 @@ def test_push_mode_one_rank_k1w_is_serial_ff():
     ops.k1_owned(colors)
     torch.cuda.synchronize()
     assert ops.candidates(colors).numel() == 0
-    assert np.array_equal(colors.cpu().numpy(), gcol.first_fit_sequential(hg))
+    from oracle import oracle as oracle_mod  # the CPU checker, not the device First-Fit
+    oracle_mod.build()
+    ff = oracle_mod.first_fit_sequential(oracle_mod.CSR(hg.offsets(), hg.adjacency()))
+    assert np.array_equal(colors.cpu().numpy(), ff)

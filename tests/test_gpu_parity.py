@@ -629,3 +629,34 @@ def test_concurrent_handles_complete():
     for g, runs in zip(gs, results):
         for run in runs:
             check_run(g, run, 1)
+
+
+def test_unsorted_rows_rejected():
+    """graph.hpp:60-68: rows must be sorted strictly ascending with no
+    self-loop; the lower-id passes rely on it, so such a CSR gets an
+    input error rather than colours."""
+    off = np.array([0, 2, 3, 4], dtype=np.int64)
+    cols = np.array([2, 1, 0, 0], dtype=np.int32)  # row 0 = [2, 1]: not ascending
+    g = gcol.Graph(off, cols)
+    with pytest.raises(gcol.input_error):
+        gcol.color_rsoc(g, 1)
+    with pytest.raises(gcol.input_error):
+        gcol.first_fit_sequential(g)
+
+
+def test_first_fit_serial_fallback_and_long_path(monkeypatch, oracle_mod):
+    """GCOL_K1_WAIT_POLLS=0 forces first_fit_sequential onto the serial
+    kernel (K1W logs every wait); a long path graph (dependency depth n)
+    exercises the waits: both equal the oracle's serial First-Fit."""
+    n = 20000
+    e = np.stack([np.arange(n - 1), np.arange(1, n)], axis=1)
+    path = gcol.build_graph(e, n)
+    rng = np.random.default_rng(5)
+    er = random_graph(rng, 5000, 8.0)
+    for g in (path, er):
+        ff = oracle_mod.first_fit_sequential(oracle_csr(oracle_mod, g))
+        assert np.array_equal(gcol.first_fit_sequential(g), ff)
+    monkeypatch.setenv("GCOL_K1_WAIT_POLLS", "0")
+    for g in (path, er):
+        ff = oracle_mod.first_fit_sequential(oracle_csr(oracle_mod, g))
+        assert np.array_equal(gcol.first_fit_sequential(g), ff)
