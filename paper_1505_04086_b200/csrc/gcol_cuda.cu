@@ -439,17 +439,6 @@ void tmark(const char* tag) {
   if (g_trace) g_trace->mark(tag);
 }
 
-// Peer pushes (multi-GPU) are switched on for the device by a __constant__
-// PeerSet that every colour-committing kernel of the module reads.  So that
-// no other handle's kernel can run while it is on: a partitioned call holds
-// the device's launch mutex from switching pushes on (after draining the
-// device) until they are off again and its stream has drained; every other
-// call holds the same mutex while it enqueues colour-committing kernels.
-std::mutex& device_launch_mutex(int dev) {
-  static std::mutex mus[64];
-  return mus[dev & 63];
-}
-
 bool is_pinned_host(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -1246,7 +1235,7 @@ int get_exec(gcol_cuda_graph* g, int rule, int lower, int k1_blocks, int mm, int
 
 // Resets the control block for a run (host-side struct, one H2D copy).
 int reset_ctrl(gcol_cuda_graph* g, int round_cap, int* in_list, int* out_list, int* flags,
-               int in_len) {
+               int in_len, const PeerSet* peers = nullptr) {
   // only the header is reset; cpr[] entries are written before being read
   const size_t hdr = offsetof(Ctrl, cpr);
   static thread_local std::vector<char> buf;
@@ -1267,6 +1256,7 @@ int reset_ctrl(gcol_cuda_graph* g, int round_cap, int* in_list, int* out_list, i
     c->hslot_flag = g->d_hslot + 3 * g->hslots;
   }
   c->hslot_bm = g->d_hslot_bm;
+  if (peers) c->peers = *peers;  // this launch pushes its commits to the peers' replicas
   GCOL_CK(cudaMemcpyAsync(g->d_ctrl, buf.data(), hdr, cudaMemcpyHostToDevice, g->stream));
   note_h2d(g, hdr);
   return GCOL_OK;
@@ -2047,8 +2037,6 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
   GCOL_CK(cudaMemsetAsync(g->d_marks, 0, sizeof(int) * n, g->stream));
   if (int rc = reset_ctrl(g, static_cast<int>(opt.round_cap), g->d_listA, g->d_listB, nullptr, 0))
     return rc;
-  // colour-committing launches: under the device launch mutex (PeerScope)
-  std::unique_lock<std::mutex> launch_lk(device_launch_mutex(g->device));
   if (eager) {
     if (int rc = launch_eager(g, rule_of(opt.priority), lower, opt.k1_blocks_per_sm, mm, wide, polls))
       return rc;
@@ -2089,7 +2077,6 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
       if (int rc = reset_split(g, &sp->second, g->k1_warps[exec])) return rc;
     GCOL_CK(cudaGraphLaunch(exec, g->stream));
   }
-  launch_lk.unlock();
   // streamed upload: K1 followed the pieces; what comes next reads anything
   if (g->ev_copied) GCOL_CK(cudaStreamWaitEvent(g->stream, g->ev_copied, 0));
   // the lower-id passes rely on sorted rows: checked once per graph, behind
@@ -2256,7 +2243,6 @@ int gcol_cuda_color_rsoc_csr(const int64_t* offsets, const int32_t* cols, int64_
 
 int gcol_cuda_first_fit_sequential(gcol_cuda_graph* g, int32_t* colors_out, int32_t colors_memory) {
   if (int rc = check_graph(g)) return rc;
-  std::lock_guard<std::mutex> launch_lk(device_launch_mutex(g->device));  // (PeerScope)
   GCOL_CK(cudaSetDevice(g->device));
   if (int rc = ensure_run_buffers(g)) return rc;
   const size_t n = static_cast<size_t>(g->n);
@@ -2364,7 +2350,6 @@ extern "C" {
 int gcol_cuda_color_catalyurek(gcol_cuda_graph* g, const gcol_cuda_options* opt_in,
                                int32_t* colors_out, int32_t colors_memory, gcol_cuda_stats* stats) {
   if (int rc = check_graph(g)) return rc;
-  std::lock_guard<std::mutex> launch_lk(device_launch_mutex(g->device));  // (PeerScope)
   gcol_cuda_options opt;
   if (int rc = read_options(opt_in, &opt)) return rc;
   if (g->n > 0 && !colors_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "colors_out is null");
@@ -2470,7 +2455,6 @@ int gcol_cuda_tentative_snapshot(gcol_cuda_graph* g, const int32_t* colors_in,
                                  const int32_t* worklist, int64_t nwl, int32_t lower_only,
                                  int32_t* colors_out, int32_t memory) {
   if (int rc = check_graph(g)) return rc;
-  std::lock_guard<std::mutex> launch_lk(device_launch_mutex(g->device));  // (PeerScope)
   if (!colors_in || !colors_out) return fail(GCOL_ERR_INVALID_ARGUMENT, "null colour buffer");
   GCOL_CK(cudaSetDevice(g->device));
   if (int rc = ensure_run_buffers(g)) return rc;
@@ -2531,7 +2515,6 @@ void launch_round_rule(gcol_cuda_graph* g, int rule) {
 int run_list_api(gcol_cuda_graph* g, const int32_t* colors, const int32_t* pending,
                  int64_t npending, int32_t priority, bool detect_only, int32_t* out,
                  int64_t* nout, int32_t memory, int32_t* colors_back) {
-  std::lock_guard<std::mutex> launch_lk(device_launch_mutex(g ? g->device : 0));  // (PeerScope)
   if (int rc = check_graph(g)) return rc;
   if (priority == GCOL_PRIORITY_DEFAULT) priority = GCOL_PRIORITY_DEGREE_ID;
   if (priority < GCOL_PRIORITY_ID_LOW || priority > GCOL_PRIORITY_ORDERED)
@@ -2675,33 +2658,6 @@ int gcol_cuda_k1_range(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, int3
 
 namespace {
 
-// Peer pushes on (the handle's partition) for the lifetime of the scope:
-// holds the device launch mutex, drains the device before switching them on
-// (no other handle's kernel can see them), switches them off and drains the
-// handle's stream before releasing it.
-struct PeerScope {
-  gcol_cuda_graph* g;
-  std::unique_lock<std::mutex> lk;
-  bool on_ = false;
-  explicit PeerScope(gcol_cuda_graph* g_) : g(g_), lk(device_launch_mutex(g_->device)) {}
-  int on() {
-    GCOL_CK(cudaDeviceSynchronize());
-    GCOL_CK(cudaMemcpyToSymbolAsync(c_peers, &g->peers, sizeof(PeerSet), 0, cudaMemcpyHostToDevice,
-                                    g->stream));
-    on_ = true;
-    return GCOL_OK;
-  }
-  int off() {
-    if (!on_) return GCOL_OK;
-    static const PeerSet none{};
-    on_ = false;
-    GCOL_CK(cudaMemcpyToSymbolAsync(c_peers, &none, sizeof(PeerSet), 0, cudaMemcpyHostToDevice,
-                                    g->stream));
-    GCOL_CK(cudaStreamSynchronize(g->stream));
-    return GCOL_OK;
-  }
-  ~PeerScope() { off(); }
-};
 
 template <int R>
 void launch_candidates(gcol_cuda_graph* g, const K1Launch& K, const int* colors) {
@@ -2757,11 +2713,9 @@ int gcol_cuda_k1_owned(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, int3
     K.S.cstride = g->part_world;
     K.S.coffset = g->part_rank;
   }
-  if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, nullptr, 0)) return rc;
+  if (int rc = reset_ctrl(g, 1, g->d_listA, g->d_listB, nullptr, 0, &g->peers)) return rc;
   if (!wait)
     if (int rc = reset_split(g, K.plan, K.grid1 * K.cw)) return rc;
-  PeerScope peers(g);
-  if (int rc = peers.on()) return rc;
   GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
   if (n > 0 && wait) {
     void* args[] = {&g->d_off, &g->d_cols, const_cast<int*>(&n), &colors_dev, &g->d_ctrl, &K.L, &K.W};
@@ -2772,7 +2726,6 @@ int gcol_cuda_k1_owned(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, int3
   }
   GCOL_CK(cudaEventRecord(g->ev_k1, g->stream));
   GCOL_CK(cudaGetLastError());
-  if (int rc = peers.off()) return rc;
   g->owned_k1_grid = K.grid1;  // the log's slices, for gcol_cuda_candidates
   g->owned_k1_log = K.L;
   Ctrl hdr;
@@ -2857,10 +2810,10 @@ int gcol_cuda_round_list(gcol_cuda_graph* g, int32_t priority, int32_t* colors_d
     return fail(GCOL_ERR_INVALID_ARGUMENT, "unknown priority rule");
   GCOL_CK(cudaSetDevice(g->device));
   if (int rc = ensure_run_buffers(g)) return rc;
-  if (int rc = reset_ctrl(g, 1, const_cast<int*>(in_dev), out_dev, nullptr, static_cast<int>(nin)))
+  // recolours reach the peers' replicas
+  if (int rc = reset_ctrl(g, 1, const_cast<int*>(in_dev), out_dev, nullptr, static_cast<int>(nin),
+                          &g->peers))
     return rc;
-  PeerScope peers(g);  // recolours reach the peers' replicas
-  if (int rc = peers.on()) return rc;
   if (nin > 0) {
     const int r = rule_of(priority);
     if (r == kIdLow) {
@@ -2875,7 +2828,6 @@ int gcol_cuda_round_list(gcol_cuda_graph* g, int32_t priority, int32_t* colors_d
     }
   }
   GCOL_CK(cudaGetLastError());
-  if (int rc = peers.off()) return rc;
   Ctrl hdr;
   GCOL_CK(cudaMemcpyAsync(&hdr, g->d_ctrl, offsetof(Ctrl, cpr), cudaMemcpyDeviceToHost, g->stream));
   GCOL_CK(cudaStreamSynchronize(g->stream));

@@ -40,6 +40,20 @@ constexpr unsigned kFull = 0xffffffffu;
 //            round over round.
 enum Rule : int { kIdLow = 0, kIdHigh = 1, kDegId = 2, kOrdered = 3 };
 
+// Multi-GPU (SURVEY.md §8(e)): every GPU keeps a full replica of the
+// colours; a partitioned run commits each colour to the local replica and
+// pushes it into every peer's replica (peer-mapped HBM over NVLink), so the
+// other GPUs see it within the round.  The peer set is per launch: it lives
+// in the handle's control block (Ctrl::peers, empty outside partitioned
+// calls) and each kernel copies it into shared memory at entry
+// (init_peers), so concurrent handles -- even several partitioned ones on
+// one device -- never see each other's peers.
+constexpr int kMaxPeers = 7;  // 8 GPUs per node
+struct PeerSet {
+  int* ptr[kMaxPeers];        // peer replicas (this GPU's own excluded)
+  int n;
+};
+
 // Device control block: round state of the on-device round loop (the GPU
 // RoundState of parallel.hpp:115-138).
 struct Ctrl {
@@ -74,6 +88,7 @@ struct Ctrl {
   unsigned* hslot_bm;               // [hslots][kBWinWords] colours seen, 0..16383
   unsigned k1_ctas_done;            // K1W: CTAs finished (the last one may end the run)
   unsigned long long prof[24];      // K1 phase cycle counters (GCOL_K1_PROFILE)
+  PeerSet peers;                    // peer replicas of this launch (n = 0: none)
   unsigned long long cpr[kMaxRoundsRecorded];  // conflicts_per_round
 };
 
@@ -127,17 +142,14 @@ __device__ __forceinline__ void st_color(int* p, int v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
-// Multi-GPU (SURVEY.md §8(e)): every GPU keeps a full replica of the
-// colours; a partitioned run commits each colour to the local replica and
-// pushes it into every peer's replica (peer-mapped HBM over NVLink), so the
-// other GPUs see it within the round.  Empty (n = 0) outside partitioned
-// runs; set per launch by the host (stream-ordered symbol copy).
-constexpr int kMaxPeers = 7;  // 8 GPUs per node
-struct PeerSet {
-  int* ptr[kMaxPeers];        // peer replicas (this GPU's own excluded)
-  int n;
-};
-__constant__ PeerSet c_peers;
+// This CTA's copy of the launch's peer set (namespace-scope shared memory:
+// one instance per CTA of every kernel that uses it).  init_peers must run
+// before any commit_color, followed by a CTA barrier.
+__shared__ PeerSet s_peers;
+
+__device__ __forceinline__ void init_peers(const Ctrl* ctrl) {
+  if (threadIdx.x == 0) s_peers = ctrl->peers;
+}
 
 __device__ __forceinline__ void st_color_sys(int* p, int v) {
   asm volatile("st.relaxed.sys.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
@@ -145,13 +157,13 @@ __device__ __forceinline__ void st_color_sys(int* p, int v) {
 
 __device__ __forceinline__ void commit_color(int* base, int v, int c) {
   st_color(base + v, c);
-  const int np = c_peers.n;
-  for (int q = 0; q < np; ++q) st_color_sys(c_peers.ptr[q] + v, c);
+  const int np = s_peers.n;
+  for (int q = 0; q < np; ++q) st_color_sys(s_peers.ptr[q] + v, c);
 }
 
 // Before a pushing kernel's threads exit: their peer stores are performed.
 __device__ __forceinline__ void peers_fence() {
-  if (c_peers.n) __threadfence_system();
+  if (s_peers.n) __threadfence_system();
 }
 
 // kSnap: snapshot mode reads a frozen, never-written array with plain loads.

@@ -816,6 +816,7 @@ __global__ void __launch_bounds__((CW + k1_producers<CW>()) * 32, 1) k1_pipe(con
     s_mbhead = 0;
     s_next = 0;
   }
+  init_peers(ctrl);
   if (warp < kCW) {
     K1Warp& W = sm.cw[warp];
     W.dv[0][lane] = -1;

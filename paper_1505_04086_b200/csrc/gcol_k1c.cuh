@@ -548,6 +548,7 @@ __global__ void __launch_bounds__(kHvThreads, 1)
     s_read[threadIdx.x] = RW;  // free
   }
   if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  init_peers(ctrl);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int G = gridDim.x;

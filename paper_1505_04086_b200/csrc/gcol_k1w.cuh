@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kWaitBlock, kClass ? kLightMinBlocks : kWaitMi
     s_npairs = 0;
     s_gathers = 0;
   }
+  init_peers(ctrl);
   __syncthreads();
   const int lane = lane_id();
   const int wpb = blockDim.x >> 5;

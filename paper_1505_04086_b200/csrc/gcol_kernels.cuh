@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(kBlock) k_list(const long long* __restrict__ o
                                                  const int* __restrict__ cols, int* colors,
                                                  Ctrl* ctrl, int* heavy, int* marks) {
   __shared__ unsigned s_win[kWarps][32];
+  init_peers(ctrl);
+  __syncthreads();
   const uint64_t pol = policy_evict_first();
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int* in = ctrl->in_list;
@@ -268,6 +270,8 @@ __global__ void __launch_bounds__(kBlock) k_heavy(const long long* __restrict__ 
                                                   Ctrl* ctrl, const int* heavy, int* marks) {
   __shared__ unsigned s_bwin[kBWinWords];
   __shared__ int s_red;
+  init_peers(ctrl);
+  __syncthreads();
   const uint64_t pol = policy_evict_first();
   if (!kDetectOnly && R != kOrdered) {
     const int npc = ctrl->heavy_pieces;

@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(kBlock) k_ordered_round(const long long* __res
   const int n = ctrl->in_len;
   const int* list = ctrl->in_list;
   const int polls_max = ctrl->ord_sorted ? INT_MAX : kOrdWaitPolls;
+  init_peers(ctrl);  // (the loop's first barrier orders it)
   for (;;) {
     if (tid == 0) s_i = (int)atomicAdd(&ctrl->ord_ticket, 1ull);
     for (int k = tid; k < kBWinWords; k += kBlock) s_bm[k] = 0u;

@@ -148,3 +148,73 @@ def test_push_mode_one_rank_k1w_is_serial_ff():
     oracle_mod.build()
     ff = oracle_mod.first_fit_sequential(oracle_mod.CSR(hg.offsets(), hg.adjacency()))
     assert np.array_equal(colors.cpu().numpy(), ff)
+
+
+def emulate_push_concurrent(off, cols, n, P, priority=gcol.Priority.degree_id):
+    """Push mode with P logical ranks running AT THE SAME TIME on one device:
+    one host thread and one stream (handle) per rank, each rank's initial
+    pass on 1/P of the SMs (GCOL_K1_WAIT_BPS), so its pushes, the other
+    ranks' stale remote reads and the cross-rank K1W waits interleave as
+    they would between GPUs.  Rounds run concurrently too; a round ends when
+    every rank's recolours (and pushes) are done."""
+    import threading
+    opt = gcol.ParallelOptions(priority=priority)
+    ops = [gdist.DeviceOps(gcol.Graph.from_device(off, cols), priority=int(priority), opt=opt)
+           for _ in range(P)]
+    reps = [torch.full((n,), -1, dtype=torch.int32, device="cuda") for _ in range(P)]
+    ptrs = [t.data_ptr() for t in reps]
+    for r in range(P):
+        ops[r].partition(r, P, ptrs)
+    torch.cuda.synchronize()
+
+    def all_ranks(fn):
+        out, errs = [None] * P, []
+
+        def run(r):
+            try:
+                out[r] = fn(r)
+            except Exception as e:  # noqa: BLE001
+                errs.append(e)
+        th = [threading.Thread(target=run, args=(r,)) for r in range(P)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=120)
+        assert not any(t.is_alive() for t in th), "a rank hung"
+        assert not errs, errs
+        torch.cuda.synchronize()
+        return out
+
+    all_ranks(lambda r: ops[r].k1_owned(reps[r]))
+    every = torch.cat([ops[r].candidates(reps[r]) for r in range(P)])
+    own = gdist.owner_of(every.long(), P)
+    work = [torch.unique(every[own == r]).to(torch.int32) for r in range(P)]
+    rounds = 0
+    while True:
+        rec = all_ranks(lambda r: ops[r].round_list(reps[r], work[r]))
+        rounds += 1
+        if sum(x.numel() for x in rec) == 0:
+            break
+        work = rec
+        assert rounds < 1000
+    return reps, rounds
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_push_mode_concurrent_ranks(P, monkeypatch):
+    import os
+    occ = 6  # K1W's resident CTAs per SM (kWaitMinBlocks)
+    monkeypatch.setenv("GCOL_K1_WAIT_BPS", str(max(1, occ // P)))
+    off, cols = graphs.erdos_renyi(120_000, 16, 21, "cuda")
+    n = off.numel() - 1
+    reps, rounds = emulate_push_concurrent(off, cols, n, P)
+    for r in range(1, P):
+        assert torch.equal(reps[0], reps[r]), "replicas diverged"
+    hg = gcol.Graph(off.cpu().numpy(), cols.cpu().numpy())
+    c = reps[0].cpu().numpy()
+    from oracle import oracle as oracle_mod
+    oracle_mod.build()
+    o = oracle_mod.CSR(hg.offsets(), hg.adjacency())
+    assert oracle_mod.verify_coloring(o, c) == []
+    assert (c >= 0).all() and (c <= np.diff(hg.offsets())).all()
+    del os
