@@ -107,6 +107,8 @@ struct ClassPlan {
   int T = 0;
   int nh = 0;
   HeavyRow* d_rows = nullptr;
+  HvRank* d_rank = nullptr;  // heavy-rank table (n / 32 words)
+  int* d_hcol = nullptr;     // compact heavy colours (nh)
 };
 
 }  // namespace
@@ -678,7 +680,9 @@ int get_class(gcol_cuda_graph* g, int T, ClassPlan** out) {
     GCOL_CK(cudaStreamSynchronize(g->stream));
     P.nh = nh;
     GCOL_CK(dalloc(&P.d_rows, static_cast<size_t>(nh), g->stream));
-    if (nh > 0) k_class_write<<<nb, kBlock, 0, g->stream>>>(g->d_off, n, T, d_cnt, P.d_rows);
+    GCOL_CK(dalloc(&P.d_rank, static_cast<size_t>((g->n + 31) / 32), g->stream));
+    GCOL_CK(dalloc(&P.d_hcol, static_cast<size_t>(nh), g->stream));
+    if (nh > 0) k_class_write<<<nb, kBlock, 0, g->stream>>>(g->d_off, n, T, d_cnt, P.d_rows, P.d_rank);
     GCOL_CK(cudaGetLastError());
     GCOL_CK(cudaFreeAsync(d_cnt, g->stream));
   }
@@ -727,6 +731,7 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
   K.W = WaitArgs{g->d_ready, g->piece_shift, polls, 1, 0, env_int("GCOL_K1W_SLEEP", 128, 0, 100000),
                  nullptr, 0ull};
   K.W.light_lim = T;
+  K.W.light_coop = env_int("GCOL_K1L_COOP", 1, 0, 1);
   // heavy pass: kHvWarps-warp CTAs, GCOL_K1H_BPS per SM (the in-flight window)
   auto hfn = k1_heavy<PairLog>;
   GCOL_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(hfn),
@@ -759,7 +764,12 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
   C->H = HeavyArgs{P->d_q16, CP->d_rows, CP->nh, env_int("GCOL_K1H_ROWW", rw_default, 1, kHvWarps - 1),
                    env_int("GCOL_K1H_RECHECK", 1, 0, 1), P->d_ctr + 3,
                    std::getenv("GCOL_K1_PROFILE") ? 1 : 0, static_cast<long long>(g->m),
-                   env_int("GCOL_K1H_PIECEW", pw_default, 1, kHvPieceWarps), g->d_ready, g->piece_shift};
+                   env_int("GCOL_K1H_PIECEW", pw_default, 1, kHvPieceWarps), g->d_ready, g->piece_shift,
+                   CP->d_rank, nullptr};
+  // compact heavy colours when the colour array does not fit L2 (GCOL_K1H_COMPACT)
+  // measured and rejected as a default: the rank lookup makes every gather two
+  // dependent loads (R-MAT 27 K1H 37.7 -> 63.9 ms, R-MAT 24 4.4 -> 7.4 ms)
+  if (env_int("GCOL_K1H_COMPACT", 0, 0, 1)) C->H.hcol = CP->d_hcol;
   // log slices: [0, grid_h) heavy CTAs (15/16 of the log: K1H logs its stale
   // reads), then the light CTAs (K1L logs only reads whose wait timed out)
   C->nregions = C->grid_h + K.grid1;
@@ -810,7 +820,7 @@ int add_class_nodes(gcol_cuda_graph* g, cudaGraph_t graph, cudaGraphNode_t dep, 
   ClassPlan* CP = &g->classes[class_threshold()];
   cudaGraphNode_t n_mark, n_h, n_evh, n_l;
   GCOL_CK(add_kernel(&n_mark, graph, &dep, 1, k_mark_pending, dim3(g->sms * 4), dim3(kBlock),
-                     static_cast<const HeavyRow*>(CP->d_rows), CP->nh, g->d_colors));
+                     static_cast<const HeavyRow*>(CP->d_rows), CP->nh, g->d_colors, C.H.hcol));
   {
     const long long* off = g->d_off;
     const int* cols = g->d_cols;
@@ -850,7 +860,7 @@ int add_class_nodes(gcol_cuda_graph* g, cudaGraph_t graph, cudaGraphNode_t dep, 
 // The same two passes launched eagerly on the library stream.
 int launch_class_eager(gcol_cuda_graph* g, ClassLaunch& C) {
   ClassPlan* CP = &g->classes[class_threshold()];
-  k_mark_pending<<<g->sms * 4, kBlock, 0, g->stream>>>(CP->d_rows, CP->nh, g->d_colors);
+  k_mark_pending<<<g->sms * 4, kBlock, 0, g->stream>>>(CP->d_rows, CP->nh, g->d_colors, C.H.hcol);
   GCOL_CK(cudaGetLastError());
   {
     const long long* off = g->d_off;
@@ -1963,7 +1973,9 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
   }
   for (auto& kv : g->splits) free_split(g, kv.second);
   for (auto& kv : g->classes)
-    if (kv.second.d_rows && g->stream) cudaFreeAsync(kv.second.d_rows, g->stream);
+    for (void* p : {static_cast<void*>(kv.second.d_rows), static_cast<void*>(kv.second.d_rank),
+                    static_cast<void*>(kv.second.d_hcol)})
+      if (p && g->stream) cudaFreeAsync(p, g->stream);
   if (g->stream) {
     if (g->owns_csr) {
       cudaFreeAsync(g->d_off, g->stream);

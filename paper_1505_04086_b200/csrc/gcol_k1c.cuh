@@ -61,6 +61,12 @@ __device__ __forceinline__ int hv_ld_color(const int* p) {
   return ld_color(p);
 #endif
 }
+__device__ __forceinline__ unsigned long long ld_nc_u64(const void* p) {
+  unsigned long long r;
+  asm volatile("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(r) : "l"(p));
+  return r;
+}
+
 constexpr int kHvWarps = 8;    // row-warp slots per K1H CTA (row warps + the producer)
 constexpr int kClassTDefault = kSmallMax + 1;  // heavy: degree >= 64
 
@@ -83,6 +89,16 @@ struct alignas(16) HvPiece {
 };
 constexpr int kHvSlotMax = 1 << 22;
 
+// Heavy-rank table: per 32-id word, the heavy ids' bit mask and the number
+// of heavy ids below the word, so rank(w) = base + popc(bits below w).  With
+// it K1H can keep the heavy rows' colours in a compact array indexed by
+// rank (4 x heavy rows bytes: R-MAT 27, 32 MB instead of a 537 MB colour
+// array that misses L2 on nearly every gather).
+struct alignas(8) HvRank {
+  unsigned bits;
+  int base;
+};
+
 struct HeavyArgs {
   HvPiece* q16;       // [npieces] piece records (split rows)
   const HeavyRow* rows;
@@ -96,7 +112,47 @@ struct HeavyArgs {
   int piece_warps;    // active piece warps per CTA (1 .. kHvPieceWarps)
   const unsigned* piece_ready;  // streamed upload: flag per 2^piece_shift adjacency
   int piece_shift;              //   entries resident (null: the whole CSR is resident)
+  const HvRank* rank;           // compact mode (hcol != null): heavy-rank table
+  int* hcol;                    //   heavy rows' colours by rank (-2 pending); colours are
+                                //   committed to both arrays
 };
+
+// K1H colour reads and writes: through the compact heavy array when H.hcol
+// is set (a light neighbour reads as -1: not started, it reads this row
+// later), else the colour array itself.
+__device__ __forceinline__ int hv_rank_of(const HeavyArgs& H, int w, bool& heavy) {
+  const unsigned long long e = ld_nc_u64(H.rank + (w >> 5));
+  const unsigned bits = (unsigned)e;
+  const int bit = w & 31;
+  heavy = (bits >> bit) & 1u;
+  return (int)(e >> 32) + __popc(bits & ((1u << bit) - 1u));
+}
+
+__device__ __forceinline__ int hv_gather(const HeavyArgs& H, const int* colors, int w) {
+  if (!H.hcol) return hv_ld_color(colors + w);
+  bool heavy;
+  const int r = hv_rank_of(H, w, heavy);
+  return heavy ? hv_ld_color(H.hcol + r) : -1;
+}
+
+__device__ __forceinline__ int hv_gather_relaxed(const HeavyArgs& H, const int* colors, int w) {
+  if (!H.hcol) return ld_color(colors + w);
+  bool heavy;
+  const int r = hv_rank_of(H, w, heavy);
+  return heavy ? ld_color(H.hcol + r) : -1;
+}
+
+// Commit heavy row v (heavy index r, -1: look it up) with colour c (one lane).
+__device__ __forceinline__ void hv_commit(const HeavyArgs& H, int* colors, int v, int r, int c) {
+  if (H.hcol) {
+    if (r < 0) {
+      bool heavy;
+      r = hv_rank_of(H, v, heavy);
+    }
+    st_color(H.hcol + r, c);
+  }
+  commit_color(colors, v, c);
+}
 
 // --------------------------------------------------------------------------
 // Heavy-row table (per graph): ordered compaction of {v : deg(v) >= T}.
@@ -147,7 +203,8 @@ __global__ void __launch_bounds__(1024) k_class_scan(int* counts, int nb, int* t
 }
 
 __global__ void __launch_bounds__(kBlock) k_class_write(const long long* __restrict__ off, int n,
-                                                        int T, const int* pre, HeavyRow* rows) {
+                                                        int T, const int* pre, HeavyRow* rows,
+                                                        HvRank* rank) {
   __shared__ int s_w[kWarps];
   __shared__ int s_base;
   if (threadIdx.x == 0) s_base = pre[blockIdx.x];
@@ -169,6 +226,8 @@ __global__ void __launch_bounds__(kBlock) k_class_write(const long long* __restr
     int before = s_base;
     for (int k = 0; k < warp; ++k) before += s_w[k];
     if (h) rows[before + __popc(m & ((1u << lane) - 1u))] = HeavyRow{b, (int)v, d};
+    const long long word = (v0 + j0) / 32 + warp;
+    if (rank && lane == 0 && word * 32 < n) rank[word] = HvRank{m, before};
     __syncthreads();
     if (threadIdx.x == 0) {
       int t = 0;
@@ -178,10 +237,14 @@ __global__ void __launch_bounds__(kBlock) k_class_write(const long long* __restr
   }
 }
 
-__global__ void k_mark_pending(const HeavyRow* __restrict__ rows, int nh, int* colors) {
+// Heavy rows start pending: colors[v] := -2, or in compact mode hcol[*] := -2
+// (a contiguous fill: K1H then reads and writes heavy colours through hcol).
+__global__ void k_mark_pending(const HeavyRow* __restrict__ rows, int nh, int* colors, int* hcol) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nh;
-       i += (long long)gridDim.x * blockDim.x)
-    colors[rows[i].v] = kPending;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (hcol) hcol[i] = kPending;
+    else colors[rows[i].v] = kPending;
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -237,8 +300,8 @@ __device__ __forceinline__ int hv_staged(const HeavyRow& e, long long m, int min
 // (colours 0..1023 OR-ed in by its pieces), commit.  Warp-collective.
 __device__ __noinline__ void hv_finish_row(const long long* __restrict__ off,
                                            const int* __restrict__ cols, int* colors,
-                                           const SplitArgs& S, int slot, int v, unsigned* win,
-                                           uint64_t pol) {
+                                           const SplitArgs& S, const HeavyArgs& H, int slot, int v,
+                                           unsigned* win, uint64_t pol) {
   const int lane = lane_id();
   const unsigned wd = ld_acquire_u32(S.slot_bm + (size_t)slot * 32 + lane);
   const unsigned fr = ~wd;
@@ -254,7 +317,7 @@ __device__ __noinline__ void hv_finish_row(const long long* __restrict__ off,
     for (int wb = 1024; color < 0 && wb <= deg; wb += 1024)
       color = warp_ff_window<false, true>(cols, colors, v, b, deg, wb, win, pol);
   }
-  if (lane == 0) commit_color(colors, v, color);
+  if (lane == 0) hv_commit(H, colors, v, -1, color);
   __syncwarp();
 }
 
@@ -267,8 +330,9 @@ __device__ __noinline__ void hv_finish_row(const long long* __restrict__ off,
 // without waiting for the add.
 __device__ __forceinline__ void hv_push_long(const long long* __restrict__ off,
                                              const int* __restrict__ cols, int* colors,
-                                             const SplitArgs& S, HvPiece* q16, int v, int deg,
+                                             const SplitArgs& S, const HeavyArgs& H, int v, int deg,
                                              long long b, unsigned* win, uint64_t pol) {
+  HvPiece* q16 = H.q16;
   const int lane = lane_id();
   const int np = (deg + kPiece - 1) / kPiece;
   unsigned slot = 0, t = 0;
@@ -296,7 +360,7 @@ __device__ __forceinline__ void hv_push_long(const long long* __restrict__ off,
   }
   // the count may be added after every piece finished (the records can be
   // seen first): then the publisher is the one that brings it to zero
-  if (__shfl_sync(kFull, (int)(before == -np), 0)) hv_finish_row(off, cols, colors, S, (int)slot, v, win, pol);
+  if (__shfl_sync(kFull, (int)(before == -np), 0)) hv_finish_row(off, cols, colors, S, H, (int)slot, v, win, pol);
 }
 
 // Claim the next piece of this CTA's mailbox below `alloc` and read its
@@ -358,7 +422,7 @@ constexpr int kHvPieceBatch = GCOL_K1H_PB;  // colour gathers per lane in flight
 template <class PL>
 __device__ __forceinline__ void hv_piece(const long long* __restrict__ off,
                                          const int* __restrict__ cols, int* colors,
-                                         const SplitArgs& S, const HvPiece& r, int* buf,
+                                         const SplitArgs& S, const HeavyArgs& H, const HvPiece& r, int* buf,
                                          unsigned long long* bar, unsigned& phase, long long m,
                                          unsigned* win, uint64_t pol, const PL& L,
                                          unsigned& gathers, int prof, long long& t_last,
@@ -394,7 +458,7 @@ __device__ __forceinline__ void hv_piece(const long long* __restrict__ off,
       past |= w[u] > v;
     }
 #pragma unroll
-    for (int u = 0; u < B; ++u) c[u] = w[u] < v ? hv_ld_color(colors + w[u]) : -3;
+    for (int u = 0; u < B; ++u) c[u] = w[u] < v ? hv_gather(H, colors, w[u]) : -3;
 #pragma unroll
     for (int u = 0; u < B; ++u) {
       gathers += w[u] < v;
@@ -421,7 +485,7 @@ __device__ __forceinline__ void hv_piece(const long long* __restrict__ off,
   int last = 0;
   if (lane == 0) last = atom_add_acq_rel(S.slot_left + slot, -1) == 1;
   last = __shfl_sync(kFull, last, 0);
-  if (last) hv_finish_row(off, cols, colors, S, slot, v, win, pol);
+  if (last) hv_finish_row(off, cols, colors, S, H, slot, v, win, pol);
   hv_tick(prof, t_last, pp[2]);
 }
 
@@ -431,7 +495,7 @@ __device__ __forceinline__ void hv_piece(const long long* __restrict__ off,
 // nc entries from the row's aligned base (shared memory), the rest global.
 template <class PL>
 __device__ __forceinline__ void hv_row(const int* __restrict__ cols, int* colors,
-                                       const HeavyArgs& H, const HeavyRow& e0, const int* staged,
+                                       const HeavyArgs& H, const HeavyRow& e0, int hr, const int* staged,
                                        int nc, unsigned* win, uint64_t pol, const PL& L,
                                        unsigned& gathers, long long& p_g0, long long& p_gx,
                                        long long& p_rc, long long& n_xb, long long& t_last) {
@@ -455,7 +519,7 @@ __device__ __forceinline__ void hv_row(const int* __restrict__ cols, int* colors
   for (int base = 0;;) {
     int c[kHvU];
 #pragma unroll
-    for (int u = 0; u < kHvU; ++u) c[u] = cb.w[u] < v ? hv_ld_color(colors + cb.w[u]) : -3;
+    for (int u = 0; u < kHvU; ++u) c[u] = cb.w[u] < v ? hv_gather(H, colors, cb.w[u]) : -3;
     bool past = false;
     unsigned stale = 0;
 #pragma unroll
@@ -481,7 +545,7 @@ __device__ __forceinline__ void hv_row(const int* __restrict__ cols, int* colors
     ++n_xb;
   }
   if (__any_sync(kFull, sw >= 0)) {
-    const int c = sw >= 0 ? ld_color(colors + sw) : -3;
+    const int c = sw >= 0 ? hv_gather_relaxed(H, colors, sw) : -3;
     hv_mark(reg, win, c, deg);
     log_pairs(L, c == kPending, sw, v);
     hv_tick(H.prof, t_last, p_rc);
@@ -495,7 +559,7 @@ __device__ __forceinline__ void hv_row(const int* __restrict__ cols, int* colors
   const unsigned nf = __ballot_sync(kFull, word != kFull);
   const int j = __ffs(nf) - 1;
   const unsigned wj = __shfl_sync(kFull, word, j);
-  if (lane == 0) commit_color(colors, v, j * 32 + __ffs(~wj) - 1);
+  if (lane == 0) hv_commit(H, colors, v, hr, j * 32 + __ffs(~wj) - 1);
   __syncwarp();
 }
 
@@ -580,7 +644,7 @@ __global__ void __launch_bounds__(kHvThreads, 1)
       HvPiece pr;
       if (hv_pop16(S, H.q16, &s_mbhead, pc_hint, pr)) {
         hv_tick(H.prof, t_last, pp[3]);
-        hv_piece<PL>(off, cols, colors, S, pr, s_pbuf[pw], &s_pbar[pw], pphase, H.m, win, pol, L,
+        hv_piece<PL>(off, cols, colors, S, H, pr, s_pbuf[pw], &s_pbar[pw], pphase, H.m, win, pol, L,
                      gathers, H.prof, t_last, pp);
         pc_hint = pc_new;
         ++n_pieces;
@@ -661,9 +725,9 @@ __global__ void __launch_bounds__(kHvThreads, 1)
       hv_tick(H.prof, t_last, p_pre);
       if (e0.v >= 0) {
         if (e0.deg >= S.min_deg)
-          hv_push_long(off, cols, colors, S, H.q16, e0.v, e0.deg, e0.b, win, pol);
+          hv_push_long(off, cols, colors, S, H, e0.v, e0.deg, e0.b, win, pol);
         else
-          hv_row<PL>(cols, colors, H, e0, s_pcols[buf][p], hv_staged(e0, H.m, S.min_deg), win, pol,
+          hv_row<PL>(cols, colors, H, e0, (int)r, s_pcols[buf][p], hv_staged(e0, H.m, S.min_deg), win, pol,
                      L, gathers, p_g0, p_gx, p_rc, n_xb, t_last);
       }
       __syncwarp();

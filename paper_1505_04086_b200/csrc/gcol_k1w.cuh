@@ -53,6 +53,7 @@ struct WaitArgs {
   int close_round;              // the last CTA closes round 1 when nothing was logged
   int light_lim;                // class-split light pass: rows of degree >= light_lim are
                                 //   the heavy pass's (already coloured, skipped)
+  int light_coop;               // light pass: long rows scanned warp-cooperatively
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -154,6 +155,85 @@ __device__ __forceinline__ void k1l_scan(const ColsGlobal& src, const int* color
   }
 }
 
+// The light pass's tile scan, warp-cooperative for the long rows: rows of
+// degree <= kLightShort are scanned by their own lane in one step; the
+// tile's longer rows (R-MAT: ~3 per tile, degree up to 63) are scanned by
+// the whole warp over their concatenated entries, 128 per step, the
+// colours OR-ed into per-row masks in shared memory.  A tile then costs
+// about two round trips instead of (its longest row / kW) of them.
+constexpr int kLightShort = 8;
+template <class Mask>
+__device__ __forceinline__ void k1l_scan_coop(const ColsGlobal& src, const int* colors, int v,
+                                              bool valid, long long b, int deg, unsigned& gathers,
+                                              Mask& mask, unsigned long long& pp,
+                                              unsigned long long* smask, unsigned long long* spp) {
+  const int lane = lane_id();
+  mask = 0;
+  pp = 0ull;
+  // short rows: one step, every load in flight at once
+  {
+    const bool sh = valid && deg <= kLightShort;
+    int w[kLightShort], c[kLightShort];
+#pragma unroll
+    for (int j = 0; j < kLightShort; ++j) w[j] = (sh && j < deg) ? src(b + j) : 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < kLightShort; ++j) c[j] = w[j] != 0x7fffffff ? ld_color(colors + w[j]) : -2;
+#pragma unroll
+    for (int j = 0; j < kLightShort; ++j) {
+      gathers += w[j] != 0x7fffffff;
+      if (static_cast<unsigned>(c[j]) <= static_cast<unsigned>(deg)) mask |= bit_of<Mask>(c[j]);
+      if (c[j] == -1 && w[j] < v) pp |= 1ull << j;
+    }
+  }
+  // long rows: warp-cooperative
+  const bool lg = valid && deg > kLightShort;
+  if (!__any_sync(kFull, lg)) return;
+  smask[lane] = 0ull;
+  spp[lane] = 0ull;
+  const int len = lg ? deg : 0;
+  int incl = len;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const int eoff = incl - len;
+  const int E = __shfl_sync(kFull, incl, 31);
+  __syncwarp();
+  constexpr int U = 4;
+  for (int i0 = 0; i0 < E; i0 += 32 * U) {
+    int w[U], r[U], jj[U], vr[U], dr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * 32 + lane;
+      const int rr = row_of(eoff, i);
+      r[u] = rr;
+      const long long br = __shfl_sync(kFull, b, rr);
+      const int er = __shfl_sync(kFull, eoff, rr);
+      vr[u] = __shfl_sync(kFull, v, rr);
+      dr[u] = __shfl_sync(kFull, deg, rr);
+      jj[u] = i - er;
+      w[u] = i < E ? src(br + jj[u]) : 0x7fffffff;
+    }
+    int c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = w[u] != 0x7fffffff ? ld_color(colors + w[u]) : -2;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      gathers += w[u] != 0x7fffffff;
+      if (static_cast<unsigned>(c[u]) <= static_cast<unsigned>(dr[u]))
+        atomicOr(smask + r[u], 1ull << c[u]);
+      if (c[u] == -1 && w[u] < vr[u]) atomicOr(spp + r[u], 1ull << jj[u]);
+    }
+  }
+  __syncwarp();
+  if (lg) {
+    mask = static_cast<Mask>(smask[lane]);
+    pp = spp[lane];
+  }
+  __syncwarp();
+}
+
 // Commit the row if nothing it read was in flight; else re-check the
 // in-flight ones until they are coloured (after max_polls: log the rest for
 // round 1) and commit.  Warp-collective.
@@ -215,6 +295,7 @@ __global__ void __launch_bounds__(kWaitBlock, kClass ? kLightMinBlocks : kWaitMi
     k1_wait(const long long* __restrict__ off, const int* __restrict__ cols, int n, int* colors,
             Ctrl* ctrl, PairLogArgs LA, WaitArgs A) {
   using Mask = typename std::conditional<kM32, unsigned, unsigned long long>::type;
+  __shared__ unsigned long long s_lmask[kWaitBlock / 32][32], s_lpp[kWaitBlock / 32][32];
   __shared__ int s_npairs;
   __shared__ unsigned s_gathers;
   if (threadIdx.x == 0) {
@@ -266,7 +347,10 @@ __global__ void __launch_bounds__(kWaitBlock, kClass ? kLightMinBlocks : kWaitMi
     if (A.trace && lane == 0) t0 = globaltimer_ns();
     Mask mask;
     unsigned long long pp;
-    if (kClass)
+    if (kClass && A.light_coop)
+      k1l_scan_coop<Mask>(src, colors, v, mine, b, deg, gathers, mask, pp,
+                          s_lmask[threadIdx.x >> 5], s_lpp[threadIdx.x >> 5]);
+    else if (kClass)
       k1l_scan<kLightScanW, Mask>(src, colors, v, mine, b, deg, gathers, mask, pp);
     else
       k1w_scan<kWaitScanW, Mask>(src, colors, v, mine, b, deg, gathers, mask, pp);
