@@ -31,6 +31,7 @@
 #include "gcol_kernels.cuh"
 #include "gcol_k1w.cuh"
 #include "gcol_k1c.cuh"
+#include "gcol_k1h2.cuh"
 #include "gcol_round1.cuh"
 
 using namespace gcol::dev;
@@ -700,7 +701,19 @@ struct ClassLaunch {
   HeavyArgs H{};
   const SplitPlan* plan = nullptr;
   int nregions = 0;
+  // the heavy kernel of this launch: k1_heavy2 (decoupled, default) or k1_heavy
+  const void* hfn = nullptr;
+  int hthreads = 0;
+  size_t hsmem = 0;
+  int publishers = 0;  // warps that may publish pieces (SplitArgs::alive starts here)
 };
+
+// GCOL_K1H_V: 2 = k1_heavy2 (gathers decoupled from the commit order, default),
+// 1 = k1_heavy (the first version, kept for A/B).
+int k1h_version() {
+  static const int v = env_int("GCOL_K1H_V", 2, 1, 2);
+  return v;
+}
 
 const void* k1_light_fn(bool m32, bool stream) {
   if (stream)
@@ -732,12 +745,16 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
                  nullptr, 0ull};
   K.W.light_lim = T;
   K.W.light_coop = env_int("GCOL_K1L_COOP", 1, 0, 1);
-  // heavy pass: kHvWarps-warp CTAs, GCOL_K1H_BPS per SM (the in-flight window)
-  auto hfn = k1_heavy<PairLog>;
-  GCOL_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(hfn),
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHvSmem)));
+  // heavy pass: one persistent CTA per SM (GCOL_K1H_BPS for experiments)
+  const bool v2 = k1h_version() == 2;
+  C->hfn = v2 ? reinterpret_cast<const void*>(k1_heavy2<PairLog>)
+              : reinterpret_cast<const void*>(k1_heavy<PairLog>);
+  C->hthreads = v2 ? kH2Threads : kHvThreads;
+  C->hsmem = v2 ? kH2Smem : kHvSmem;
+  GCOL_CK(cudaFuncSetAttribute(C->hfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(C->hsmem)));
   int hocc = 1;
-  GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hocc, hfn, kHvThreads, kHvSmem));
+  GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hocc, C->hfn, C->hthreads, C->hsmem));
   hocc = std::max(1, hocc);
   const int bps = env_int("GCOL_K1H_BPS", 1, 1, hocc);
   const long long chunks = (CP->nh + kHvWarps - 1) / kHvWarps;
@@ -765,7 +782,18 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
                    env_int("GCOL_K1H_RECHECK", 1, 0, 1), P->d_ctr + 3,
                    std::getenv("GCOL_K1_PROFILE") ? 1 : 0, static_cast<long long>(g->m),
                    env_int("GCOL_K1H_PIECEW", pw_default, 1, kHvPieceWarps), g->d_ready, g->piece_shift,
-                   CP->d_rank, nullptr};
+                   CP->d_rank, nullptr, 0, 0, 0, 0};
+  if (v2) {
+    // k1_heavy2: commit warps (the colour-quality knob), build warps (latency
+    // hiding), piece warps; ring = how far the builders may run ahead
+    C->H.commit_warps = env_int("GCOL_K1H_CW", 4, 1, 8);
+    C->H.piece_warps = env_int("GCOL_K1H_PIECEW", 8, 1, kHvPieceWarps);
+    C->H.build_warps = env_int("GCOL_K1H_BW", kH2Warps - C->H.commit_warps - C->H.piece_warps, 1,
+                               kH2Warps - C->H.commit_warps - C->H.piece_warps);
+    C->H.ring = env_int("GCOL_K1H_RING", kH2Ring, 4, kH2Ring);
+    C->H.polls = env_int("GCOL_K1H_POLLS", 0, 0, 1 << 20);
+  }
+  C->publishers = C->grid_h * (v2 ? C->H.commit_warps : C->H.row_warps);
   // compact heavy colours when the colour array does not fit L2 (GCOL_K1H_COMPACT)
   // measured and rejected as a default: the rank lookup makes every gather two
   // dependent loads (R-MAT 27 K1H 37.7 -> 63.9 ms, R-MAT 24 4.4 -> 7.4 ms)
@@ -826,10 +854,10 @@ int add_class_nodes(gcol_cuda_graph* g, cudaGraph_t graph, cudaGraphNode_t dep, 
     const int* cols = g->d_cols;
     void* args[] = {&off, &cols, &g->d_colors, &g->d_ctrl, &C.LH, &C.S, &C.H};
     cudaKernelNodeParams p{};
-    p.func = reinterpret_cast<void*>(k1_heavy<PairLog>);
+    p.func = const_cast<void*>(C.hfn);
     p.gridDim = dim3(C.grid_h);
-    p.blockDim = dim3(kHvThreads);
-    p.sharedMemBytes = static_cast<unsigned>(kHvSmem);
+    p.blockDim = dim3(C.hthreads);
+    p.sharedMemBytes = static_cast<unsigned>(C.hsmem);
     p.kernelParams = args;
     GCOL_CK(cudaGraphAddKernelNode(&n_h, graph, &n_mark, 1, &p));
   }
@@ -866,8 +894,8 @@ int launch_class_eager(gcol_cuda_graph* g, ClassLaunch& C) {
     const long long* off = g->d_off;
     const int* cols = g->d_cols;
     void* args[] = {&off, &cols, &g->d_colors, &g->d_ctrl, &C.LH, &C.S, &C.H};
-    GCOL_CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k1_heavy<PairLog>),
-                                        dim3(C.grid_h), dim3(kHvThreads), args, kHvSmem, g->stream));
+    GCOL_CK(cudaLaunchCooperativeKernel(C.hfn, dim3(C.grid_h), dim3(C.hthreads), args, C.hsmem,
+                                        g->stream));
   }
   GCOL_CK(cudaEventRecord(g->ev_k1h, g->stream));
   const int n = static_cast<int>(g->n);
@@ -1086,7 +1114,7 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
   GCOL_CK(add_kernel(&b_ctl, body, &b_heavy, 1, k_control, dim3(1), dim3(1), g->d_ctrl, handle, 1));
   GCOL_CK(cudaGraphAddEventRecordNode(&n_ev2, graph, &n_while, 1, g->ev_end));
   GCOL_CK(cudaGraphInstantiate(out_exec, graph, 0));
-  g->k1_warps[*out_exec] = cls ? CL.grid_h * CL.H.row_warps : K.grid1 * (K.cw ? K.cw : kWaitBlock / 32);
+  g->k1_warps[*out_exec] = cls ? CL.publishers : K.grid1 * (K.cw ? K.cw : kWaitBlock / 32);
   g->exec_class[*out_exec] = cls ? 1 : 0;
   *out_graph = graph;
   return GCOL_OK;
@@ -1145,7 +1173,7 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
   const bool cls = kLower && k1v == 3;
   if (cls) {
     if (int rc = plan_k1_class(g, &CL, polls)) return rc;
-    if (int rc = reset_split(g, CL.plan, CL.grid_h * CL.H.row_warps)) return rc;
+    if (int rc = reset_split(g, CL.plan, CL.publishers)) return rc;
     GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
     if (int rc = launch_class_eager(g, CL)) return rc;
   } else if (kLower && k1v == 2) {
@@ -2137,7 +2165,22 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
     }
   const int rounds = hdr.round;
   const bool class_run = (exec && g->exec_class[exec]) || (eager && lower && wide == 3);
-  if (std::getenv("GCOL_K1_PROFILE") && class_run) {
+  if (std::getenv("GCOL_K1_PROFILE") && class_run && k1h_version() == 2) {
+    const unsigned long long* P = hdr.prof;
+    const double r = std::max(1.0, static_cast<double>(P[6]));
+    const double pcs = std::max(1.0, static_cast<double>(P[7]));
+    std::fprintf(stderr,
+                 "[k1h2 profile] per row: commit warps wait %.0f + commit %.0f cycles; build warps wait "
+                 "%.0f + build %.0f | pending kept %.3f per row, still pending at the last look %.4f | "
+                 "piece warps: %.0f cycles per piece (pop %.0f, TMA wait %.0f, gathers %.0f, finish "
+                 "%.0f), busy %.1f%% | rows %llu pieces %llu\n",
+                 P[0] / r, P[1] / r, P[2] / r, P[3] / r, P[4] / r, P[8] / r,
+                 (P[9] + P[10] + P[11] + P[12]) / pcs, P[12] / pcs, P[9] / pcs, P[10] / pcs,
+                 P[11] / pcs,
+                 100.0 * (P[9] + P[10] + P[11] + P[12]) /
+                     std::max(1.0, static_cast<double>(P[9] + P[10] + P[11] + P[12] + P[5])),
+                 static_cast<unsigned long long>(P[6]), static_cast<unsigned long long>(P[7]));
+  } else if (std::getenv("GCOL_K1_PROFILE") && class_run) {
     const unsigned long long* P = hdr.prof;
     const double r = std::max(1.0, static_cast<double>(P[6]));
     const double pcs = std::max(1.0, static_cast<double>(P[7]));

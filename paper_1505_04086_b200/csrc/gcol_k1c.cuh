@@ -115,6 +115,8 @@ struct HeavyArgs {
   const HvRank* rank;           // compact mode (hcol != null): heavy-rank table
   int* hcol;                    //   heavy rows' colours by rank (-2 pending); colours are
                                 //   committed to both arrays
+  // k1_heavy2 (gcol_k1h2.cuh): warps per role, ring slots, extra last-look polls
+  int commit_warps, build_warps, ring, polls;
 };
 
 // K1H colour reads and writes: through the compact heavy array when H.hcol
