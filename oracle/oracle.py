@@ -127,6 +127,11 @@ def ref() -> C.CDLL:
                                         C.c_double, C.c_uint64, C.POINTER(C.c_int)]
         L.ref_shuffle_vertices.restype = _vp
         L.ref_shuffle_vertices.argtypes = [_vp, C.c_uint64, _vp]
+        L.ref_parse_text.restype = _vp
+        L.ref_parse_text.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_int64, C.POINTER(C.c_int),
+                                     C.POINTER(C.c_uint64)]
+        L.ref_save_edge_list.restype = C.c_uint64
+        L.ref_save_edge_list.argtypes = [_vp, C.c_char_p, C.c_uint64]
         _ref = L
     return _ref
 
@@ -284,6 +289,24 @@ class RefGraph:
         if st.value != 0:
             raise ValueError(ref().ref_last_error().decode())
         return cls(p)
+
+    @classmethod
+    def parse_text(cls, text: bytes, fmt: str = "edgelist", num_vertices: int = -1):
+        """The reference's load_edge_list / load_matrix_market on `text`.
+        Returns (graph, None) or (None, (kind, line, message))."""
+        st, line = C.c_int(0), C.c_uint64(0)
+        p = ref().ref_parse_text(text, len(text), 2 if fmt == "mm" else 1, num_vertices,
+                                 C.byref(st), C.byref(line))
+        if st.value != 0:
+            kind = {-1: "input", -2: "capacity", -5: "parse", -6: "unsupported_format"}.get(st.value, "other")
+            return None, (kind, int(line.value), ref().ref_last_error().decode())
+        return cls(p), None
+
+    def save_edge_list(self) -> bytes:
+        k = ref().ref_save_edge_list(self.ptr, None, 0)
+        buf = C.create_string_buffer(int(k) + 1)
+        ref().ref_save_edge_list(self.ptr, buf, k)
+        return buf.raw[:k]
 
     @classmethod
     def rmat(cls, scale, edge_factor, a, b, c, d, seed) -> "RefGraph":

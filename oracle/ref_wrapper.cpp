@@ -18,15 +18,19 @@
 //   count_colors           coloring.hpp:181-196
 //   lockstep_color         lockstep.hpp:37-78
 //   generate_rmat / shuffle_vertices  rmat.hpp:82-155
+//   load_edge_list / save_edge_list / load_matrix_market  graph_io.hpp:83-221
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <optional>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "gcol/coloring.hpp"
 #include "gcol/graph.hpp"
+#include "gcol/graph_io.hpp"
 #include "gcol/lockstep.hpp"
 #include "gcol/parallel.hpp"
 #include "gcol/rmat.hpp"
@@ -37,9 +41,11 @@ namespace {
 thread_local std::string g_err;
 
 // Error codes: 0 ok, -1 input_error, -2 capacity_error, -3 logic_error,
-// -4 other exception.
+// -4 other exception, -5 parse_error, -6 unsupported_format_error.
 int code_of(const std::exception& e) {
   g_err = e.what();
+  if (dynamic_cast<const gcol::parse_error*>(&e)) return -5;
+  if (dynamic_cast<const gcol::unsupported_format_error*>(&e)) return -6;
   if (dynamic_cast<const gcol::input_error*>(&e)) return -1;
   if (dynamic_cast<const gcol::capacity_error*>(&e)) return -2;
   if (dynamic_cast<const std::logic_error*>(&e)) return -3;
@@ -101,6 +107,39 @@ void* ref_graph_from_csr(const uint64_t* off, const uint32_t* cols, uint32_t n, 
 }
 
 void ref_graph_free(void* g) { delete static_cast<gcol::Graph*>(g); }
+
+// The reference's text loaders on an in-memory source.  format 1: edge list
+// (num_vertices < 0: from the ids), 2: Matrix Market.  *line = the
+// parse_error's line (0 otherwise).
+void* ref_parse_text(const char* text, uint64_t len, int format, int64_t num_vertices, int* status,
+                     uint64_t* line) {
+  *line = 0;
+  try {
+    std::istringstream in(std::string(text, static_cast<std::size_t>(len)));
+    *status = 0;
+    if (format == 2) return new gcol::Graph(gcol::load_matrix_market(in));
+    std::optional<gcol::vertex_t> n;
+    if (num_vertices >= 0) n = static_cast<gcol::vertex_t>(num_vertices);
+    return new gcol::Graph(gcol::load_edge_list(in, n));
+  } catch (const gcol::parse_error& e) {
+    *line = e.line();
+    *status = code_of(e);
+    return nullptr;
+  } catch (const std::exception& e) {
+    *status = code_of(e);
+    return nullptr;
+  }
+}
+
+// save_edge_list into a caller buffer; returns the text length (call with
+// cap = 0 to size it).
+uint64_t ref_save_edge_list(const void* gp, char* out, uint64_t cap) {
+  std::ostringstream os;
+  gcol::save_edge_list(os, *static_cast<const gcol::Graph*>(gp));
+  const std::string s = os.str();
+  if (out && cap >= s.size()) std::memcpy(out, s.data(), s.size());
+  return s.size();
+}
 
 uint32_t ref_num_vertices(const void* g) { return static_cast<const gcol::Graph*>(g)->num_vertices(); }
 uint64_t ref_num_adjacency(const void* g) { return static_cast<const gcol::Graph*>(g)->adjacency().size(); }

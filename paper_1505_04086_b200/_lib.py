@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgcol_cuda.so")
+# GCOL_CUDA_LIB: another build of the same ABI (A/B tooling); the default is the in-tree library
+LIB_PATH = os.environ.get("GCOL_CUDA_LIB") or os.path.join(HERE, "libgcol_cuda.so")
 
 GCOL_OK = 0
 GCOL_ERR_INVALID_ARGUMENT = 1

@@ -61,8 +61,49 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+IO_LIB = os.path.join(HERE, "libgcol_io.so")
+CLI_BIN = os.path.join(HERE, "gcol_b200")
+
+
+def _newer(target: str, deps) -> bool:
+    return os.path.exists(target) and all(os.path.getmtime(target) > os.path.getmtime(d) for d in deps)
+
+
+def build_io() -> str:
+    """libgcol_io.so: the host-side text loaders behind include/gcol_io.h (g++ only)."""
+    deps = [os.path.join(CSRC, "gcol_io_abi.cpp"), os.path.join(REPO, "include", "gcol_io.hpp"),
+            os.path.join(REPO, "include", "gcol_io.h")]
+    if _newer(IO_LIB, deps):
+        return IO_LIB
+    cmd = ["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-I", os.path.join(REPO, "include"),
+           "-o", IO_LIB, deps[0]]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("building libgcol_io.so failed")
+    return IO_LIB
+
+
+def build_cli() -> str:
+    """gcol_b200: the color / verify / bench front-end over the C ABI."""
+    lib = build()
+    src = os.path.join(REPO, "tools", "gcol_b200_cli.cpp")
+    deps = [src, lib, os.path.join(REPO, "include", "gcol_io.hpp"), os.path.join(REPO, "include", "gcol_cuda.h")]
+    if _newer(CLI_BIN, deps):
+        return CLI_BIN
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(REPO, "include"), src, "-o", CLI_BIN,
+           "-L", HERE, "-lgcol_cuda", "-Wl,-rpath,$ORIGIN"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("building gcol_b200 failed")
+    return CLI_BIN
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_io())
+    print(build_cli())
 
 
 ADAPTER_SRC = os.path.join(REPO, "tests", "cpp", "adapter_check.cpp")

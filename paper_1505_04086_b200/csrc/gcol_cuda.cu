@@ -108,8 +108,6 @@ struct ClassPlan {
   int T = 0;
   int nh = 0;
   HeavyRow* d_rows = nullptr;
-  HvRank* d_rank = nullptr;  // heavy-rank table (n / 32 words)
-  int* d_hcol = nullptr;     // compact heavy colours (nh)
 };
 
 }  // namespace
@@ -681,9 +679,7 @@ int get_class(gcol_cuda_graph* g, int T, ClassPlan** out) {
     GCOL_CK(cudaStreamSynchronize(g->stream));
     P.nh = nh;
     GCOL_CK(dalloc(&P.d_rows, static_cast<size_t>(nh), g->stream));
-    GCOL_CK(dalloc(&P.d_rank, static_cast<size_t>((g->n + 31) / 32), g->stream));
-    GCOL_CK(dalloc(&P.d_hcol, static_cast<size_t>(nh), g->stream));
-    if (nh > 0) k_class_write<<<nb, kBlock, 0, g->stream>>>(g->d_off, n, T, d_cnt, P.d_rows, P.d_rank);
+    if (nh > 0) k_class_write<<<nb, kBlock, 0, g->stream>>>(g->d_off, n, T, d_cnt, P.d_rows);
     GCOL_CK(cudaGetLastError());
     GCOL_CK(cudaFreeAsync(d_cnt, g->stream));
   }
@@ -701,17 +697,19 @@ struct ClassLaunch {
   HeavyArgs H{};
   const SplitPlan* plan = nullptr;
   int nregions = 0;
-  // the heavy kernel of this launch: k1_heavy2 (decoupled, default) or k1_heavy
+  // the heavy kernel of this launch: k1_heavy (default) or k1_heavy2 (GCOL_K1H_V=2)
   const void* hfn = nullptr;
   int hthreads = 0;
   size_t hsmem = 0;
   int publishers = 0;  // warps that may publish pieces (SplitArgs::alive starts here)
 };
 
-// GCOL_K1H_V: 2 = k1_heavy2 (gathers decoupled from the commit order, default),
-// 1 = k1_heavy (the first version, kept for A/B).
+// GCOL_K1H_V: 1 = k1_heavy (default), 2 = k1_heavy2 (gathers decoupled from
+// the commit order; measured on B200: R-MAT 24 heavy pass 5.9 -> 3.7 ms but
+// 662-667 colours, outside the 1.05 gate of 612 -- the builders' lead is a
+// second in-flight window -- so it stays an experiment).
 int k1h_version() {
-  static const int v = env_int("GCOL_K1H_V", 2, 1, 2);
+  static const int v = env_int("GCOL_K1H_V", 1, 1, 2);
   return v;
 }
 
@@ -782,7 +780,7 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
                    env_int("GCOL_K1H_RECHECK", 1, 0, 1), P->d_ctr + 3,
                    std::getenv("GCOL_K1_PROFILE") ? 1 : 0, static_cast<long long>(g->m),
                    env_int("GCOL_K1H_PIECEW", pw_default, 1, kHvPieceWarps), g->d_ready, g->piece_shift,
-                   CP->d_rank, nullptr, 0, 0, 0, 0};
+                   0, 0, 0, 0};
   if (v2) {
     // k1_heavy2: commit warps (the colour-quality knob), build warps (latency
     // hiding), piece warps; ring = how far the builders may run ahead
@@ -794,10 +792,6 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
     C->H.polls = env_int("GCOL_K1H_POLLS", 0, 0, 1 << 20);
   }
   C->publishers = C->grid_h * (v2 ? C->H.commit_warps : C->H.row_warps);
-  // compact heavy colours when the colour array does not fit L2 (GCOL_K1H_COMPACT)
-  // measured and rejected as a default: the rank lookup makes every gather two
-  // dependent loads (R-MAT 27 K1H 37.7 -> 63.9 ms, R-MAT 24 4.4 -> 7.4 ms)
-  if (env_int("GCOL_K1H_COMPACT", 0, 0, 1)) C->H.hcol = CP->d_hcol;
   // log slices: [0, grid_h) heavy CTAs (15/16 of the log: K1H logs its stale
   // reads), then the light CTAs (K1L logs only reads whose wait timed out)
   C->nregions = C->grid_h + K.grid1;
@@ -848,7 +842,7 @@ int add_class_nodes(gcol_cuda_graph* g, cudaGraph_t graph, cudaGraphNode_t dep, 
   ClassPlan* CP = &g->classes[class_threshold()];
   cudaGraphNode_t n_mark, n_h, n_evh, n_l;
   GCOL_CK(add_kernel(&n_mark, graph, &dep, 1, k_mark_pending, dim3(g->sms * 4), dim3(kBlock),
-                     static_cast<const HeavyRow*>(CP->d_rows), CP->nh, g->d_colors, C.H.hcol));
+                     static_cast<const HeavyRow*>(CP->d_rows), CP->nh, g->d_colors));
   {
     const long long* off = g->d_off;
     const int* cols = g->d_cols;
@@ -888,7 +882,7 @@ int add_class_nodes(gcol_cuda_graph* g, cudaGraph_t graph, cudaGraphNode_t dep, 
 // The same two passes launched eagerly on the library stream.
 int launch_class_eager(gcol_cuda_graph* g, ClassLaunch& C) {
   ClassPlan* CP = &g->classes[class_threshold()];
-  k_mark_pending<<<g->sms * 4, kBlock, 0, g->stream>>>(CP->d_rows, CP->nh, g->d_colors, C.H.hcol);
+  k_mark_pending<<<g->sms * 4, kBlock, 0, g->stream>>>(CP->d_rows, CP->nh, g->d_colors);
   GCOL_CK(cudaGetLastError());
   {
     const long long* off = g->d_off;
@@ -2001,8 +1995,7 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
   }
   for (auto& kv : g->splits) free_split(g, kv.second);
   for (auto& kv : g->classes)
-    for (void* p : {static_cast<void*>(kv.second.d_rows), static_cast<void*>(kv.second.d_rank),
-                    static_cast<void*>(kv.second.d_hcol)})
+    for (void* p : {static_cast<void*>(kv.second.d_rows)})
       if (p && g->stream) cudaFreeAsync(p, g->stream);
   if (g->stream) {
     if (g->owns_csr) {

@@ -61,12 +61,6 @@ __device__ __forceinline__ int hv_ld_color(const int* p) {
   return ld_color(p);
 #endif
 }
-__device__ __forceinline__ unsigned long long ld_nc_u64(const void* p) {
-  unsigned long long r;
-  asm volatile("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(r) : "l"(p));
-  return r;
-}
-
 constexpr int kHvWarps = 8;    // row-warp slots per K1H CTA (row warps + the producer)
 constexpr int kClassTDefault = kSmallMax + 1;  // heavy: degree >= 64
 
@@ -89,16 +83,6 @@ struct alignas(16) HvPiece {
 };
 constexpr int kHvSlotMax = 1 << 22;
 
-// Heavy-rank table: per 32-id word, the heavy ids' bit mask and the number
-// of heavy ids below the word, so rank(w) = base + popc(bits below w).  With
-// it K1H can keep the heavy rows' colours in a compact array indexed by
-// rank (4 x heavy rows bytes: R-MAT 27, 32 MB instead of a 537 MB colour
-// array that misses L2 on nearly every gather).
-struct alignas(8) HvRank {
-  unsigned bits;
-  int base;
-};
-
 struct HeavyArgs {
   HvPiece* q16;       // [npieces] piece records (split rows)
   const HeavyRow* rows;
@@ -112,47 +96,22 @@ struct HeavyArgs {
   int piece_warps;    // active piece warps per CTA (1 .. kHvPieceWarps)
   const unsigned* piece_ready;  // streamed upload: flag per 2^piece_shift adjacency
   int piece_shift;              //   entries resident (null: the whole CSR is resident)
-  const HvRank* rank;           // compact mode (hcol != null): heavy-rank table
-  int* hcol;                    //   heavy rows' colours by rank (-2 pending); colours are
-                                //   committed to both arrays
   // k1_heavy2 (gcol_k1h2.cuh): warps per role, ring slots, extra last-look polls
   int commit_warps, build_warps, ring, polls;
 };
 
-// K1H colour reads and writes: through the compact heavy array when H.hcol
-// is set (a light neighbour reads as -1: not started, it reads this row
-// later), else the colour array itself.
-__device__ __forceinline__ int hv_rank_of(const HeavyArgs& H, int w, bool& heavy) {
-  const unsigned long long e = ld_nc_u64(H.rank + (w >> 5));
-  const unsigned bits = (unsigned)e;
-  const int bit = w & 31;
-  heavy = (bits >> bit) & 1u;
-  return (int)(e >> 32) + __popc(bits & ((1u << bit) - 1u));
+// K1H colour reads and writes.  (A compact heavy-colour array indexed through
+// a rank table was measured and removed: two dependent loads per gather lost
+// on both R-MAT configs, and even switched off its branch in these helpers
+// kept the compiler from batching the gathers -- R-MAT 24 K1H 4.4 -> 5.9 ms.)
+__device__ __forceinline__ int hv_gather(const HeavyArgs&, const int* colors, int w) {
+  return hv_ld_color(colors + w);
 }
-
-__device__ __forceinline__ int hv_gather(const HeavyArgs& H, const int* colors, int w) {
-  if (!H.hcol) return hv_ld_color(colors + w);
-  bool heavy;
-  const int r = hv_rank_of(H, w, heavy);
-  return heavy ? hv_ld_color(H.hcol + r) : -1;
+__device__ __forceinline__ int hv_gather_relaxed(const HeavyArgs&, const int* colors, int w) {
+  return ld_color(colors + w);
 }
-
-__device__ __forceinline__ int hv_gather_relaxed(const HeavyArgs& H, const int* colors, int w) {
-  if (!H.hcol) return ld_color(colors + w);
-  bool heavy;
-  const int r = hv_rank_of(H, w, heavy);
-  return heavy ? ld_color(H.hcol + r) : -1;
-}
-
-// Commit heavy row v (heavy index r, -1: look it up) with colour c (one lane).
-__device__ __forceinline__ void hv_commit(const HeavyArgs& H, int* colors, int v, int r, int c) {
-  if (H.hcol) {
-    if (r < 0) {
-      bool heavy;
-      r = hv_rank_of(H, v, heavy);
-    }
-    st_color(H.hcol + r, c);
-  }
+// Commit heavy row v with colour c (one lane).
+__device__ __forceinline__ void hv_commit(const HeavyArgs&, int* colors, int v, int, int c) {
   commit_color(colors, v, c);
 }
 
@@ -205,8 +164,7 @@ __global__ void __launch_bounds__(1024) k_class_scan(int* counts, int nb, int* t
 }
 
 __global__ void __launch_bounds__(kBlock) k_class_write(const long long* __restrict__ off, int n,
-                                                        int T, const int* pre, HeavyRow* rows,
-                                                        HvRank* rank) {
+                                                        int T, const int* pre, HeavyRow* rows) {
   __shared__ int s_w[kWarps];
   __shared__ int s_base;
   if (threadIdx.x == 0) s_base = pre[blockIdx.x];
@@ -228,8 +186,6 @@ __global__ void __launch_bounds__(kBlock) k_class_write(const long long* __restr
     int before = s_base;
     for (int k = 0; k < warp; ++k) before += s_w[k];
     if (h) rows[before + __popc(m & ((1u << lane) - 1u))] = HeavyRow{b, (int)v, d};
-    const long long word = (v0 + j0) / 32 + warp;
-    if (rank && lane == 0 && word * 32 < n) rank[word] = HvRank{m, before};
     __syncthreads();
     if (threadIdx.x == 0) {
       int t = 0;
@@ -239,14 +195,11 @@ __global__ void __launch_bounds__(kBlock) k_class_write(const long long* __restr
   }
 }
 
-// Heavy rows start pending: colors[v] := -2, or in compact mode hcol[*] := -2
-// (a contiguous fill: K1H then reads and writes heavy colours through hcol).
-__global__ void k_mark_pending(const HeavyRow* __restrict__ rows, int nh, int* colors, int* hcol) {
+// Heavy rows start pending: colors[v] := -2.
+__global__ void k_mark_pending(const HeavyRow* __restrict__ rows, int nh, int* colors) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nh;
-       i += (long long)gridDim.x * blockDim.x) {
-    if (hcol) hcol[i] = kPending;
-    else colors[rows[i].v] = kPending;
-  }
+       i += (long long)gridDim.x * blockDim.x)
+    colors[rows[i].v] = kPending;
 }
 
 // --------------------------------------------------------------------------

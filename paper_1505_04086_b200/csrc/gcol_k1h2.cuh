@@ -1,6 +1,6 @@
 // gcol_k1h2.cuh -- K1H with the gathers decoupled from the commit order
-// (the default heavy pass of the class split; gcol_k1c.cuh holds the first
-// version, k1_heavy, and everything the two share).
+// (an experiment, GCOL_K1H_V=2; gcol_k1c.cuh holds the default heavy pass,
+// k1_heavy, and everything the two share).
 //
 // Same contract as k1_heavy: heavy rows (degree >= T) in ascending id order,
 // each First-Fit over its LOWER heavy neighbours, a lower neighbour still
