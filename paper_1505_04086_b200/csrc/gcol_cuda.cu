@@ -32,6 +32,7 @@
 #include "gcol_k1w.cuh"
 #include "gcol_k1c.cuh"
 #include "gcol_k1h2.cuh"
+#include "gcol_k1hw.cuh"
 #include "gcol_round1.cuh"
 
 using namespace gcol::dev;
@@ -707,9 +708,11 @@ struct ClassLaunch {
 // GCOL_K1H_V: 1 = k1_heavy (default), 2 = k1_heavy2 (gathers decoupled from
 // the commit order; measured on B200: R-MAT 24 heavy pass 5.9 -> 3.7 ms but
 // 662-667 colours, outside the 1.05 gate of 612 -- the builders' lead is a
-// second in-flight window -- so it stays an experiment).
+// second in-flight window -- so it stays an experiment); 3 = k1_heavy_wait
+// (gcol_k1hw.cuh: heavy rows wait for their pending lower neighbours, exact
+// First-Fit on the heavy subgraph, no cap on the rows in flight).
 int k1h_version() {
-  static const int v = env_int("GCOL_K1H_V", 1, 1, 2);
+  static const int v = env_int("GCOL_K1H_V", 1, 1, 3);
   return v;
 }
 
@@ -744,11 +747,12 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
   K.W.light_lim = T;
   K.W.light_coop = env_int("GCOL_K1L_COOP", 1, 0, 1);
   // heavy pass: one persistent CTA per SM (GCOL_K1H_BPS for experiments)
-  const bool v2 = k1h_version() == 2;
-  C->hfn = v2 ? reinterpret_cast<const void*>(k1_heavy2<PairLog>)
-              : reinterpret_cast<const void*>(k1_heavy<PairLog>);
-  C->hthreads = v2 ? kH2Threads : kHvThreads;
-  C->hsmem = v2 ? kH2Smem : kHvSmem;
+  const bool v2 = k1h_version() == 2, v3 = k1h_version() == 3;
+  C->hfn = v3   ? reinterpret_cast<const void*>(k1_heavy_wait<PairLog>)
+           : v2 ? reinterpret_cast<const void*>(k1_heavy2<PairLog>)
+                : reinterpret_cast<const void*>(k1_heavy<PairLog>);
+  C->hthreads = v3 ? kHwThreads : v2 ? kH2Threads : kHvThreads;
+  C->hsmem = v3 ? kHwSmem : v2 ? kH2Smem : kHvSmem;
   GCOL_CK(cudaFuncSetAttribute(C->hfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(C->hsmem)));
   int hocc = 1;
@@ -790,6 +794,14 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
                                kH2Warps - C->H.commit_warps - C->H.piece_warps);
     C->H.ring = env_int("GCOL_K1H_RING", kH2Ring, 4, kH2Ring);
     C->H.polls = env_int("GCOL_K1H_POLLS", 0, 0, 1 << 20);
+  }
+  if (v3) {
+    // k1_heavy_wait: row warps fill the SM (the window no longer touches the
+    // colour count), piece warps serve the split rows; polls = the guard
+    C->H.piece_warps = env_int("GCOL_K1H_PIECEW", 8, 1, kHvPieceWarps);
+    C->H.row_warps = env_int("GCOL_K1H_ROWW", kHwWarps - C->H.piece_warps, 1, kHwWarps - C->H.piece_warps);
+    C->H.polls = env_int("GCOL_K1H_POLLS", 1 << 20, 0, 1 << 30);
+    C->H.slot_pend = P->d_q_seq;
   }
   C->publishers = C->grid_h * (v2 ? C->H.commit_warps : C->H.row_warps);
   // log slices: [0, grid_h) heavy CTAs (15/16 of the log: K1H logs its stale
@@ -2158,7 +2170,22 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
     }
   const int rounds = hdr.round;
   const bool class_run = (exec && g->exec_class[exec]) || (eager && lower && wide == 3);
-  if (std::getenv("GCOL_K1_PROFILE") && class_run && k1h_version() == 2) {
+  if (std::getenv("GCOL_K1_PROFILE") && class_run && k1h_version() == 3) {
+    const unsigned long long* P = hdr.prof;
+    const double r = std::max(1.0, static_cast<double>(P[6]));
+    const double pcs = std::max(1.0, static_cast<double>(P[7]));
+    std::fprintf(stderr,
+                 "[k1hw profile] row warps, cycles per row: claim %.0f, first scan %.0f, waiting for "
+                 "pending neighbours %.0f, waiting for own pieces %.0f | %.3f of the rows waited, %.2f "
+                 "polls per row | piece warps: %.0f cycles per piece (pop %.0f, TMA wait %.0f, gathers "
+                 "%.0f, finish %.0f), busy %.1f%% | rows %llu pieces %llu\n",
+                 P[0] / r, P[1] / r, P[2] / r, P[3] / r, P[8] / r, P[4] / r,
+                 (P[9] + P[10] + P[11] + P[12]) / pcs, P[12] / pcs, P[9] / pcs, P[10] / pcs,
+                 P[11] / pcs,
+                 100.0 * (P[9] + P[10] + P[11] + P[12]) /
+                     std::max(1.0, static_cast<double>(P[9] + P[10] + P[11] + P[12] + P[5])),
+                 static_cast<unsigned long long>(P[6]), static_cast<unsigned long long>(P[7]));
+  } else if (std::getenv("GCOL_K1_PROFILE") && class_run && k1h_version() == 2) {
     const unsigned long long* P = hdr.prof;
     const double r = std::max(1.0, static_cast<double>(P[6]));
     const double pcs = std::max(1.0, static_cast<double>(P[7]));

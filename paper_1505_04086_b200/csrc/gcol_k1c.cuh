@@ -98,6 +98,9 @@ struct HeavyArgs {
   int piece_shift;              //   entries resident (null: the whole CSR is resident)
   // k1_heavy2 (gcol_k1h2.cuh): warps per role, ring slots, extra last-look polls
   int commit_warps, build_warps, ring, polls;
+  // k1_heavy_wait (gcol_k1hw.cuh): per split-row slot, INT_MAX - the position of the
+  // first entry a piece read as pending (0: none); zeroed before every run
+  unsigned* slot_pend;
 };
 
 // K1H colour reads and writes.  (A compact heavy-colour array indexed through
