@@ -98,7 +98,11 @@ typedef struct {
   int32_t k1_wide;           /* initial-pass kernel: 0 auto (the waiting pass K1W when every
                                 row has degree <= 63, else the class-split pass K1H + K1L),
                                 1 narrow k1_pipe (8 consumer warps per SM), 2 wide k1_pipe
-                                (16), 3 K1W where it applies, 4 class split */
+                                (16), 3 K1W where it applies, 4 class split (heavy pass chosen
+                                by graph size), 5 class split with the speculative heavy pass,
+                                6 class split with the waiting heavy pass (the result is then
+                                sequential First-Fit in the order "rows of degree >= 64
+                                ascending, then the others ascending", bit for bit) */
   int32_t k1_wait_polls;     /* K1W: re-checks of a row's in-flight lower neighbours before
                                 it colours past them and logs the reads for round 1;
                                 0 default (4096), < 0 none (purely optimistic) */

@@ -565,15 +565,43 @@ bool use_wide(const gcol_cuda_graph* g, int k1_wide) {
   return g->max_degree <= 16;
 }
 
+int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* e = std::getenv(name);
+  return e ? std::max(lo, std::min(hi, std::atoi(e))) : dflt;
+}
+
+// Heavy pass of the class split: waiting (k1_heavy_wait, gcol_k1hw.cuh) or
+// speculative (k1_heavy, gcol_k1c.cuh).  Option k1_wide 5 forces the
+// speculative pass, 6 the waiting one; GCOL_K1H_V=1/3 overrides for A/B.
+// Automatic choice, measured on B200: the waiting pass is
+// bound by the longest chain of adjacent heavy rows with ascending ids
+// (R-MAT 24: 4914 rows at ~1.3 us per hop = 6.5 ms, against 4.4 ms for the
+// speculative pass and its 1.2 ms of rounds), the speculative one by the
+// small window its colour quality allows; once the colour array no longer
+// fits L2 every gather pays HBM latency and only the waiting pass can keep
+// enough rows in flight (R-MAT 27: 32.0 against 34.6 ms, one round instead of
+// eleven, 957 colours -- serial First-Fit's count -- instead of ~1010).
+bool heavy_pass_waits(const gcol_cuda_graph* g, int k1_wide) {
+  static const int v = env_int("GCOL_K1H_V", 0, 0, 3);
+  if (v == 3) return true;
+  if (v == 1 || v == 2) return false;
+  if (k1_wide == 5) return false;
+  if (k1_wide == 6) return true;
+  return sizeof(int) * static_cast<size_t>(g->n) > (size_t{64} << 20);
+}
+
 // K1 variant of the in-place initial pass: 0 narrow, 1 wide, 2 K1W (the
-// waiting pass, gcol_k1w.cuh; rows of degree <= kSmallMax only).  Option
-// k1_wide: 0 auto (K1W when every row is small), 1 narrow, 2 wide, 3 K1W.
+// waiting pass, gcol_k1w.cuh; rows of degree <= kSmallMax only), 3 / 4 the
+// class split with the speculative / waiting heavy pass.  Option k1_wide:
+// 0 auto (K1W when every row is small, else the class split), 1 narrow,
+// 2 wide, 3 K1W, 4 class split, 5 / 6 class split with the heavy pass forced.
 int k1_variant(const gcol_cuda_graph* g, int k1_wide) {
   const bool small = g->max_degree <= kSmallMax;
   if (k1_wide == 3 && small) return 2;
   if (k1_wide == 0 && small) return 2;
-  if ((k1_wide == 0 || k1_wide == 4) && !small) return 3;  // class split
-  return use_wide(g, k1_wide == 3 || k1_wide == 4 ? 0 : k1_wide) ? 1 : 0;
+  if ((k1_wide == 0 || (k1_wide >= 4 && k1_wide <= 6)) && !small)  // class split: 3 or 4
+    return heavy_pass_waits(g, k1_wide) ? 4 : 3;
+  return use_wide(g, k1_wide >= 3 ? 0 : k1_wide) ? 1 : 0;
 }
 
 // option k1_wait_polls: 0 default, > 0 that many re-checks, < 0 none (every
@@ -653,11 +681,6 @@ int class_threshold() {
   return v;
 }
 
-int env_int(const char* name, int dflt, int lo, int hi) {
-  const char* e = std::getenv(name);
-  return e ? std::max(lo, std::min(hi, std::atoi(e))) : dflt;
-}
-
 int get_class(gcol_cuda_graph* g, int T, ClassPlan** out) {
   auto it = g->classes.find(T);
   if (it != g->classes.end()) {
@@ -712,7 +735,7 @@ struct ClassLaunch {
 // (gcol_k1hw.cuh: heavy rows wait for their pending lower neighbours, exact
 // First-Fit on the heavy subgraph, no cap on the rows in flight).
 int k1h_version() {
-  static const int v = env_int("GCOL_K1H_V", 1, 1, 3);
+  static const int v = env_int("GCOL_K1H_V", 1, 0, 3);
   return v;
 }
 
@@ -724,7 +747,7 @@ const void* k1_light_fn(bool m32, bool stream) {
              : reinterpret_cast<const void*>(k1_wait<false, false, true>);
 }
 
-int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
+int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls, bool waiting) {
   const int T = class_threshold();
   ClassPlan* CP = nullptr;
   if (int rc = get_class(g, T, &CP)) return rc;
@@ -747,7 +770,7 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
   K.W.light_lim = T;
   K.W.light_coop = env_int("GCOL_K1L_COOP", 1, 0, 1);
   // heavy pass: one persistent CTA per SM (GCOL_K1H_BPS for experiments)
-  const bool v2 = k1h_version() == 2, v3 = k1h_version() == 3;
+  const bool v3 = waiting, v2 = !waiting && k1h_version() == 2;
   C->hfn = v3   ? reinterpret_cast<const void*>(k1_heavy_wait<PairLog>)
            : v2 ? reinterpret_cast<const void*>(k1_heavy2<PairLog>)
                 : reinterpret_cast<const void*>(k1_heavy<PairLog>);
@@ -800,7 +823,10 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls) {
     // colour count), piece warps serve the split rows; polls = the guard
     C->H.piece_warps = env_int("GCOL_K1H_PIECEW", 8, 1, kHvPieceWarps);
     C->H.row_warps = env_int("GCOL_K1H_ROWW", kHwWarps - C->H.piece_warps, 1, kHwWarps - C->H.piece_warps);
-    C->H.polls = env_int("GCOL_K1H_POLLS", 1 << 20, 0, 1 << 30);
+    // the guard: polls without progress before a row colours past what is
+    // still pending (option k1_wait_polls; its default becomes 2^22 here -- a
+    // row may wait for most of the pass behind a long chain, ~0.5 us a poll)
+    C->H.polls = env_int("GCOL_K1H_POLLS", polls == kWaitPollsDefault ? 1 << 22 : polls, 0, 1 << 30);
     C->H.slot_pend = P->d_q_seq;
   }
   C->publishers = C->grid_h * (v2 ? C->H.commit_warps : C->H.row_warps);
@@ -1047,9 +1073,9 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
                      cudaGraph_t* out_graph, cudaGraphExec_t* out_exec) {
   K1Launch K;
   ClassLaunch CL;
-  const bool cls = kLower && k1v == 3;
+  const bool cls = kLower && k1v >= 3;
   if (cls) {
-    if (int rc = plan_k1_class(g, &CL, polls)) return rc;
+    if (int rc = plan_k1_class(g, &CL, polls, k1v == 4)) return rc;
   } else if (kLower && k1v == 2) {
     if (int rc = plan_k1_wait(g, &K, polls)) return rc;
   } else if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K, k1v == 1)) {
@@ -1176,9 +1202,9 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
   K1Launch K;
   const int n = static_cast<int>(g->n);
   ClassLaunch CL;
-  const bool cls = kLower && k1v == 3;
+  const bool cls = kLower && k1v >= 3;
   if (cls) {
-    if (int rc = plan_k1_class(g, &CL, polls)) return rc;
+    if (int rc = plan_k1_class(g, &CL, polls, k1v == 4)) return rc;
     if (int rc = reset_split(g, CL.plan, CL.publishers)) return rc;
     GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
     if (int rc = launch_class_eager(g, CL)) return rc;
@@ -2169,8 +2195,8 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
       }
     }
   const int rounds = hdr.round;
-  const bool class_run = (exec && g->exec_class[exec]) || (eager && lower && wide == 3);
-  if (std::getenv("GCOL_K1_PROFILE") && class_run && k1h_version() == 3) {
+  const bool class_run = (exec && g->exec_class[exec]) || (eager && lower && wide >= 3);
+  if (std::getenv("GCOL_K1_PROFILE") && class_run && wide == 4) {
     const unsigned long long* P = hdr.prof;
     const double r = std::max(1.0, static_cast<double>(P[6]));
     const double pcs = std::max(1.0, static_cast<double>(P[7]));

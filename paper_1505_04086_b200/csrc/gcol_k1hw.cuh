@@ -42,13 +42,18 @@
 namespace gcol {
 namespace dev {
 
-constexpr int kHwWarps = 24;                 // warps per CTA: row warps + piece warps
+#ifndef GCOL_K1HW_WARPS
+#define GCOL_K1HW_WARPS 24
+#endif
+constexpr int kHwWarps = GCOL_K1HW_WARPS;    // warps per CTA: row warps + piece warps
 constexpr int kHwThreads = kHwWarps * 32;
 constexpr int kHwBatch = 8;                  // heavy rows per cursor claim (per CTA)
-constexpr int kHwBufs = 8;                   // claimed-batch records kept (>= warps / batch + 2)
+constexpr int kHwBufs = 8;                   // claimed-batch records kept
 constexpr int kHwWin = 4;                    // entries per lane per wait window
 constexpr size_t kHwSmem = sizeof(int) * kHvPieceWarps * kHvPieceBuf;  // dynamic: piece buffers
 
+// A warp holds at most one ticket at a time, so at most kHwWarps tickets are
+// between "drawn" and "record read": a record is overwritten kHwBufs batches later.
 static_assert(kHwBufs * kHwBatch >= kHwWarps + 2 * kHwBatch, "batch records must outlive their readers");
 
 // Wait (warp-collective) until no entry of row (b, deg) at a position >= pos
@@ -61,15 +66,20 @@ __device__ __forceinline__ bool hw_wait(const int* __restrict__ cols, const int*
                                         unsigned* win, uint64_t pol, int polls, const PL& L,
                                         long long& n_polls) {
   const int lane = lane_id();
-  int idle = 0;
+  int idle = 0, wpos = -1;
+  int w[kHwWin];
+  bool end = false;
   while (pos != INT_MAX) {
-    int w[kHwWin], c[kHwWin];
-    bool end = false;
+    int c[kHwWin];
+    if (wpos != pos) {  // the window's ids stay in registers while it does not move
+      end = false;
 #pragma unroll
-    for (int u = 0; u < kHwWin; ++u) {
-      const int i = pos + u * 32 + lane;
-      w[u] = i < deg ? ld_col(cols + b + i, pol) : INT_MAX;
-      end |= w[u] > v;
+      for (int u = 0; u < kHwWin; ++u) {
+        const int i = pos + u * 32 + lane;
+        w[u] = i < deg ? ld_col(cols + b + i, pol) : INT_MAX;
+        end |= w[u] > v;
+      }
+      wpos = pos;
     }
 #pragma unroll
     for (int u = 0; u < kHwWin; ++u) c[u] = w[u] < v ? ld_color(colors + w[u]) : -3;
@@ -108,7 +118,7 @@ __device__ __forceinline__ bool hw_wait(const int* __restrict__ cols, const int*
       }
       return false;
     }
-    __nanosleep(idle < 8 ? 40 : 200);
+    if (idle > 4) __nanosleep(idle < 64 ? 32 : 256);
   }
   return true;
 }
@@ -347,7 +357,10 @@ __global__ void __launch_bounds__(kHwThreads, 1)
     // ------------------------------- row warps -------------------------------
     for (;;) {
       // ticket t = row t % B of the CTA's batch t / B; the warp that draws a
-      // batch's first ticket claims the batch from the global cursor
+      // batch's first ticket claims the batch from the global cursor, in
+      // ticket order (so a higher ticket is always a higher row).  One global
+      // claim per row was measured and lost: the same-address atomics cost
+      // 2.4k -> 4.8k cycles per row on R-MAT 27 (heavy pass 32 -> 39 ms).
       int t = 0;
       if (lane == 0) t = atomicAdd(&s_ticket, 1);
       t = __shfl_sync(kFull, t, 0);
@@ -355,7 +368,6 @@ __global__ void __launch_bounds__(kHwThreads, 1)
       long long r = 0;
       if (lane == 0) {
         if (p == 0) {
-          // claims in ticket order, so a higher ticket is always a higher row
           if (lb > 0)
             while (ld_acquire_cta_s32(&s_btag[(lb - 1) % kHwBufs]) != lb - 1) {
             }

@@ -660,3 +660,99 @@ def test_first_fit_serial_fallback_and_long_path(monkeypatch, oracle_mod):
     for g in (path, er):
         ff = oracle_mod.first_fit_sequential(oracle_csr(oracle_mod, g))
         assert np.array_equal(gcol.first_fit_sequential(g), ff)
+
+
+def class_order_first_fit(oracle_mod, off, cols, T=64):
+    """Sequential First-Fit (coloring.hpp:110-116, the oracle's) in the order
+    "rows of degree >= T ascending, then the others ascending": relabel,
+    colour with the oracle, map back."""
+    n = off.size - 1
+    deg = np.diff(off)
+    heavy = deg >= T
+    order = np.concatenate([np.nonzero(heavy)[0], np.nonzero(~heavy)[0]])
+    newid = np.empty(n, np.int64)
+    newid[order] = np.arange(n)
+    rows = np.repeat(np.arange(n), deg)
+    r2, c2 = newid[rows], newid[cols]
+    k = np.lexsort((c2, r2))
+    off2 = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(r2, minlength=n), out=off2[1:])
+    ff = oracle_mod.first_fit_sequential(oracle_mod.CSR(off2, c2[k].astype(np.int32)))
+    return ff[newid]
+
+
+def test_waiting_heavy_pass_is_class_order_first_fit(oracle_mod):
+    """k1_wide=6: heavy rows wait for their pending lower heavy neighbours
+    (k1_heavy_wait), light rows for their lower light ones (K1L) -- the result
+    is First-Fit in class order bit for bit, nothing is logged, one round."""
+    rng = np.random.default_rng(404)
+    graphs_ = [hub_graph(rng, 5000, 3, 2500, 4.0), hub_graph(rng, 60_000, 40, 5000, 6.0),
+               hub_graph(rng, 200_000, 12, 40_000, 3.0), hub_graph(rng, 30_000, 300, 1500, 2.0)]
+    for g in graphs_:
+        want = class_order_first_fit(oracle_mod, g.offsets(), g.adjacency())
+        for _ in range(3):
+            run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=6))
+            check_run(g, run, 1)
+            assert run.stats.heavy_rows > 0 and run.stats.pairs_logged == 0
+            assert run.stats.rounds == 1 and list(run.stats.conflicts_per_round) == [0]
+            assert np.array_equal(run.coloring, want)
+
+
+def test_waiting_heavy_pass_rmat_scaled_exact(oracle_mod):
+    """R-MAT scale 18 and 20 (dense hub core, long dependency chains)."""
+    for sd in (6, 4):
+        off, cols = graphs.make_config("rmat24", "cuda", scale_down=sd)
+        g = gcol.Graph.from_device(off, cols)
+        off_np, cols_np = off.cpu().numpy(), cols.cpu().numpy()
+        want = class_order_first_fit(oracle_mod, off_np, cols_np)
+        for _ in range(2):
+            run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=6))
+            assert run.stats.pairs_logged == 0 and run.stats.rounds == 1
+            assert np.array_equal(run.coloring, want)
+        # never more colours than the reference's multi-threaded RSOC would be allowed
+        o = oracle_mod.CSR(off_np, cols_np)
+        ref = oracle_mod.color_parallel(o, 8, "rsoc")[1]["num_colors"]
+        assert int(want.max()) + 1 <= int(1.05 * ref)
+
+
+def test_waiting_heavy_pass_guard_logs_and_rounds_repair(oracle_mod):
+    """k1_wait_polls < 0: no waiting at all -- every pending read is logged at
+    once (the guard path of k1_heavy_wait) with a full SM of rows in flight;
+    the rounds must repair it.  A small poll budget sits in between."""
+    rng = np.random.default_rng(405)
+    g = hub_graph(rng, 60_000, 40, 5000, 6.0)
+    for polls in (-1, 2):
+        run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=6, k1_wait_polls=polls))
+        check_run(g, run, 1)
+        assert run.stats.heavy_rows > 0
+    run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=6, k1_wait_polls=-1))
+    assert run.stats.pairs_logged > 0
+
+
+def test_waiting_heavy_pass_streamed_one_call(monkeypatch, oracle_mod):
+    """One-call host path with the waiting heavy pass: rows start only once
+    their adjacency pieces are resident (1M-entry pieces), result still exact."""
+    off, cols = graphs.make_config("rmat24", "cuda", scale_down=5)
+    h_off, h_cols = off.cpu().pin_memory(), cols.cpu().pin_memory()
+    want = class_order_first_fit(oracle_mod, h_off.numpy(), h_cols.numpy())
+    out = torch.empty(off.numel() - 1, dtype=torch.int32).pin_memory()
+    for shift in ("31", "20", "20"):
+        monkeypatch.setenv("GCOL_UPLOAD_SHIFT", shift)
+        out.fill_(-7)
+        run = gcol.color_rsoc_csr(h_off, h_cols, 1, gcol.ParallelOptions(k1_wide=6), colors_out=out)
+        assert run.stats.heavy_rows > 0 and run.stats.pairs_logged == 0
+        assert np.array_equal(out.numpy(), want)
+
+
+def test_heavy_pass_choice_by_option():
+    """k1_wide 5 / 6 force the speculative / waiting heavy pass; 4 and 0 pick by
+    graph size (small graphs: speculative)."""
+    rng = np.random.default_rng(406)
+    g = hub_graph(rng, 20000, 5, 3000, 4.0)
+    for w in (0, 4, 5, 6):
+        run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=w))
+        check_run(g, run, 1)
+        assert run.stats.heavy_rows > 0
+    a = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=6)).coloring
+    b = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=6)).coloring
+    assert np.array_equal(a, b)  # deterministic
