@@ -66,34 +66,37 @@ __device__ __forceinline__ bool hw_wait(const int* __restrict__ cols, const int*
                                         unsigned* win, uint64_t pol, int polls, const PL& L,
                                         long long& n_polls) {
   const int lane = lane_id();
-  int idle = 0, wpos = -1;
+  int idle = 0, base = -1;
   int w[kHwWin];
   bool end = false;
   while (pos != INT_MAX) {
     int c[kHwWin];
-    if (wpos != pos) {  // the window's ids stay in registers while it does not move
+    if (base < 0) {  // (re)load the window: its ids stay in registers while pos moves inside it
+      base = pos;
       end = false;
 #pragma unroll
       for (int u = 0; u < kHwWin; ++u) {
-        const int i = pos + u * 32 + lane;
+        const int i = base + u * 32 + lane;
         w[u] = i < deg ? ld_col(cols + b + i, pol) : INT_MAX;
         end |= w[u] > v;
       }
-      wpos = pos;
     }
+    // entries before pos are final and marked already
 #pragma unroll
-    for (int u = 0; u < kHwWin; ++u) c[u] = w[u] < v ? ld_color(colors + w[u]) : -3;
+    for (int u = 0; u < kHwWin; ++u)
+      c[u] = (w[u] < v && base + u * 32 + lane >= pos) ? ld_color(colors + w[u]) : -3;
     int first = INT_MAX;
 #pragma unroll
     for (int u = 0; u < kHwWin; ++u) {
       hv_mark(reg, win, c[u], lim);
-      if (c[u] == kPending) first = min(first, pos + u * 32 + lane);
+      if (c[u] == kPending) first = min(first, base + u * 32 + lane);
     }
     first = __reduce_min_sync(kFull, first);
     ++n_polls;
     if (first == INT_MAX) {  // the window is final
       if (__any_sync(kFull, end)) break;
-      pos += kHwWin * 32;
+      pos = base + kHwWin * 32;
+      base = -1;
       idle = 0;
       continue;
     }
@@ -218,6 +221,8 @@ __device__ __forceinline__ void hw_hub(const long long* __restrict__ off, const 
   hv_tick(H.prof, t_last, p_pieces);
   unsigned long long reg = 0ull;
   const unsigned pw = ld_relaxed_u32(H.slot_pend + slot);
+  // the pieces' bitmap is final here: read it before the wait, off the hop to the next row
+  const unsigned slot_word = ld_relaxed_u32(S.slot_bm + (size_t)slot * 32 + lane);
   if (pw != 0u) {
     ++n_waited;
     hw_wait<PL>(cols, colors, v, b, deg, INT_MAX - (int)pw, 1023, reg, win, pol, H.polls, L, n_polls);
@@ -226,7 +231,7 @@ __device__ __forceinline__ void hw_hub(const long long* __restrict__ off, const 
   const unsigned lo = __reduce_or_sync(kFull, (unsigned)reg);
   const unsigned hi = __reduce_or_sync(kFull, (unsigned)(reg >> 32));
   __syncwarp();
-  unsigned word = win[lane] | ld_relaxed_u32(S.slot_bm + (size_t)slot * 32 + lane);
+  unsigned word = win[lane] | slot_word;
   if (lane == 0) word |= lo;
   if (lane == 1) word |= hi;
   const unsigned nz = __ballot_sync(kFull, word != kFull);
