@@ -27,4 +27,11 @@ GCOL_EAGER=1 GCOL_K1H_V=3 timeout 900 ncu --set full --clock-control none --impo
 GCOL_EAGER=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KRE" -c 400 --csv \
   --log-file $OUT/launches_rmat24.csv python tools/one_run.py rmat24 > $OUT/launches_rmat24.log 2>&1
 }
+# summaries here (the reports together exceed what gpurun brings back); one report kept
+for r in k1hw_rmat27 k1l_rmat27 k1h_rmat24 kheavy_rmat24 klist_rmat24 k1hw_rmat24; do
+  if [ -f $OUT/$r.ncu-rep ]; then
+    ( python tools/ncu_summary.py report $OUT/$r.ncu-rep; echo; echo "hottest source lines:"; python tools/ncu_hot.py $OUT/$r.ncu-rep 20 ) > $OUT/${r}_full.txt 2>&1
+    [ $r = k1hw_rmat27 ] || rm -f $OUT/$r.ncu-rep
+  fi
+done
 ls -la $OUT
