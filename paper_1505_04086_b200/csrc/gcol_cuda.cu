@@ -109,6 +109,8 @@ struct ClassPlan {
   int T = 0;
   int nh = 0;
   HeavyRow* d_rows = nullptr;
+  HvRank* d_rank = nullptr;  // heavy-rank table, (n + 31) / 32 words (big graphs only)
+  int* d_hcol = nullptr;     // heavy colours by rank (compact K1HW)
 };
 
 }  // namespace
@@ -581,13 +583,23 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 // fits L2 every gather pays HBM latency and only the waiting pass can keep
 // enough rows in flight (R-MAT 27: 32.0 against 34.6 ms, one round instead of
 // eleven, 957 colours -- serial First-Fit's count -- instead of ~1010).
+// The colour array no longer fits L2 (B200: 126 MB, about half usable for it
+// next to the streaming CSR).  GCOL_L2_COLOURS_MB moves the limit (tests use
+// 0 to run the big-graph path -- waiting heavy pass, compact colours -- on
+// small graphs); read per call.
+bool colours_beyond_l2(const gcol_cuda_graph* g) {
+  const char* e = std::getenv("GCOL_L2_COLOURS_MB");
+  const size_t mb = e ? static_cast<size_t>(std::max(0, std::atoi(e))) : 64;
+  return sizeof(int) * static_cast<size_t>(g->n) > (mb << 20);
+}
+
 bool heavy_pass_waits(const gcol_cuda_graph* g, int k1_wide) {
   static const int v = env_int("GCOL_K1H_V", 0, 0, 3);
   if (v == 3) return true;
   if (v == 1 || v == 2) return false;
   if (k1_wide == 5) return false;
   if (k1_wide == 6) return true;
-  return sizeof(int) * static_cast<size_t>(g->n) > (size_t{64} << 20);
+  return colours_beyond_l2(g);
 }
 
 // K1 variant of the in-place initial pass: 0 narrow, 1 wide, 2 K1W (the
@@ -703,7 +715,11 @@ int get_class(gcol_cuda_graph* g, int T, ClassPlan** out) {
     GCOL_CK(cudaStreamSynchronize(g->stream));
     P.nh = nh;
     GCOL_CK(dalloc(&P.d_rows, static_cast<size_t>(nh), g->stream));
-    if (nh > 0) k_class_write<<<nb, kBlock, 0, g->stream>>>(g->d_off, n, T, d_cnt, P.d_rows);
+    if (colours_beyond_l2(g) && nh > 0) {  // the compact waiting heavy pass will want them
+      GCOL_CK(dalloc(&P.d_rank, static_cast<size_t>((g->n + 31) / 32), g->stream));
+      GCOL_CK(dalloc(&P.d_hcol, static_cast<size_t>(nh), g->stream));
+    }
+    if (nh > 0) k_class_write<<<nb, kBlock, 0, g->stream>>>(g->d_off, n, T, d_cnt, P.d_rows, P.d_rank);
     GCOL_CK(cudaGetLastError());
     GCOL_CK(cudaFreeAsync(d_cnt, g->stream));
   }
@@ -739,7 +755,14 @@ int k1h_version() {
   return v;
 }
 
-const void* k1_light_fn(bool m32, bool stream) {
+const void* k1_light_fn(bool m32, bool stream, bool compact) {
+  if (compact) {
+    if (stream)
+      return m32 ? reinterpret_cast<const void*>(k1_wait<true, true, true, true>)
+                 : reinterpret_cast<const void*>(k1_wait<true, false, true, true>);
+    return m32 ? reinterpret_cast<const void*>(k1_wait<false, true, true, true>)
+               : reinterpret_cast<const void*>(k1_wait<false, false, true, true>);
+  }
   if (stream)
     return m32 ? reinterpret_cast<const void*>(k1_wait<true, true, true>)
                : reinterpret_cast<const void*>(k1_wait<true, false, true>);
@@ -753,7 +776,12 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls, bool waiting) {
   if (int rc = get_class(g, T, &CP)) return rc;
   // light pass: a fully resident waiting grid (as K1W)
   K1Launch& K = C->light;
-  K.wfn = k1_light_fn(T <= 32, g->d_ready != nullptr);
+  // compact heavy colours (rank table + 4 nh bytes, L2-resident) once the colour array
+  // itself is not: GCOL_K1HW_COMPACT=0 keeps the gathers on the colour array for A/B;
+  // GCOL_K1L_COMPACT=0 only the light pass's
+  const bool compact = waiting && CP->d_rank && env_int("GCOL_K1HW_COMPACT", 1, 0, 1) == 1;
+  const bool lcompact = compact && env_int("GCOL_K1L_COMPACT", 1, 0, 1) == 1;
+  K.wfn = k1_light_fn(T <= 32, g->d_ready != nullptr, lcompact);
   int occ = 1;
   GCOL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K.wfn, kWaitBlock, 0));
   occ = std::max(1, std::min(occ, 2048 / kWaitBlock));
@@ -769,9 +797,14 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls, bool waiting) {
                  nullptr, 0ull};
   K.W.light_lim = T;
   K.W.light_coop = env_int("GCOL_K1L_COOP", 1, 0, 1);
+  if (lcompact) {
+    K.W.rank = reinterpret_cast<const uint2*>(CP->d_rank);
+    K.W.hcol = CP->d_hcol;
+  }
   // heavy pass: one persistent CTA per SM (GCOL_K1H_BPS for experiments)
   const bool v3 = waiting, v2 = !waiting && k1h_version() == 2;
-  C->hfn = v3   ? reinterpret_cast<const void*>(k1_heavy_wait<PairLog>)
+  C->hfn = v3   ? (compact ? reinterpret_cast<const void*>(k1_heavy_wait<PairLog, true>)
+                           : reinterpret_cast<const void*>(k1_heavy_wait<PairLog, false>))
            : v2 ? reinterpret_cast<const void*>(k1_heavy2<PairLog>)
                 : reinterpret_cast<const void*>(k1_heavy<PairLog>);
   C->hthreads = v3 ? kHwThreads : v2 ? kH2Threads : kHvThreads;
@@ -828,6 +861,10 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls, bool waiting) {
     // row may wait for most of the pass behind a long chain, ~0.5 us a poll)
     C->H.polls = env_int("GCOL_K1H_POLLS", polls == kWaitPollsDefault ? 1 << 22 : polls, 0, 1 << 30);
     C->H.slot_pend = P->d_q_seq;
+    if (compact) {
+      C->H.rank = CP->d_rank;
+      C->H.hcol = CP->d_hcol;
+    }
   }
   C->publishers = C->grid_h * (v2 ? C->H.commit_warps : C->H.row_warps);
   // log slices: [0, grid_h) heavy CTAs (15/16 of the log: K1H logs its stale
@@ -880,7 +917,7 @@ int add_class_nodes(gcol_cuda_graph* g, cudaGraph_t graph, cudaGraphNode_t dep, 
   ClassPlan* CP = &g->classes[class_threshold()];
   cudaGraphNode_t n_mark, n_h, n_evh, n_l;
   GCOL_CK(add_kernel(&n_mark, graph, &dep, 1, k_mark_pending, dim3(g->sms * 4), dim3(kBlock),
-                     static_cast<const HeavyRow*>(CP->d_rows), CP->nh, g->d_colors));
+                     static_cast<const HeavyRow*>(CP->d_rows), CP->nh, g->d_colors, C.H.hcol));
   {
     const long long* off = g->d_off;
     const int* cols = g->d_cols;
@@ -920,7 +957,7 @@ int add_class_nodes(gcol_cuda_graph* g, cudaGraph_t graph, cudaGraphNode_t dep, 
 // The same two passes launched eagerly on the library stream.
 int launch_class_eager(gcol_cuda_graph* g, ClassLaunch& C) {
   ClassPlan* CP = &g->classes[class_threshold()];
-  k_mark_pending<<<g->sms * 4, kBlock, 0, g->stream>>>(CP->d_rows, CP->nh, g->d_colors);
+  k_mark_pending<<<g->sms * 4, kBlock, 0, g->stream>>>(CP->d_rows, CP->nh, g->d_colors, C.H.hcol);
   GCOL_CK(cudaGetLastError());
   {
     const long long* off = g->d_off;
@@ -2033,7 +2070,8 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
   }
   for (auto& kv : g->splits) free_split(g, kv.second);
   for (auto& kv : g->classes)
-    for (void* p : {static_cast<void*>(kv.second.d_rows)})
+    for (void* p : {static_cast<void*>(kv.second.d_rows), static_cast<void*>(kv.second.d_rank),
+                    static_cast<void*>(kv.second.d_hcol)})
       if (p && g->stream) cudaFreeAsync(p, g->stream);
   if (g->stream) {
     if (g->owns_csr) {

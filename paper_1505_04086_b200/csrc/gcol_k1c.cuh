@@ -83,6 +83,17 @@ struct alignas(16) HvPiece {
 };
 constexpr int kHvSlotMax = 1 << 22;
 
+// Heavy-rank table (per graph, built with the heavy-row table): per 32-id
+// word, the heavy ids' bit mask and the number of heavy ids below the word,
+// so rank(w) = base + popc(bits below w).  The compact variant of the waiting
+// heavy pass (gcol_k1hw.cuh) keeps the heavy rows' colours in an array indexed
+// by rank: 4 x heavy rows bytes (R-MAT 27: 32 MB, L2-resident) instead of
+// gathers into a 537 MB colour array that miss L2 four times out of five.
+struct alignas(8) HvRank {
+  unsigned bits;
+  int base;
+};
+
 struct HeavyArgs {
   HvPiece* q16;       // [npieces] piece records (split rows)
   const HeavyRow* rows;
@@ -101,6 +112,10 @@ struct HeavyArgs {
   // k1_heavy_wait (gcol_k1hw.cuh): per split-row slot, INT_MAX - the position of the
   // first entry a piece read as pending (0: none); zeroed before every run
   unsigned* slot_pend;
+  // compact variant of k1_heavy_wait: rank table and the heavy colours by rank
+  // (-2 pending); every commit writes both this array and the colour array
+  const HvRank* rank;
+  int* hcol;
 };
 
 // K1H colour reads and writes.  (A compact heavy-colour array indexed through
@@ -167,7 +182,8 @@ __global__ void __launch_bounds__(1024) k_class_scan(int* counts, int nb, int* t
 }
 
 __global__ void __launch_bounds__(kBlock) k_class_write(const long long* __restrict__ off, int n,
-                                                        int T, const int* pre, HeavyRow* rows) {
+                                                        int T, const int* pre, HeavyRow* rows,
+                                                        HvRank* rank) {
   __shared__ int s_w[kWarps];
   __shared__ int s_base;
   if (threadIdx.x == 0) s_base = pre[blockIdx.x];
@@ -189,6 +205,7 @@ __global__ void __launch_bounds__(kBlock) k_class_write(const long long* __restr
     int before = s_base;
     for (int k = 0; k < warp; ++k) before += s_w[k];
     if (h) rows[before + __popc(m & ((1u << lane) - 1u))] = HeavyRow{b, (int)v, d};
+    if (rank && lane == 0 && v < n) rank[v >> 5] = HvRank{m, before};  // v = the word's first id
     __syncthreads();
     if (threadIdx.x == 0) {
       int t = 0;
@@ -198,11 +215,14 @@ __global__ void __launch_bounds__(kBlock) k_class_write(const long long* __restr
   }
 }
 
-// Heavy rows start pending: colors[v] := -2.
-__global__ void k_mark_pending(const HeavyRow* __restrict__ rows, int nh, int* colors) {
+// Heavy rows start pending: colors[v] := -2; compact variant: hcol[*] := -2
+// (K1HW then reads heavy colours only through hcol).
+__global__ void k_mark_pending(const HeavyRow* __restrict__ rows, int nh, int* colors, int* hcol) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nh;
-       i += (long long)gridDim.x * blockDim.x)
-    colors[rows[i].v] = kPending;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (hcol) hcol[i] = kPending;
+    else colors[rows[i].v] = kPending;
+  }
 }
 
 // --------------------------------------------------------------------------

@@ -52,6 +52,32 @@ constexpr int kHwBufs = 8;                   // claimed-batch records kept
 constexpr int kHwWin = 4;                    // entries per lane per wait window
 constexpr size_t kHwSmem = sizeof(int) * kHvPieceWarps * kHvPieceBuf;  // dynamic: piece buffers
 
+// Where a neighbour's colour is read.  Plain variant: the colour array, index
+// w.  Compact variant (kC): the heavy colours by rank -- one 8-byte load of
+// the rank word, then rank = base + popc(bits below w); -1 for a light row
+// (its colour is not read at all: it has not started and reads this row
+// itself later).
+__device__ __forceinline__ uint2 ld_nc_u32x2(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+
+template <bool kC>
+__device__ __forceinline__ int hw_slot(const HeavyArgs& H, int w) {
+  if (!kC) return w;
+  const uint2 e = ld_nc_u32x2(H.rank + (w >> 5));
+  const unsigned bit = 1u << (w & 31);
+  return (e.x & bit) ? (int)e.y + __popc(e.x & (bit - 1u)) : -1;
+}
+
+// Commit heavy row v (heavy index hr) with colour c (one lane).
+template <bool kC>
+__device__ __forceinline__ void hw_commit(const HeavyArgs& H, int* colors, int v, long long hr, int c) {
+  if (kC) st_color(H.hcol + hr, c);  // what the waiting rows poll
+  commit_color(colors, v, c);        // what the light pass, the rounds and the caller read
+}
+
 // A warp holds at most one ticket at a time, so at most kHwWarps tickets are
 // between "drawn" and "record read": a record is overwritten kHwBufs batches later.
 static_assert(kHwBufs * kHwBatch >= kHwWarps + 2 * kHwBatch, "batch records must outlive their readers");
@@ -60,14 +86,15 @@ static_assert(kHwBufs * kHwBatch >= kHwWarps + 2 * kHwBatch, "batch records must
 // and an id below v reads as pending; colours that became final are marked.
 // Past `polls` polls without progress the remaining pending entries are
 // logged (returns false).  pos == INT_MAX: nothing to wait for.
-template <class PL>
-__device__ __forceinline__ bool hw_wait(const int* __restrict__ cols, const int* colors, int v,
-                                        long long b, int deg, int pos, int lim, unsigned long long& reg,
-                                        unsigned* win, uint64_t pol, int polls, const PL& L,
-                                        long long& n_polls) {
+template <class PL, bool kC>
+__device__ __forceinline__ bool hw_wait(const int* __restrict__ cols, const int* colors, const HeavyArgs& H,
+                                        int v, long long b, int deg, int pos, int lim,
+                                        unsigned long long& reg, unsigned* win, uint64_t pol, int polls,
+                                        const PL& L, long long& n_polls) {
   const int lane = lane_id();
+  const int* cbase = kC ? H.hcol : colors;
   int idle = 0, base = -1;
-  int w[kHwWin];
+  int a[kHwWin];  // the window's colour slots (-1: nothing to read)
   bool end = false;
   while (pos != INT_MAX) {
     int c[kHwWin];
@@ -75,16 +102,20 @@ __device__ __forceinline__ bool hw_wait(const int* __restrict__ cols, const int*
       base = pos;
       end = false;
 #pragma unroll
+      int w[kHwWin];
+#pragma unroll
       for (int u = 0; u < kHwWin; ++u) {
         const int i = base + u * 32 + lane;
         w[u] = i < deg ? ld_col(cols + b + i, pol) : INT_MAX;
         end |= w[u] > v;
       }
+#pragma unroll
+      for (int u = 0; u < kHwWin; ++u) a[u] = w[u] < v ? hw_slot<kC>(H, w[u]) : -1;
     }
     // entries before pos are final and marked already
 #pragma unroll
     for (int u = 0; u < kHwWin; ++u)
-      c[u] = (w[u] < v && base + u * 32 + lane >= pos) ? ld_color(colors + w[u]) : -3;
+      c[u] = (a[u] >= 0 && base + u * 32 + lane >= pos) ? ld_color(cbase + a[u]) : -3;
     int first = INT_MAX;
 #pragma unroll
     for (int u = 0; u < kHwWin; ++u) {
@@ -112,7 +143,8 @@ __device__ __forceinline__ bool hw_wait(const int* __restrict__ cols, const int*
         for (int u = 0; u < kHwWin; ++u) {
           const int i = pos + u * 32 + lane;
           const int ww = i < deg ? ld_col(cols + b + i, pol) : INT_MAX;
-          const int cc = ww < v ? ld_color(colors + ww) : -3;
+          const int aa = ww < v ? hw_slot<kC>(H, ww) : -1;
+          const int cc = aa >= 0 ? ld_color(cbase + aa) : -3;
           hv_mark(reg, win, cc, lim);
           log_pairs(L, cc == kPending, ww, v);
           e2 |= ww > v;
@@ -127,9 +159,9 @@ __device__ __forceinline__ bool hw_wait(const int* __restrict__ cols, const int*
 }
 
 // One heavy row below the split threshold (warp-collective).
-template <class PL>
+template <class PL, bool kC>
 __device__ __forceinline__ void hw_row(const int* __restrict__ cols, int* colors, const HeavyArgs& H,
-                                       const HeavyRow& e0, unsigned* win, uint64_t pol, const PL& L,
+                                       const HeavyRow& e0, long long hr, unsigned* win, uint64_t pol, const PL& L,
                                        unsigned& gathers, long long& p_scan, long long& p_wait,
                                        long long& n_polls, long long& n_waited, long long& t_last) {
   const int lane = lane_id();
@@ -139,14 +171,26 @@ __device__ __forceinline__ void hw_row(const int* __restrict__ cols, int* colors
   __syncwarp();
   unsigned long long reg = 0ull;
   int pmin = INT_MAX;
+  const int* cbase = kC ? H.hcol : colors;
   HvCols cb = hv_load_block(cols, b, deg, 0, pol);
   for (int base = 0;;) {
     int c[kHvU];
     bool past = false;
+    if (kC) {  // the rank words first (eight independent loads), then the colours
+      int a[kHvU];
 #pragma unroll
-    for (int u = 0; u < kHvU; ++u) {
-      c[u] = cb.w[u] < v ? hv_gather(H, colors, cb.w[u]) : -3;
-      past |= cb.w[u] > v;  // sorted row (INT_MAX past the end)
+      for (int u = 0; u < kHvU; ++u) {
+        a[u] = cb.w[u] < v ? hw_slot<true>(H, cb.w[u]) : -1;
+        past |= cb.w[u] > v;  // sorted row (INT_MAX past the end)
+      }
+#pragma unroll
+      for (int u = 0; u < kHvU; ++u) c[u] = a[u] >= 0 ? hv_ld_color(cbase + a[u]) : -3;
+    } else {
+#pragma unroll
+      for (int u = 0; u < kHvU; ++u) {
+        c[u] = cb.w[u] < v ? hv_ld_color(cbase + cb.w[u]) : -3;
+        past |= cb.w[u] > v;
+      }
     }
     const bool more = base + kHvBlock < deg && !__any_sync(kFull, past);
     HvCols nb;
@@ -165,7 +209,7 @@ __device__ __forceinline__ void hw_row(const int* __restrict__ cols, int* colors
   hv_tick(H.prof, t_last, p_scan);
   if (pmin != INT_MAX) {
     ++n_waited;
-    hw_wait<PL>(cols, colors, v, b, deg, pmin, deg, reg, win, pol, H.polls, L, n_polls);
+    hw_wait<PL, kC>(cols, colors, H, v, b, deg, pmin, deg, reg, win, pol, H.polls, L, n_polls);
     hv_tick(H.prof, t_last, p_wait);
   }
   const unsigned lo = __reduce_or_sync(kFull, (unsigned)reg);
@@ -177,16 +221,43 @@ __device__ __forceinline__ void hw_row(const int* __restrict__ cols, int* colors
   const unsigned nf = __ballot_sync(kFull, word != kFull);
   const int j = __ffs(nf) - 1;
   const unsigned wj = __shfl_sync(kFull, word, j);
-  if (lane == 0) commit_color(colors, v, j * 32 + __ffs(~wj) - 1);
+  if (lane == 0) hw_commit<kC>(H, colors, v, hr, j * 32 + __ffs(~wj) - 1);
   __syncwarp();
+}
+
+// First-Fit of a split row restricted to the colour window [wb, wb + 1024),
+// over its lower heavy neighbours (all final by now); -1 when the window
+// holds no free colour <= deg.  Only when the first 1024 colours are all taken.
+template <bool kC>
+__device__ __noinline__ int hw_ff_window(const int* __restrict__ cols, const int* colors, const HeavyArgs& H,
+                                         int v, long long b, int deg, int wb, unsigned* win, uint64_t pol) {
+  const int lane = lane_id();
+  const int* cbase = kC ? H.hcol : colors;
+  win[lane] = 0u;
+  __syncwarp();
+  for (int i0 = 0; i0 < deg; i0 += 32) {
+    const int i = i0 + lane;
+    const int w = i < deg ? ld_col(cols + b + i, pol) : INT_MAX;
+    const int a = w < v ? hw_slot<kC>(H, w) : -1;
+    const int c = a >= 0 ? ld_color(cbase + a) : -1;
+    if (c >= wb && c < wb + 1024 && c <= deg) atomicOr(&win[(c - wb) >> 5], 1u << (c & 31));
+    if (__any_sync(kFull, w > v)) break;
+  }
+  __syncwarp();
+  const unsigned word = win[lane];
+  const unsigned nf = __ballot_sync(kFull, word != kFull);
+  if (!nf) return -1;
+  const int j = __ffs(nf) - 1;
+  const int c = wb + j * 32 + __ffs(~__shfl_sync(kFull, word, j)) - 1;
+  return c <= deg ? c : -1;
 }
 
 // One split row (warp-collective; the owner): publish its pieces, wait for
 // them, wait for what they read as pending, First-Fit, commit.
-template <class PL>
+template <class PL, bool kC>
 __device__ __forceinline__ void hw_hub(const long long* __restrict__ off, const int* __restrict__ cols,
                                        int* colors, const SplitArgs& S, const HeavyArgs& H,
-                                       const HeavyRow& e0, unsigned* win, uint64_t pol, const PL& L,
+                                       const HeavyRow& e0, long long hr, unsigned* win, uint64_t pol, const PL& L,
                                        long long& p_pieces, long long& p_wait, long long& n_polls,
                                        long long& n_waited, long long& t_last) {
   const int lane = lane_id();
@@ -225,7 +296,7 @@ __device__ __forceinline__ void hw_hub(const long long* __restrict__ off, const 
   const unsigned slot_word = ld_relaxed_u32(S.slot_bm + (size_t)slot * 32 + lane);
   if (pw != 0u) {
     ++n_waited;
-    hw_wait<PL>(cols, colors, v, b, deg, INT_MAX - (int)pw, 1023, reg, win, pol, H.polls, L, n_polls);
+    hw_wait<PL, kC>(cols, colors, H, v, b, deg, INT_MAX - (int)pw, 1023, reg, win, pol, H.polls, L, n_polls);
     hv_tick(H.prof, t_last, p_wait);
   }
   const unsigned lo = __reduce_or_sync(kFull, (unsigned)reg);
@@ -242,9 +313,9 @@ __device__ __forceinline__ void hw_hub(const long long* __restrict__ off, const 
   } else {  // 1024 distinct lower colours: the next windows, scanning the row (all final now)
     color = -1;
     for (int wb = 1024; color < 0 && wb <= deg; wb += 1024)
-      color = warp_ff_window<false, true>(cols, colors, v, b, deg, wb, win, pol);
+      color = hw_ff_window<kC>(cols, colors, H, v, b, deg, wb, win, pol);
   }
-  if (lane == 0) commit_color(colors, v, color);
+  if (lane == 0) hw_commit<kC>(H, colors, v, hr, color);
   __syncwarp();
 }
 
@@ -252,6 +323,7 @@ __device__ __forceinline__ void hw_hub(const long long* __restrict__ off, const 
 // that a pending neighbour is not logged -- the smallest position of one is
 // left for the owner in H.slot_pend[slot] -- and the last piece does not
 // commit.
+template <bool kC>
 __device__ __forceinline__ void hw_piece(const long long* __restrict__ off, const int* __restrict__ cols,
                                          const int* colors, const SplitArgs& S, const HeavyArgs& H,
                                          const HvPiece& r, int* buf, unsigned long long* bar,
@@ -288,8 +360,16 @@ __device__ __forceinline__ void hw_piece(const long long* __restrict__ off, cons
       w[u] = i >= len ? INT_MAX : (o + i < nc ? buf[o + i] : ld_col(cols + r.a + i, pol));
       past |= w[u] > v;
     }
+    if (kC) {
+      int a[B];
 #pragma unroll
-    for (int u = 0; u < B; ++u) c[u] = w[u] < v ? hv_gather(H, colors, w[u]) : -3;
+      for (int u = 0; u < B; ++u) a[u] = w[u] < v ? hw_slot<true>(H, w[u]) : -1;
+#pragma unroll
+      for (int u = 0; u < B; ++u) c[u] = a[u] >= 0 ? hv_ld_color(H.hcol + a[u]) : -3;
+    } else {
+#pragma unroll
+      for (int u = 0; u < B; ++u) c[u] = w[u] < v ? hv_ld_color(colors + w[u]) : -3;
+    }
 #pragma unroll
     for (int u = 0; u < B; ++u) {
       gathers += w[u] < v;
@@ -316,7 +396,7 @@ __device__ __forceinline__ void hw_piece(const long long* __restrict__ off, cons
   hv_tick(H.prof, t_last, pp[2]);
 }
 
-template <class PL>
+template <class PL, bool kC>
 __global__ void __launch_bounds__(kHwThreads, 1)
     k1_heavy_wait(const long long* __restrict__ off, const int* __restrict__ cols, int* colors, Ctrl* ctrl,
                   PairLogArgs LA, SplitArgs S, HeavyArgs H) {
@@ -398,9 +478,9 @@ __global__ void __launch_bounds__(kHwThreads, 1)
       __syncwarp();
       hv_tick(H.prof, t_last, p_claim);
       if (e0.deg >= S.min_deg)
-        hw_hub<PL>(off, cols, colors, S, H, e0, win, pol, L, p_pieces, p_wait, n_polls, n_waited, t_last);
+        hw_hub<PL, kC>(off, cols, colors, S, H, e0, r, win, pol, L, p_pieces, p_wait, n_polls, n_waited, t_last);
       else
-        hw_row<PL>(cols, colors, H, e0, win, pol, L, gathers, p_scan, p_wait, n_polls, n_waited, t_last);
+        hw_row<PL, kC>(cols, colors, H, e0, r, win, pol, L, gathers, p_scan, p_wait, n_polls, n_waited, t_last);
       ++n_rows;
     }
     // retired: its piece allocations before the count drops
@@ -417,7 +497,7 @@ __global__ void __launch_bounds__(kHwThreads, 1)
       HvPiece pr;
       if (hv_pop16(S, H.q16, &s_mbhead, pc_hint, pr)) {
         hv_tick(H.prof, t_last, pp[3]);
-        hw_piece(off, cols, colors, S, H, pr, s_pbuf[pw], &s_pbar[pw], pphase, win, pol, gathers, t_last, pp);
+        hw_piece<kC>(off, cols, colors, S, H, pr, s_pbuf[pw], &s_pbar[pw], pphase, win, pol, gathers, t_last, pp);
         pc_hint = pc_new;
         ++n_pieces;
         continue;

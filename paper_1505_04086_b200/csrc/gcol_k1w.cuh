@@ -54,7 +54,33 @@ struct WaitArgs {
   int light_lim;                // class-split light pass: rows of degree >= light_lim are
                                 //   the heavy pass's (already coloured, skipped)
   int light_coop;               // light pass: long rows scanned warp-cooperatively
+  // light pass with compact heavy colours (class split on graphs whose colour array exceeds
+  // L2, gcol_k1hw.cuh): the heavy-rank table ({bits, base} per 32 ids) and the heavy rows'
+  // colours by rank, all final before this pass starts
+  const uint2* rank;
+  const int* hcol;
 };
+
+// Colour of neighbour w of light row v in the light pass, compact variant:
+// the rank word says whether w is heavy (then its colour comes from the
+// compact array, L2-resident) or light (a lower one is read from the colour
+// array and may be in flight; a higher one has not started and is not read
+// at all).  Two phases so that a step's rank loads are all in flight together.
+__device__ __forceinline__ uint2 k1l_rank_word(const WaitArgs& A, int w) {
+  uint2 r;
+  asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(A.rank + (w >> 5)));
+  return r;
+}
+__device__ __forceinline__ int k1l_colour(const WaitArgs& A, const int* colors, uint2 e, int w, int v) {
+  const unsigned bit = 1u << (w & 31);
+  if (e.x & bit) {
+    int c;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];"
+                 : "=r"(c) : "l"(A.hcol + ((int)e.y + __popc(e.x & (bit - 1u)))));
+    return c;
+  }
+  return w < v ? ld_color(colors + w) : -2;
+}
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -162,11 +188,12 @@ __device__ __forceinline__ void k1l_scan(const ColsGlobal& src, const int* color
 // colours OR-ed into per-row masks in shared memory.  A tile then costs
 // about two round trips instead of (its longest row / kW) of them.
 constexpr int kLightShort = 8;
-template <class Mask>
+template <class Mask, bool kC = false>
 __device__ __forceinline__ void k1l_scan_coop(const ColsGlobal& src, const int* colors, int v,
                                               bool valid, long long b, int deg, unsigned& gathers,
                                               Mask& mask, unsigned long long& pp,
-                                              unsigned long long* smask, unsigned long long* spp) {
+                                              unsigned long long* smask, unsigned long long* spp,
+                                              const WaitArgs& A) {
   const int lane = lane_id();
   mask = 0;
   pp = 0ull;
@@ -176,8 +203,16 @@ __device__ __forceinline__ void k1l_scan_coop(const ColsGlobal& src, const int* 
     int w[kLightShort], c[kLightShort];
 #pragma unroll
     for (int j = 0; j < kLightShort; ++j) w[j] = (sh && j < deg) ? src(b + j) : 0x7fffffff;
+    if (kC) {
+      uint2 e[kLightShort];
 #pragma unroll
-    for (int j = 0; j < kLightShort; ++j) c[j] = w[j] != 0x7fffffff ? ld_color(colors + w[j]) : -2;
+      for (int j = 0; j < kLightShort; ++j) e[j] = w[j] != 0x7fffffff ? k1l_rank_word(A, w[j]) : make_uint2(0u, 0u);
+#pragma unroll
+      for (int j = 0; j < kLightShort; ++j) c[j] = w[j] != 0x7fffffff ? k1l_colour(A, colors, e[j], w[j], v) : -2;
+    } else {
+#pragma unroll
+      for (int j = 0; j < kLightShort; ++j) c[j] = w[j] != 0x7fffffff ? ld_color(colors + w[j]) : -2;
+    }
 #pragma unroll
     for (int j = 0; j < kLightShort; ++j) {
       gathers += w[j] != 0x7fffffff;
@@ -216,8 +251,16 @@ __device__ __forceinline__ void k1l_scan_coop(const ColsGlobal& src, const int* 
       w[u] = i < E ? src(br + jj[u]) : 0x7fffffff;
     }
     int c[U];
+    if (kC) {
+      uint2 e[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) c[u] = w[u] != 0x7fffffff ? ld_color(colors + w[u]) : -2;
+      for (int u = 0; u < U; ++u) e[u] = w[u] != 0x7fffffff ? k1l_rank_word(A, w[u]) : make_uint2(0u, 0u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = w[u] != 0x7fffffff ? k1l_colour(A, colors, e[u], w[u], vr[u]) : -2;
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = w[u] != 0x7fffffff ? ld_color(colors + w[u]) : -2;
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       gathers += w[u] != 0x7fffffff;
@@ -290,7 +333,8 @@ constexpr int kWaitMinBlocks = 6;  // 48 resident warps per SM: 40 registers
 // kM32: every degree is <= 31, so the forbidden set fits 32 bits.
 // kClass: the light pass of the class-split initial pass (gcol_k1c.cuh):
 // rows of degree >= A.light_lim are skipped and whole rows are scanned.
-template <bool kStream, bool kM32, bool kClass = false>
+// kLC (with kClass): heavy neighbours' colours come from the compact array (A.rank, A.hcol).
+template <bool kStream, bool kM32, bool kClass = false, bool kLC = false>
 __global__ void __launch_bounds__(kWaitBlock, kClass ? kLightMinBlocks : kWaitMinBlocks)
     k1_wait(const long long* __restrict__ off, const int* __restrict__ cols, int n, int* colors,
             Ctrl* ctrl, PairLogArgs LA, WaitArgs A) {
@@ -347,9 +391,9 @@ __global__ void __launch_bounds__(kWaitBlock, kClass ? kLightMinBlocks : kWaitMi
     if (A.trace && lane == 0) t0 = globaltimer_ns();
     Mask mask;
     unsigned long long pp;
-    if (kClass && A.light_coop)
-      k1l_scan_coop<Mask>(src, colors, v, mine, b, deg, gathers, mask, pp,
-                          s_lmask[threadIdx.x >> 5], s_lpp[threadIdx.x >> 5]);
+    if (kClass && (kLC || A.light_coop))
+      k1l_scan_coop<Mask, kLC>(src, colors, v, mine, b, deg, gathers, mask, pp,
+                               s_lmask[threadIdx.x >> 5], s_lpp[threadIdx.x >> 5], A);
     else if (kClass)
       k1l_scan<kLightScanW, Mask>(src, colors, v, mine, b, deg, gathers, mask, pp);
     else

@@ -756,3 +756,46 @@ def test_heavy_pass_choice_by_option():
     a = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=6)).coloring
     b = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=6)).coloring
     assert np.array_equal(a, b)  # deterministic
+
+
+def test_waiting_heavy_pass_compact_colours_exact(monkeypatch, oracle_mod):
+    """The big-graph path on small graphs (GCOL_L2_COLOURS_MB=0): automatic
+    choice = waiting heavy pass reading the heavy colours through the rank
+    table and the compact array.  Same contract: class-order First-Fit bit for
+    bit; the colour array holds every final colour for the light pass."""
+    monkeypatch.setenv("GCOL_L2_COLOURS_MB", "0")
+    rng = np.random.default_rng(407)
+    cases = [hub_graph(rng, 5000, 3, 2500, 4.0), hub_graph(rng, 60_000, 40, 5000, 6.0),
+             hub_graph(rng, 200_001, 12, 40_000, 3.0), hub_graph(rng, 30_011, 300, 1500, 2.0)]
+    for g in cases:
+        want = class_order_first_fit(oracle_mod, g.offsets(), g.adjacency())
+        for w in (0, 6):
+            run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=w))
+            check_run(g, run, 1)
+            assert run.stats.heavy_rows > 0 and run.stats.pairs_logged == 0 and run.stats.rounds == 1
+            assert np.array_equal(run.coloring, want)
+    off, cols = graphs.make_config("rmat24", "cuda", scale_down=4)
+    g = gcol.Graph.from_device(off, cols)
+    want = class_order_first_fit(oracle_mod, off.cpu().numpy(), cols.cpu().numpy())
+    for _ in range(2):
+        run = gcol.color_rsoc(g, 1)
+        assert run.stats.pairs_logged == 0 and np.array_equal(run.coloring, want)
+    # guard path through the compact reads
+    g = cases[1]
+    run = gcol.color_rsoc(g, 1, gcol.ParallelOptions(k1_wide=6, k1_wait_polls=-1))
+    check_run(g, run, 1)
+    assert run.stats.pairs_logged > 0
+
+
+def test_waiting_heavy_pass_compact_streamed_one_call(monkeypatch, oracle_mod):
+    monkeypatch.setenv("GCOL_L2_COLOURS_MB", "0")
+    off, cols = graphs.make_config("rmat24", "cuda", scale_down=5)
+    h_off, h_cols = off.cpu().pin_memory(), cols.cpu().pin_memory()
+    want = class_order_first_fit(oracle_mod, h_off.numpy(), h_cols.numpy())
+    out = torch.empty(off.numel() - 1, dtype=torch.int32).pin_memory()
+    for shift in ("31", "20"):
+        monkeypatch.setenv("GCOL_UPLOAD_SHIFT", shift)
+        out.fill_(-7)
+        run = gcol.color_rsoc_csr(h_off, h_cols, 1, colors_out=out)
+        assert run.stats.heavy_rows > 0 and run.stats.pairs_logged == 0
+        assert np.array_equal(out.numpy(), want)
