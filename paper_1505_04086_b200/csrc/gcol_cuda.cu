@@ -110,7 +110,9 @@ struct ClassPlan {
   int nh = 0;
   HeavyRow* d_rows = nullptr;
   HvRank* d_rank = nullptr;  // heavy-rank table, (n + 31) / 32 words (big graphs only)
-  int* d_hcol = nullptr;     // heavy colours by rank (compact K1HW)
+  int* d_hcol = nullptr;     // heavy colours by rank (compact K1HW); inside d_rank's allocation,
+                             //   so that one L2 persisting window covers both
+  size_t compact_bytes = 0;  // rank table + padding + heavy colours
 };
 
 }  // namespace
@@ -716,8 +718,13 @@ int get_class(gcol_cuda_graph* g, int T, ClassPlan** out) {
     P.nh = nh;
     GCOL_CK(dalloc(&P.d_rows, static_cast<size_t>(nh), g->stream));
     if (colours_beyond_l2(g) && nh > 0) {  // the compact waiting heavy pass will want them
-      GCOL_CK(dalloc(&P.d_rank, static_cast<size_t>((g->n + 31) / 32), g->stream));
-      GCOL_CK(dalloc(&P.d_hcol, static_cast<size_t>(nh), g->stream));
+      const size_t words = static_cast<size_t>((g->n + 31) / 32);
+      const size_t rank_bytes = (words * sizeof(HvRank) + 255) & ~size_t{255};
+      P.compact_bytes = rank_bytes + sizeof(int) * static_cast<size_t>(nh);
+      unsigned char* base = nullptr;
+      GCOL_CK(dalloc(&base, P.compact_bytes, g->stream));
+      P.d_rank = reinterpret_cast<HvRank*>(base);
+      P.d_hcol = reinterpret_cast<int*>(base + rank_bytes);
     }
     if (nh > 0) k_class_write<<<nb, kBlock, 0, g->stream>>>(g->d_off, n, T, d_cnt, P.d_rows, P.d_rank);
     GCOL_CK(cudaGetLastError());
@@ -884,7 +891,8 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls, bool waiting) {
 // persisting access-policy window over it (GCOL_L2_PERSIST=0 disables).
 // Every colour gather of the passes goes to it; the CSR streams past with
 // evict_first.  Returns false when the device offers no persisting L2.
-bool colour_window(gcol_cuda_graph* g, cudaAccessPolicyWindow* w) {
+bool colour_window(gcol_cuda_graph* g, cudaAccessPolicyWindow* w, const void* compact_base = nullptr,
+                   size_t compact_bytes = 0) {
   static const int on = env_int("GCOL_L2_PERSIST", 1, 0, 1);
   if (!on) return false;
   int maxp = 0, maxw = 0;
@@ -899,8 +907,10 @@ bool colour_window(gcol_cuda_graph* g, cudaAccessPolicyWindow* w) {
     }
     limit_set = true;
   }
-  const size_t bytes = std::min<size_t>(sizeof(int) * static_cast<size_t>(g->n), static_cast<size_t>(maxw));
-  w->base_ptr = g->d_colors;
+  // compact variant: what the gathers read is the rank table and the heavy colours
+  const size_t want = compact_base ? compact_bytes : sizeof(int) * static_cast<size_t>(g->n);
+  const size_t bytes = std::min<size_t>(want, static_cast<size_t>(maxw));
+  w->base_ptr = compact_base ? const_cast<void*>(compact_base) : static_cast<void*>(g->d_colors);
   w->num_bytes = bytes;
   w->hitRatio = static_cast<float>(std::min(1.0, static_cast<double>(maxp) / static_cast<double>(bytes)));
   w->hitProp = cudaAccessPropertyPersisting;
@@ -946,7 +956,8 @@ int add_class_nodes(gcol_cuda_graph* g, cudaGraph_t graph, cudaGraphNode_t dep, 
   GCOL_CK(cudaGraphAddKernelNode(&n_l, graph, &n_evh, 1, &p));
   GCOL_CK(cudaGraphKernelNodeSetAttribute(n_l, cudaLaunchAttributeCooperative, &coop));
   cudaLaunchAttributeValue apw{};
-  if (colour_window(g, &apw.accessPolicyWindow)) {
+  const bool cw = C.H.hcol != nullptr;
+  if (colour_window(g, &apw.accessPolicyWindow, cw ? CP->d_rank : nullptr, cw ? CP->compact_bytes : 0)) {
     GCOL_CK(cudaGraphKernelNodeSetAttribute(n_h, cudaLaunchAttributeAccessPolicyWindow, &apw));
     GCOL_CK(cudaGraphKernelNodeSetAttribute(n_l, cudaLaunchAttributeAccessPolicyWindow, &apw));
   }
@@ -2070,8 +2081,7 @@ int gcol_cuda_graph_destroy(gcol_cuda_graph* g) {
   }
   for (auto& kv : g->splits) free_split(g, kv.second);
   for (auto& kv : g->classes)
-    for (void* p : {static_cast<void*>(kv.second.d_rows), static_cast<void*>(kv.second.d_rank),
-                    static_cast<void*>(kv.second.d_hcol)})
+    for (void* p : {static_cast<void*>(kv.second.d_rows), static_cast<void*>(kv.second.d_rank)})
       if (p && g->stream) cudaFreeAsync(p, g->stream);
   if (g->stream) {
     if (g->owns_csr) {
