@@ -968,6 +968,12 @@ int add_class_nodes(gcol_cuda_graph* g, cudaGraph_t graph, cudaGraphNode_t dep, 
 // The same two passes launched eagerly on the library stream.
 int launch_class_eager(gcol_cuda_graph* g, ClassLaunch& C) {
   ClassPlan* CP = &g->classes[class_threshold()];
+  // the same L2 persisting window as the graph's kernel nodes, as a stream attribute
+  cudaStreamAttrValue apw{};
+  const bool cw = C.H.hcol != nullptr;
+  const bool windowed =
+      colour_window(g, &apw.accessPolicyWindow, cw ? CP->d_rank : nullptr, cw ? CP->compact_bytes : 0);
+  if (windowed) GCOL_CK(cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &apw));
   k_mark_pending<<<g->sms * 4, kBlock, 0, g->stream>>>(CP->d_rows, CP->nh, g->d_colors, C.H.hcol);
   GCOL_CK(cudaGetLastError());
   {
@@ -983,6 +989,10 @@ int launch_class_eager(gcol_cuda_graph* g, ClassLaunch& C) {
                   &C.light.L, &C.light.W};
   GCOL_CK(cudaLaunchCooperativeKernel(C.light.wfn, dim3(C.light.grid1), dim3(kWaitBlock), args, 0,
                                       g->stream));
+  if (windowed) {
+    apw.accessPolicyWindow.num_bytes = 0;  // the kernels after the passes: no window
+    GCOL_CK(cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &apw));
+  }
   return GCOL_OK;
 }
 
