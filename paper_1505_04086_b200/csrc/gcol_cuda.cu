@@ -31,7 +31,6 @@
 #include "gcol_kernels.cuh"
 #include "gcol_k1w.cuh"
 #include "gcol_k1c.cuh"
-#include "gcol_k1h2.cuh"
 #include "gcol_k1hw.cuh"
 #include "gcol_round1.cuh"
 
@@ -598,7 +597,7 @@ bool colours_beyond_l2(const gcol_cuda_graph* g) {
 bool heavy_pass_waits(const gcol_cuda_graph* g, int k1_wide) {
   static const int v = env_int("GCOL_K1H_V", 0, 0, 3);
   if (v == 3) return true;
-  if (v == 1 || v == 2) return false;
+  if (v == 1) return false;
   if (k1_wide == 5) return false;
   if (k1_wide == 6) return true;
   return colours_beyond_l2(g);
@@ -744,23 +743,12 @@ struct ClassLaunch {
   HeavyArgs H{};
   const SplitPlan* plan = nullptr;
   int nregions = 0;
-  // the heavy kernel of this launch: k1_heavy (default) or k1_heavy2 (GCOL_K1H_V=2)
+  // the heavy kernel of this launch: k1_heavy (speculative) or k1_heavy_wait
   const void* hfn = nullptr;
   int hthreads = 0;
   size_t hsmem = 0;
   int publishers = 0;  // warps that may publish pieces (SplitArgs::alive starts here)
 };
-
-// GCOL_K1H_V: 1 = k1_heavy (default), 2 = k1_heavy2 (gathers decoupled from
-// the commit order; measured on B200: R-MAT 24 heavy pass 5.9 -> 3.7 ms but
-// 662-667 colours, outside the 1.05 gate of 612 -- the builders' lead is a
-// second in-flight window -- so it stays an experiment); 3 = k1_heavy_wait
-// (gcol_k1hw.cuh: heavy rows wait for their pending lower neighbours, exact
-// First-Fit on the heavy subgraph, no cap on the rows in flight).
-int k1h_version() {
-  static const int v = env_int("GCOL_K1H_V", 1, 0, 3);
-  return v;
-}
 
 const void* k1_light_fn(bool m32, bool stream, bool compact) {
   if (compact) {
@@ -809,13 +797,12 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls, bool waiting) {
     K.W.hcol = CP->d_hcol;
   }
   // heavy pass: one persistent CTA per SM (GCOL_K1H_BPS for experiments)
-  const bool v3 = waiting, v2 = !waiting && k1h_version() == 2;
+  const bool v3 = waiting;
   C->hfn = v3   ? (compact ? reinterpret_cast<const void*>(k1_heavy_wait<PairLog, true>)
                            : reinterpret_cast<const void*>(k1_heavy_wait<PairLog, false>))
-           : v2 ? reinterpret_cast<const void*>(k1_heavy2<PairLog>)
                 : reinterpret_cast<const void*>(k1_heavy<PairLog>);
-  C->hthreads = v3 ? kHwThreads : v2 ? kH2Threads : kHvThreads;
-  C->hsmem = v3 ? kHwSmem : v2 ? kH2Smem : kHvSmem;
+  C->hthreads = v3 ? kHwThreads : kHvThreads;
+  C->hsmem = v3 ? kHwSmem : kHvSmem;
   GCOL_CK(cudaFuncSetAttribute(C->hfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(C->hsmem)));
   int hocc = 1;
@@ -847,17 +834,7 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls, bool waiting) {
                    env_int("GCOL_K1H_RECHECK", 1, 0, 1), P->d_ctr + 3,
                    std::getenv("GCOL_K1_PROFILE") ? 1 : 0, static_cast<long long>(g->m),
                    env_int("GCOL_K1H_PIECEW", pw_default, 1, kHvPieceWarps), g->d_ready, g->piece_shift,
-                   0, 0, 0, 0};
-  if (v2) {
-    // k1_heavy2: commit warps (the colour-quality knob), build warps (latency
-    // hiding), piece warps; ring = how far the builders may run ahead
-    C->H.commit_warps = env_int("GCOL_K1H_CW", 4, 1, 8);
-    C->H.piece_warps = env_int("GCOL_K1H_PIECEW", 8, 1, kHvPieceWarps);
-    C->H.build_warps = env_int("GCOL_K1H_BW", kH2Warps - C->H.commit_warps - C->H.piece_warps, 1,
-                               kH2Warps - C->H.commit_warps - C->H.piece_warps);
-    C->H.ring = env_int("GCOL_K1H_RING", kH2Ring, 4, kH2Ring);
-    C->H.polls = env_int("GCOL_K1H_POLLS", 0, 0, 1 << 20);
-  }
+                   0};
   if (v3) {
     // k1_heavy_wait: row warps fill the SM (the window no longer touches the
     // colour count), piece warps serve the split rows; polls = the guard
@@ -873,7 +850,7 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls, bool waiting) {
       C->H.hcol = CP->d_hcol;
     }
   }
-  C->publishers = C->grid_h * (v2 ? C->H.commit_warps : C->H.row_warps);
+  C->publishers = C->grid_h * C->H.row_warps;
   // log slices: [0, grid_h) heavy CTAs (15/16 of the log: K1H logs its stale
   // reads), then the light CTAs (K1L logs only reads whose wait timed out)
   C->nregions = C->grid_h + K.grid1;
@@ -2264,21 +2241,6 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
                  "polls per row | piece warps: %.0f cycles per piece (pop %.0f, TMA wait %.0f, gathers "
                  "%.0f, finish %.0f), busy %.1f%% | rows %llu pieces %llu\n",
                  P[0] / r, P[1] / r, P[2] / r, P[3] / r, P[8] / r, P[4] / r,
-                 (P[9] + P[10] + P[11] + P[12]) / pcs, P[12] / pcs, P[9] / pcs, P[10] / pcs,
-                 P[11] / pcs,
-                 100.0 * (P[9] + P[10] + P[11] + P[12]) /
-                     std::max(1.0, static_cast<double>(P[9] + P[10] + P[11] + P[12] + P[5])),
-                 static_cast<unsigned long long>(P[6]), static_cast<unsigned long long>(P[7]));
-  } else if (std::getenv("GCOL_K1_PROFILE") && class_run && k1h_version() == 2) {
-    const unsigned long long* P = hdr.prof;
-    const double r = std::max(1.0, static_cast<double>(P[6]));
-    const double pcs = std::max(1.0, static_cast<double>(P[7]));
-    std::fprintf(stderr,
-                 "[k1h2 profile] per row: commit warps wait %.0f + commit %.0f cycles; build warps wait "
-                 "%.0f + build %.0f | pending kept %.3f per row, still pending at the last look %.4f | "
-                 "piece warps: %.0f cycles per piece (pop %.0f, TMA wait %.0f, gathers %.0f, finish "
-                 "%.0f), busy %.1f%% | rows %llu pieces %llu\n",
-                 P[0] / r, P[1] / r, P[2] / r, P[3] / r, P[4] / r, P[8] / r,
                  (P[9] + P[10] + P[11] + P[12]) / pcs, P[12] / pcs, P[9] / pcs, P[10] / pcs,
                  P[11] / pcs,
                  100.0 * (P[9] + P[10] + P[11] + P[12]) /

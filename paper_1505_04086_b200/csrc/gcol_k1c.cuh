@@ -107,10 +107,10 @@ struct HeavyArgs {
   int piece_warps;    // active piece warps per CTA (1 .. kHvPieceWarps)
   const unsigned* piece_ready;  // streamed upload: flag per 2^piece_shift adjacency
   int piece_shift;              //   entries resident (null: the whole CSR is resident)
-  // k1_heavy2 (gcol_k1h2.cuh): warps per role, ring slots, extra last-look polls
-  int commit_warps, build_warps, ring, polls;
-  // k1_heavy_wait (gcol_k1hw.cuh): per split-row slot, INT_MAX - the position of the
+  // k1_heavy_wait (gcol_k1hw.cuh): polls without progress before a row colours past what
+  // is still pending; per split-row slot, INT_MAX - the position of the
   // first entry a piece read as pending (0: none); zeroed before every run
+  int polls;
   unsigned* slot_pend;
   // compact variant of k1_heavy_wait: rank table and the heavy colours by rank
   // (-2 pending); every commit writes both this array and the colour array
@@ -118,10 +118,12 @@ struct HeavyArgs {
   int* hcol;
 };
 
-// K1H colour reads and writes.  (A compact heavy-colour array indexed through
-// a rank table was measured and removed: two dependent loads per gather lost
-// on both R-MAT configs, and even switched off its branch in these helpers
-// kept the compiler from batching the gathers -- R-MAT 24 K1H 4.4 -> 5.9 ms.)
+// K1H colour reads and writes.  (A compact heavy-colour array behind a rank
+// table, as a run-time option of THIS pass, was measured and removed: two
+// dependent loads per gather lost in a window-limited pass, and even switched
+// off its branch in these helpers kept the compiler from batching the gathers
+// -- R-MAT 24 K1H 4.4 -> 5.9 ms.  The waiting pass has it as a compile-time
+// variant, gcol_k1hw.cuh.)
 __device__ __forceinline__ int hv_gather(const HeavyArgs&, const int* colors, int w) {
   return hv_ld_color(colors + w);
 }

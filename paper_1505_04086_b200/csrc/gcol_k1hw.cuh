@@ -1,5 +1,5 @@
 // gcol_k1hw.cuh -- K1HW: the WAITING heavy pass of the class split
-// (GCOL_K1H_V=3; gcol_k1c.cuh holds k1_heavy and everything shared).
+// (k1_wide 6, or chosen by graph size; gcol_k1c.cuh holds k1_heavy and everything shared).
 //
 // Same place in the pass as k1_heavy: heavy rows (degree >= T) in ascending id
 // order, each First-Fit over its LOWER heavy neighbours, before the light pass
