@@ -392,7 +392,10 @@ __device__ __forceinline__ void hw_piece(const long long* __restrict__ off, cons
     atomicMax(H.slot_pend + slot, (unsigned)(INT_MAX - ((int)(r.a - b) + pmin)));
   }
   __syncwarp();
-  if (lane == 0) atom_add_acq_rel(S.slot_left + slot, -1);
+  // nobody needs the old value (the owner polls the count): a release reduction, so the
+  // warp moves on to its next piece without waiting for the round trip
+  if (lane == 0)
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(S.slot_left + slot), "r"(-1) : "memory");
   hv_tick(H.prof, t_last, pp[2]);
 }
 
@@ -404,6 +407,7 @@ __global__ void __launch_bounds__(kHwThreads, 1)
   auto s_pbuf = reinterpret_cast<int(*)[kHvPieceBuf]>(k1hw_raw);
   __shared__ unsigned s_win[kHwWarps][32];
   __shared__ unsigned long long s_pbar[kHvPieceWarps];
+  __shared__ __align__(16) int4 s_brec[kHwBufs][kHwBatch];  // the claimed batches' table records
   __shared__ int s_bgb[kHwBufs], s_btag[kHwBufs];
   __shared__ int s_ticket, s_npairs, s_mbhead;
   __shared__ unsigned s_gathers;
@@ -450,23 +454,32 @@ __global__ void __launch_bounds__(kHwThreads, 1)
       if (lane == 0) t = atomicAdd(&s_ticket, 1);
       t = __shfl_sync(kFull, t, 0);
       const int lb = t / kHwBatch, p = t % kHwBatch, bb = lb % kHwBufs;
-      long long r = 0;
-      if (lane == 0) {
-        if (p == 0) {
+      if (p == 0) {
+        // the claimer also brings the batch's table records (one 128-byte line)
+        // into shared memory, so the other seven rows start without that miss
+        int gb = 0;
+        if (lane == 0) {
           if (lb > 0)
             while (ld_acquire_cta_s32(&s_btag[(lb - 1) % kHwBufs]) != lb - 1) {
             }
-          s_bgb[bb] = (int)atomicAdd(H.cursor, 1u);
-          st_release_cta_s32(&s_btag[bb], lb);
-        } else {
+          gb = (int)atomicAdd(H.cursor, 1u);
+          s_bgb[bb] = gb;
+        }
+        gb = __shfl_sync(kFull, gb, 0);
+        const long long rr = (long long)gb * kHwBatch + lane;
+        if (lane < kHwBatch && rr < H.nh)
+          s_brec[bb][lane] = __ldg(reinterpret_cast<const int4*>(H.rows + rr));
+        __syncwarp();
+        if (lane == 0) st_release_cta_s32(&s_btag[bb], lb);
+      } else {
+        if (lane == 0)
           while (ld_acquire_cta_s32(&s_btag[bb]) != lb) {
           }
-        }
-        r = (long long)s_bgb[bb] * kHwBatch + p;
+        __syncwarp();
       }
-      r = __shfl_sync(kFull, r, 0);
+      const long long r = (long long)s_bgb[bb] * kHwBatch + p;
       if (r >= H.nh) break;
-      const int4 q = __ldg(reinterpret_cast<const int4*>(H.rows + r));
+      const int4 q = s_brec[bb][p];
       HeavyRow e0;
       e0.b = ((long long)(unsigned)q.y << 32) | (unsigned)q.x;
       e0.v = q.z;
