@@ -409,10 +409,14 @@ def run_ours(args):
     achieved = k1_bytes / k1_mean / 1e9
     peak, peak_src = measured_peak()
     traffic = profile_traffic(args.config)
-    # the class split's heavy pass: the library's rule (gcol_cuda.cu heavy_pass_waits) --
-    # waiting once the colour array no longer fits L2, GCOL_K1H_V overriding
+    # the class split's heavy pass: the library's rule (gcol_cuda.cu heavy_pass_variant) --
+    # the waiting pass: exact with compact colours once the colour array no longer fits L2,
+    # with a short poll budget otherwise; GCOL_K1H_V=1 selects the speculative k1_heavy
     hv = os.environ.get("GCOL_K1H_V", "0")
-    heavy_kernel = "k1_heavy_wait" if (hv == "3" or (hv == "0" and 4 * n > (64 << 20))) else "k1_heavy"
+    big = 4 * n > (64 << 20)
+    heavy_kernel = ("k1_heavy" if hv == "1" else
+                    "k1_heavy_wait<compact>" if big else
+                    "k1_heavy_wait" + ("" if hv == "3" else " (short poll budget)"))
     kname = ("k1_wait" if maxdeg <= 63 else
              f"k_mark_pending + {heavy_kernel} + k1_wait<light> (class split)" if class_split else "k1_pipe")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -98,8 +98,10 @@ typedef struct {
   int32_t k1_wide;           /* initial-pass kernel: 0 auto (the waiting pass K1W when every
                                 row has degree <= 63, else the class-split pass K1H + K1L),
                                 1 narrow k1_pipe (8 consumer warps per SM), 2 wide k1_pipe
-                                (16), 3 K1W where it applies, 4 class split (heavy pass chosen
-                                by graph size), 5 class split with the speculative heavy pass,
+                                (16), 3 K1W where it applies, 4 class split (waiting heavy pass: exact
+                                once the colour array exceeds L2, else with a short budget of
+                                polls after which a row colours past a pending neighbour and the
+                                rounds repair it), 5 class split with the speculative heavy pass,
                                 6 class split with the waiting heavy pass (the result is then
                                 sequential First-Fit in the order "rows of degree >= 64
                                 ascending, then the others ascending", bit for bit) */

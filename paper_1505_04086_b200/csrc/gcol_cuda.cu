@@ -573,17 +573,28 @@ int env_int(const char* name, int dflt, int lo, int hi) {
   return e ? std::max(lo, std::min(hi, std::atoi(e))) : dflt;
 }
 
-// Heavy pass of the class split: waiting (k1_heavy_wait, gcol_k1hw.cuh) or
-// speculative (k1_heavy, gcol_k1c.cuh).  Option k1_wide 5 forces the
-// speculative pass, 6 the waiting one; GCOL_K1H_V=1/3 overrides for A/B.
-// Automatic choice, measured on B200: the waiting pass is
-// bound by the longest chain of adjacent heavy rows with ascending ids
-// (R-MAT 24: 4914 rows at ~1.3 us per hop = 6.5 ms, against 4.4 ms for the
-// speculative pass and its 1.2 ms of rounds), the speculative one by the
-// small window its colour quality allows; once the colour array no longer
-// fits L2 every gather pays HBM latency and only the waiting pass can keep
-// enough rows in flight (R-MAT 27: 32.0 against 34.6 ms, one round instead of
-// eleven, 957 colours -- serial First-Fit's count -- instead of ~1010).
+// Heavy pass of the class split, measured on B200:
+//   3  speculative (k1_heavy, gcol_k1c.cuh): a small in-flight window keeps
+//      the hubs from colliding; rounds repair what collides.  R-MAT 24:
+//      6.2 ms, ~585 colours, ~20 rounds.
+//   4  waiting, exact (k1_heavy_wait, gcol_k1hw.cuh): First-Fit on the heavy
+//      subgraph bit for bit, one round.  Bound by the longest chain of
+//      adjacent heavy rows with ascending ids when the gathers are cheap
+//      (R-MAT 24: 4914 rows, 5.7-7.1 ms by box) and by the gathers when they
+//      are not (R-MAT 27: 32.3 ms against 45.5 speculative).
+//   5  waiting with a small budget of polls without progress (kHwShortPolls):
+//      a row stuck behind the chain colours past what is still pending and
+//      logs it -- the few conflicts this leaves are between chain rows and a
+//      handful of rounds repairs them.  R-MAT 24: 4.8 ms, 532-539 colours
+//      (serial First-Fit 531), 3-8 rounds; budget 4: 4.7 ms / ~548 / 11-15,
+//      8: 5.0 ms / ~531 / 3, 16: 5.7 ms.  On R-MAT 27 a budget only adds
+//      rounds (8: 34.5 ms, 32: 33.5 ms, exact 32.3 ms).
+// Choice: option k1_wide 5 forces the speculative pass, 6 the exact waiting
+// one (k1_wait_polls then bounds it); 4 and 0 take the exact waiting pass
+// with compact colours once the colour array exceeds L2, else the short
+// budget (or k1_wait_polls when given).  GCOL_K1H_V=1/3 override for A/B.
+constexpr int kHwShortPolls = 6;
+
 // The colour array no longer fits L2 (B200: 126 MB, about half usable for it
 // next to the streaming CSR).  GCOL_L2_COLOURS_MB moves the limit (tests use
 // 0 to run the big-graph path -- waiting heavy pass, compact colours -- on
@@ -594,26 +605,27 @@ bool colours_beyond_l2(const gcol_cuda_graph* g) {
   return sizeof(int) * static_cast<size_t>(g->n) > (mb << 20);
 }
 
-bool heavy_pass_waits(const gcol_cuda_graph* g, int k1_wide) {
+int heavy_pass_variant(const gcol_cuda_graph* g, int k1_wide) {
   static const int v = env_int("GCOL_K1H_V", 0, 0, 3);
-  if (v == 3) return true;
-  if (v == 1) return false;
-  if (k1_wide == 5) return false;
-  if (k1_wide == 6) return true;
-  return colours_beyond_l2(g);
+  if (v == 3) return 4;
+  if (v == 1) return 3;
+  if (k1_wide == 5) return 3;
+  if (k1_wide == 6) return 4;
+  return colours_beyond_l2(g) ? 4 : 5;
 }
 
 // K1 variant of the in-place initial pass: 0 narrow, 1 wide, 2 K1W (the
-// waiting pass, gcol_k1w.cuh; rows of degree <= kSmallMax only), 3 / 4 the
-// class split with the speculative / waiting heavy pass.  Option k1_wide:
+// waiting pass, gcol_k1w.cuh; rows of degree <= kSmallMax only), 3 / 4 / 5 the
+// class split with the speculative / waiting / short-budget waiting heavy
+// pass.  Option k1_wide:
 // 0 auto (K1W when every row is small, else the class split), 1 narrow,
 // 2 wide, 3 K1W, 4 class split, 5 / 6 class split with the heavy pass forced.
 int k1_variant(const gcol_cuda_graph* g, int k1_wide) {
   const bool small = g->max_degree <= kSmallMax;
   if (k1_wide == 3 && small) return 2;
   if (k1_wide == 0 && small) return 2;
-  if ((k1_wide == 0 || (k1_wide >= 4 && k1_wide <= 6)) && !small)  // class split: 3 or 4
-    return heavy_pass_waits(g, k1_wide) ? 4 : 3;
+  if ((k1_wide == 0 || (k1_wide >= 4 && k1_wide <= 6)) && !small)  // class split: 3, 4 or 5
+    return heavy_pass_variant(g, k1_wide);
   return use_wide(g, k1_wide >= 3 ? 0 : k1_wide) ? 1 : 0;
 }
 
@@ -765,7 +777,8 @@ const void* k1_light_fn(bool m32, bool stream, bool compact) {
              : reinterpret_cast<const void*>(k1_wait<false, false, true>);
 }
 
-int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls, bool waiting) {
+int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls, int variant) {
+  const bool waiting = variant >= 4;
   const int T = class_threshold();
   ClassPlan* CP = nullptr;
   if (int rc = get_class(g, T, &CP)) return rc;
@@ -843,7 +856,9 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls, bool waiting) {
     // the guard: polls without progress before a row colours past what is
     // still pending (option k1_wait_polls; its default becomes 2^22 here -- a
     // row may wait for most of the pass behind a long chain, ~0.5 us a poll)
-    C->H.polls = env_int("GCOL_K1H_POLLS", polls == kWaitPollsDefault ? 1 << 22 : polls, 0, 1 << 30);
+    // ... unless this is the short-budget variant (heavy_pass_variant)
+    const int dflt = variant == 5 ? kHwShortPolls : 1 << 22;
+    C->H.polls = env_int("GCOL_K1H_POLLS", polls == kWaitPollsDefault ? dflt : polls, 0, 1 << 30);
     C->H.slot_pend = P->d_q_seq;
     if (compact) {
       C->H.rank = CP->d_rank;
@@ -1110,7 +1125,7 @@ int build_rsoc_graph(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, 
   ClassLaunch CL;
   const bool cls = kLower && k1v >= 3;
   if (cls) {
-    if (int rc = plan_k1_class(g, &CL, polls, k1v == 4)) return rc;
+    if (int rc = plan_k1_class(g, &CL, polls, k1v)) return rc;
   } else if (kLower && k1v == 2) {
     if (int rc = plan_k1_wait(g, &K, polls)) return rc;
   } else if (int rc = plan_k1<false, kLower, true>(g, k1_blocks, split_min, &K, k1v == 1)) {
@@ -1239,7 +1254,7 @@ int run_eager(gcol_cuda_graph* g, int k1_blocks, int split_min, int k1v, int pol
   ClassLaunch CL;
   const bool cls = kLower && k1v >= 3;
   if (cls) {
-    if (int rc = plan_k1_class(g, &CL, polls, k1v == 4)) return rc;
+    if (int rc = plan_k1_class(g, &CL, polls, k1v)) return rc;
     if (int rc = reset_split(g, CL.plan, CL.publishers)) return rc;
     GCOL_CK(cudaEventRecord(g->ev_start, g->stream));
     if (int rc = launch_class_eager(g, CL)) return rc;
@@ -2231,7 +2246,7 @@ int gcol_cuda_color_rsoc(gcol_cuda_graph* g, const gcol_cuda_options* opt_in, in
     }
   const int rounds = hdr.round;
   const bool class_run = (exec && g->exec_class[exec]) || (eager && lower && wide >= 3);
-  if (std::getenv("GCOL_K1_PROFILE") && class_run && wide == 4) {
+  if (std::getenv("GCOL_K1_PROFILE") && class_run && wide >= 4) {
     const unsigned long long* P = hdr.prof;
     const double r = std::max(1.0, static_cast<double>(P[6]));
     const double pcs = std::max(1.0, static_cast<double>(P[7]));
