@@ -851,7 +851,9 @@ int plan_k1_class(gcol_cuda_graph* g, ClassLaunch* C, int polls, int variant) {
   if (v3) {
     // k1_heavy_wait: row warps fill the SM (the window no longer touches the
     // colour count), piece warps serve the split rows; polls = the guard
-    C->H.piece_warps = env_int("GCOL_K1H_PIECEW", 8, 1, kHvPieceWarps);
+    // (R-MAT 27, compact: pieces 85 % busy at 16 + 8; R-MAT 24 at the short budget: pieces
+    // 47 % busy at 16 + 8, 18 + 6 is 4.5 % faster, 20 + 4 no better)
+    C->H.piece_warps = env_int("GCOL_K1H_PIECEW", variant == 5 ? 6 : 8, 1, kHvPieceWarps);
     C->H.row_warps = env_int("GCOL_K1H_ROWW", kHwWarps - C->H.piece_warps, 1, kHwWarps - C->H.piece_warps);
     // the guard: polls without progress before a row colours past what is
     // still pending (option k1_wait_polls; its default becomes 2^22 here -- a
